@@ -1,0 +1,172 @@
+/* pcb200.h — C ABI of the B200-native Paillier / 3P-ADMM-PC2 hot path.
+ *
+ * This is the drop-in boundary.  The reference has no FFI: its seam is the C++ class
+ * pcadmm::Paillier (/root/reference/proj/include/pcadmm/paillier.hpp:104-181) and the quantizer
+ * free functions (quantize.hpp:32-71).  Each entry point below names the reference member it
+ * replaces.  The C++ facade (paper_2601_14980_b200/csrc/host/pcb200.hpp) and the Python package
+ * re-expose the reference signatures on top of these calls; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *   - Big integers are fixed-width little-endian uint32 limb arrays.  For a context with an
+ *     L-limb modulus n (L = pcb_ctx_n_limbs):  plaintexts and r use L limbs (or a narrower
+ *     m_limbs for quantized plaintexts), ciphertexts use 2L limbs.  Batches are AoS:
+ *     element i occupies [i*width, (i+1)*width).
+ *   - Pointers may be device pointers (stream-ordered, no hidden copies) or host pointers
+ *     (staged through device scratch; the call synchronises the stream before returning).
+ *   - Exceptions of the reference become pcb_status values; batched calls also write one int32
+ *     status per element (nullable) so a single bad element does not hide the others.
+ *   - There is no CPU fallback: without a CUDA device every compute call returns PCB_E_CUDA.
+ *   - Thread-safety: one context may be used from several host threads on distinct streams.
+ */
+#ifndef PCB200_H
+#define PCB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pcb_ctx pcb_ctx;
+typedef struct CUstream_st* pcb_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  PCB_OK = 0,
+  PCB_E_PLAINTEXT_RANGE = 1,  /* m >= n            invalid_argument  paillier.cpp:242        */
+  PCB_E_RANDOMNESS_RANGE = 2, /* r == 0 or r >= n  invalid_argument  paillier.cpp:322-323    */
+  PCB_E_CIPHER_RANGE = 3,     /* c >= n^2          invalid_argument  paillier.cpp:348,356    */
+  PCB_E_NOT_UNIT = 4,         /* gcd(c,n) != 1     runtime_error     paillier.cpp:34-41      */
+  PCB_E_OVERFLOW = 5,         /* plain_bits guard  overflow_error    paillier.cpp:245-251    */
+  PCB_E_NO_PRIVATE = 6,       /* private op on a public-only context   logic_error             */
+  PCB_E_SHAPE = 7,            /* bad sizes/window/key size              invalid_argument        */
+  PCB_E_UNSUPPORTED = 8,      /* valid request this build does not implement (e.g. random g)    */
+  PCB_E_CUDA = 9,             /* CUDA runtime error or no device                                  */
+  PCB_E_ALLOC = 10,           /* device/host allocation failed                                    */
+  PCB_E_RANGE_UPDATE = 11     /* decrypted ADMM update out of range: ProtocolError protocol.cpp:20-27 */
+} pcb_status;
+
+/* ---- keys (host; one-time work) ------------------------------------------ */
+
+/* pcadmm::keygen(Rng&, key_bits, GMode::binomial) — paillier.cpp:106-123, bit-exact including
+ * the splitmix64 stream consumption.  *rng_state is the Rng::state before/after.  key_bits must
+ * be 64, 1024, 2048 or 4096 (the reference's accepted set).  n gets key_bits/32 limbs (64-bit:
+ * 2), p and q get half of that. */
+pcb_status pcb_keygen(uint64_t* rng_state, uint32_t key_bits, uint32_t* n, uint32_t* p, uint32_t* q);
+
+/* pcadmm::random_prime(Rng&, bits, 40) — bignat.cpp:497-515 (used for 3072-bit keys via
+ * keypair_from_primes).  out gets ceil(bits/32) limbs. */
+pcb_status pcb_random_prime(uint64_t* rng_state, uint32_t bits, uint32_t* out);
+
+/* ---- context ------------------------------------------------------------------------------ */
+
+/* Builds the per-key device constants (Montgomery contexts for p^2, q^2, p, q, n^2, exponent
+ * window schedules, CRT factors).  Replaces Paillier(KeyPair) / Paillier(PublicKey)
+ * (paillier.cpp:193-212).  p and q (pq_limbs each) may be NULL for a public-key-only context
+ * (the edge role).  binomial g = n+1 only (the reference default, GMode::binomial). */
+pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t n_limbs,
+                          const uint32_t* p, const uint32_t* q, uint32_t pq_limbs);
+void pcb_ctx_destroy(pcb_ctx* ctx);
+uint32_t pcb_ctx_n_limbs(const pcb_ctx* ctx);   /* L: limb width of plaintexts and r       */
+uint32_t pcb_ctx_n_bits(const pcb_ctx* ctx);    /* bit length of n (plain_bits guard bound) */
+int pcb_ctx_has_private(const pcb_ctx* ctx);
+/* Copies n (L limbs) / n^2 (2L limbs) out of the context. */
+pcb_status pcb_ctx_get_n(const pcb_ctx* ctx, uint32_t* n, uint32_t* n2);
+/* Exponentiation ledger, pcadmm::OpCount (paillier.hpp:84-87): same counting rules as the
+ * reference (pow_half per p^2/q^2 exponentiation, pow_full per n^2 exponentiation/matvec row). */
+void pcb_ctx_counters(const pcb_ctx* ctx, uint64_t* pow_full, uint64_t* pow_half);
+void pcb_ctx_reset_counters(pcb_ctx* ctx);
+
+/* ---- randomness ---------------------------------------------------------------------------- */
+
+/* count x Paillier::sample_r(rng) — paillier.cpp:233-239 with bignat.cpp:388-445: splitmix64
+ * words, rejection until 0 < r < n, gcd(r, n) == 1.  Generated on the GPU from the counter form
+ * of splitmix64 and stream-compacted, so r_out and the final *rng_state are identical to the
+ * reference's serial draw loop (paillier.cpp:499-500). */
+pcb_status pcb_sample_r(pcb_ctx* ctx, uint64_t* rng_state, size_t count, uint32_t* r_out,
+                        pcb_stream stream);
+
+/* ---- encryption / decryption -------------------------------------------------------------- */
+
+/* c_i = (1 + m_i n) r_i^n mod n^2.
+ *   use_crt = 1: Paillier::crt_encrypt_with_r (paillier.cpp:334-344), needs p, q;
+ *   use_crt = 0: Paillier::encrypt_with_r     (paillier.cpp:320-328), public key only.
+ * m: count x m_limbs (m_limbs <= L), r: count x L, c: count x 2L. */
+pcb_status pcb_encrypt(pcb_ctx* ctx, const uint32_t* m, uint32_t m_limbs, const uint32_t* r,
+                       size_t count, uint32_t* c, int use_crt, int32_t* status, pcb_stream stream);
+
+/* m_i = L(c_i^eps mod n^2) mu mod n.
+ *   use_crt = 1: Paillier::crt_decrypt (paillier.cpp:354-361);  use_crt = 0: decrypt (346-352).
+ * Both compute the same residue (c^(p-1) mod p^2 / L_p / h_p form + CRT on the device).
+ * c: count x 2L, m: count x L. */
+pcb_status pcb_decrypt(pcb_ctx* ctx, const uint32_t* c, size_t count, uint32_t* m, int use_crt,
+                       int32_t* status, pcb_stream stream);
+
+/* ---- homomorphic operations (public key suffices) ----------------------------------------- */
+
+/* out_i = a_i * b_i mod n^2 — Paillier::hom_add (paillier.cpp:428-432).  plain_bits tracking
+ * stays on the host (facade), exactly as the reference formula. */
+pcb_status pcb_hom_add(pcb_ctx* ctx, const uint32_t* a, const uint32_t* b, size_t count,
+                       uint32_t* out, pcb_stream stream);
+
+/* out_i = c_i^k_i mod n^2 — Paillier::hom_scalar_mul (paillier.cpp:434-439), k_i < 2^64. */
+pcb_status pcb_hom_scalar_mul(pcb_ctx* ctx, const uint64_t* k, const uint32_t* c, size_t count,
+                              uint32_t* out, pcb_stream stream);
+
+/* out_i = alpha_i * prod_j zv_j^expo[i][j] mod n^2 — Paillier::hom_matvec
+ * (paillier.cpp:441-493).  expo is rows x cols row-major u64; window in [1, 8] selects the
+ * reference's table width (the result does not depend on it). */
+pcb_status pcb_hom_matvec(pcb_ctx* ctx, const uint32_t* alpha, const uint64_t* expo,
+                          const uint32_t* zv, size_t rows, size_t cols, uint32_t window,
+                          uint32_t* out, pcb_stream stream);
+
+/* Edge step (protocol.cpp:264-271): zv_j = z_j * v_j mod n^2 (hom_add), then hom_matvec.
+ * Also range-checks z_j, v_j < n^2 (ProtocolError "ciphertext outside the group"). */
+pcb_status pcb_edge_step(pcb_ctx* ctx, const uint32_t* alpha, const uint64_t* expo,
+                         const uint32_t* zc, const uint32_t* vc, size_t cols, uint32_t window,
+                         uint32_t* out, pcb_stream stream);
+
+/* out = prod_i c_i mod n^2 (balanced reduction tree; order-independent value, SURVEY.md §0
+ * fact 9).  count >= 1. */
+pcb_status pcb_aggregate(pcb_ctx* ctx, const uint32_t* c, size_t count, uint32_t* out,
+                         pcb_stream stream);
+
+/* ---- fused quantize / dequantize (quantize.cpp, FP64 without contraction) ------------------ */
+
+/* Gamma2 (fine = 0, quantize.cpp:31-35) or Gamma1 (fine = 1, 37-41) of count doubles, then
+ * encryption with r (as pcb_encrypt).  q_out (nullable) receives the quantized integers
+ * (u64, or u128 as lo/hi pairs when fine); clamps (nullable, host) receives {low, high}. */
+pcb_status pcb_quantize_encrypt(pcb_ctx* ctx, const double* v, size_t count, double z_min,
+                                double z_max, double delta, int fine, const uint32_t* r,
+                                int use_crt, uint32_t* c, uint64_t* q_out, uint64_t* clamps,
+                                pcb_stream stream);
+
+/* Master block update (protocol.cpp:494-511): decrypt count updates, range-gate them
+ * (check_update_range, protocol.cpp:20-27), inverse_quantize_x (quantize.cpp:84-112) with the
+ * block's Gamma2(B) row sums, then z = S_{lambda/rho}(x + v), v = x + v - z in place.
+ * q_z, q_nv: the Gamma2 integers the block was encrypted from (count each). */
+pcb_status pcb_decrypt_update(pcb_ctx* ctx, const uint32_t* c, size_t count,
+                              const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
+                              double z_min, double z_max, double delta, double kappa, double* x,
+                              double* z, double* v, int32_t* status, pcb_stream stream);
+
+/* ---- generic primitive + measurement ------------------------------------------------------ */
+
+/* y_i = x_i^e mod m for an odd modulus m (m_limbs <= 96) and a batch-uniform exponent e —
+ * the batched ModArith::pow (paillier.cpp:26-30).  Inputs/outputs m_limbs wide. */
+pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t* e, uint32_t e_limbs,
+                            const uint32_t* x, size_t count, uint32_t* y, pcb_stream stream);
+
+/* IMAD roofline microbenchmark on the current device: kind 0 = IMAD.WIDE.U32 chains,
+ * kind 1 = IMAD.LO + IMAD.HI pairs.  Returns MAC32/s (< 0 on error). */
+double pcb_imad_peak(int kind, int iters, float* ms_out);
+
+/* Number of kernels this library has launched (process-wide), for bench.py's gpu_launches. */
+uint64_t pcb_launch_count(void);
+
+const char* pcb_status_str(pcb_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCB200_H */

@@ -1,0 +1,583 @@
+// abi.cu — the C ABI of include/pcb200.h: context construction (per-key constants), host/device
+// pointer staging, dispatch to the templated kernels, error mapping.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <vector>
+
+#include "host/hbn.hpp"
+#include "paillier_params.cuh"
+#include "pcb_internal.h"
+
+namespace pcb {
+
+std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> c{0};
+  return c;
+}
+
+// ---- scratch + staging ----------------------------------------------------------------------
+pcb_status scratch_alloc(size_t bytes, void** p, cudaStream_t st) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  return cudaMallocAsync(p, bytes, st) == cudaSuccess ? PCB_OK : PCB_E_ALLOC;
+}
+void scratch_free(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+pcb_status stage_in(const void* p, size_t bytes, cudaStream_t st, Staged* s) {
+  s->bytes = bytes;
+  if (!p || is_device_ptr(p)) {
+    s->dev = const_cast<void*>(p);
+    s->host = false;
+    return PCB_OK;
+  }
+  s->host = true;
+  if (auto e = scratch_alloc(bytes, &s->dev, st)) return e;
+  return cuda_check(cudaMemcpyAsync(s->dev, p, bytes, cudaMemcpyHostToDevice, st));
+}
+
+pcb_status stage_out(void* p, size_t bytes, cudaStream_t st, Staged* s) {
+  s->bytes = bytes;
+  if (!p || is_device_ptr(p)) {
+    s->dev = p;
+    s->host = false;
+    return PCB_OK;
+  }
+  s->host = true;
+  return scratch_alloc(bytes, &s->dev, st);
+}
+
+pcb_status unstage_out(void* p, Staged* s, cudaStream_t st) {
+  if (!s->host || !p) return PCB_OK;
+  return cuda_check(cudaMemcpyAsync(p, s->dev, s->bytes, cudaMemcpyDeviceToHost, st));
+}
+
+void unstage(Staged* s, cudaStream_t st) {
+  if (s->host && s->dev) scratch_free(s->dev, st);
+  s->dev = nullptr;
+  s->host = false;
+}
+
+// ---- constants ------------------------------------------------------------------------------
+static uint32_t neg_inv32(uint32_t m0) {
+  uint32_t inv = 1;
+  for (int i = 0; i < 5; i++) inv *= 2u - m0 * inv;
+  return 0u - inv;
+}
+
+template <int S>
+static void fill_mod(ModCtx<S>& c, const HBN& m) {
+  std::memset(&c, 0, sizeof(c));
+  m.to_limbs(c.m, S);
+  mod(HBN(1) << (64 * S), m).to_limbs(c.r2, S);
+  c.minv = neg_inv32(c.m[0]);
+}
+
+// Left-to-right sliding window schedule (see mont.cuh).  Window width w, table of the
+// 2^(w-1) odd powers.
+std::vector<uint32_t> build_schedule(const HBN& e, int w) {
+  std::vector<uint32_t> ops;
+  long i = (long)e.bit_length() - 1;
+  bool first = true;
+  uint32_t pending = 0;
+  while (i >= 0) {
+    if (!e.bit((size_t)i)) {
+      pending++;
+      i--;
+      continue;
+    }
+    long j = i - w + 1;
+    if (j < 0) j = 0;
+    while (!e.bit((size_t)j)) j++;
+    uint32_t d = 0;
+    for (long k = i; k >= j; k--) d = (d << 1) | (e.bit((size_t)k) ? 1u : 0u);
+    const uint32_t len = (uint32_t)(i - j + 1);
+    if (first) {
+      ops.push_back((d - 1) / 2);
+      first = false;
+    } else {
+      ops.push_back(((pending + len) << 16) | ((d - 1) / 2));
+    }
+    pending = 0;
+    i = j - 1;
+  }
+  if (pending) ops.push_back((pending << 16) | 0xffffu);
+  return ops;
+}
+
+// Expand the window schedule into the per-product byte stream consumed by mont_pow:
+// ops[0] = seed table index, then kOpSquare per squaring and a table index per multiply.
+std::vector<uint8_t> build_ops(const HBN& e, int w) {
+  std::vector<uint32_t> sch = build_schedule(e, w);
+  std::vector<uint8_t> ops;
+  ops.push_back((uint8_t)(sch[0] & 0xffffu));
+  for (size_t i = 1; i < sch.size(); i++) {
+    const uint32_t nsq = sch[i] >> 16, idx = sch[i] & 0xffffu;
+    ops.insert(ops.end(), nsq, kOpSquare);
+    if (idx != 0xffffu) ops.push_back((uint8_t)idx);
+  }
+  return ops;
+}
+
+constexpr int kWindow = 5;
+constexpr int kTab = 1 << (kWindow - 1);
+
+}  // namespace pcb
+
+using namespace pcb;
+
+struct pcb_ctx {
+  int device = 0;
+  uint32_t L = 0, nbits = 0;
+  bool has_prv = false;
+  int S = 0;   // p^2 / q^2 kernel width
+  int S2 = 0;  // n^2 kernel width
+  HBN n, n2, p, q;
+  std::vector<uint8_t> enc_blob, dec_blob, n2_blob;
+  uint8_t* d_sched = nullptr;  // all exponent op streams, concatenated
+  int off_enc_p = 0, len_enc_p = 0, off_enc_q = 0, len_enc_q = 0;
+  int off_dec_p = 0, len_dec_p = 0, off_dec_q = 0, len_dec_q = 0;
+  int off_pub = 0, len_pub = 0;  // exponent n at n^2 (direct encryption)
+  std::atomic<uint64_t> pow_full{0}, pow_half{0};
+};
+
+namespace pcb {
+// launchers (paillier.cu / n2ops.cu)
+template <int S>
+pcb_status launch_crt_encrypt(const CrtEncConsts<S>& k, Sched sp, Sched sq, int ntab, const uint32_t* m,
+                              int m_limbs, const uint32_t* r, int L, size_t count, uint32_t* c, int32_t* st,
+                              const double* qv, double zmin, double zmax, double delta, int fine, uint64_t* q_out,
+                              unsigned long long* clamps, cudaStream_t stream);
+template <int S>
+pcb_status launch_crt_decrypt(const CrtDecConsts<S>& k, Sched sp, Sched sq, int ntab, const uint32_t* c, int L,
+                              size_t count, uint32_t* m, int32_t* st, cudaStream_t stream);
+}  // namespace pcb
+
+namespace {
+
+template <int S>
+void build_enc(pcb_ctx* x) {
+  CrtEncConsts<S> k;
+  std::memset(&k, 0, sizeof(k));
+  HBN p2 = x->p * x->p, q2 = x->q * x->q;
+  fill_mod<S>(k.mp, p2);
+  fill_mod<S>(k.mq, q2);
+  const HBN R = HBN(1) << (32 * S);
+  mod(x->n * R, p2).to_limbs(k.nRp, S);
+  mod(x->n * R, q2).to_limbs(k.nRq, S);
+  HBN inv;
+  if (!mod_inverse(mod(p2, q2), q2, inv)) throw std::invalid_argument("p and q share a factor");
+  inv.to_limbs(k.inv, S);
+  x->n.to_limbs(k.n, S);
+  x->enc_blob.assign(reinterpret_cast<uint8_t*>(&k), reinterpret_cast<uint8_t*>(&k) + sizeof(k));
+}
+
+template <int S>
+void build_dec(pcb_ctx* x) {
+  constexpr int H = S / 2;
+  CrtDecConsts<S> k;
+  std::memset(&k, 0, sizeof(k));
+  HBN p2 = x->p * x->p, q2 = x->q * x->q;
+  fill_mod<S>(k.mp, p2);
+  fill_mod<S>(k.mq, q2);
+  fill_mod<H>(k.sp, x->p);
+  fill_mod<H>(k.sq, x->q);
+  mod(HBN(1) << (96 * S), p2).to_limbs(k.r3p, S);
+  mod(HBN(1) << (96 * S), q2).to_limbs(k.r3q, S);
+  const HBN RH = HBN(1) << (32 * H);
+  HBN t;
+  if (!mod_inverse(x->p, RH, t)) throw std::invalid_argument("even p");
+  t.to_limbs(k.pinv_lo, H);
+  if (!mod_inverse(x->q, RH, t)) throw std::invalid_argument("even q");
+  t.to_limbs(k.qinv_lo, H);
+  // h_p = L_p(g^(p-1) mod p^2)^-1 mod p with g = n + 1
+  const HBN g = x->n + HBN(1);
+  for (int side = 0; side < 2; side++) {
+    const HBN& pr = side ? x->q : x->p;
+    const HBN& m2 = side ? q2 : p2;
+    HBN xx = pow_mod(g, pr - HBN(1), m2);
+    HBN l, r;
+    divmod(xx - HBN(1), pr, l, r);
+    HBN h;
+    if (!mod_inverse(l, pr, h)) throw std::invalid_argument("degenerate key (h_p)");
+    mod(h * RH, pr).to_limbs(side ? k.hq : k.hp, H);
+  }
+  HBN pinvq;
+  if (!mod_inverse(mod(x->p, x->q), x->q, pinvq)) throw std::invalid_argument("p and q share a factor");
+  pinvq.to_limbs(k.pinvq, H);
+  x->p.to_limbs(k.p, H);
+  x->q.to_limbs(k.q, H);
+  x->n2.to_limbs(k.n2, 2 * S);
+  x->dec_blob.assign(reinterpret_cast<uint8_t*>(&k), reinterpret_cast<uint8_t*>(&k) + sizeof(k));
+}
+
+pcb_status set_device(const pcb_ctx* x) { return cuda_check(cudaSetDevice(x->device)); }
+
+struct StreamSync {
+  cudaStream_t st;
+  bool need;
+  ~StreamSync() {
+    if (need) cudaStreamSynchronize(st);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* pcb_status_str(pcb_status s) {
+  switch (s) {
+    case PCB_OK: return "ok";
+    case PCB_E_PLAINTEXT_RANGE: return "plaintext not below n";
+    case PCB_E_RANDOMNESS_RANGE: return "randomness not in [1, n)";
+    case PCB_E_CIPHER_RANGE: return "ciphertext not below n^2";
+    case PCB_E_NOT_UNIT: return "ciphertext outside the multiplicative group";
+    case PCB_E_OVERFLOW: return "homomorphic accumulation exceeds plaintext space";
+    case PCB_E_NO_PRIVATE: return "no private key loaded";
+    case PCB_E_SHAPE: return "invalid argument (shape / window / size)";
+    case PCB_E_UNSUPPORTED: return "unsupported by this build";
+    case PCB_E_CUDA: return "CUDA error (or no device)";
+    case PCB_E_ALLOC: return "allocation failed";
+    case PCB_E_RANGE_UPDATE: return "combined update out of range";
+  }
+  return "unknown status";
+}
+
+uint64_t pcb_launch_count(void) { return launch_counter().load(); }
+
+pcb_status pcb_keygen(uint64_t* rng_state, uint32_t key_bits, uint32_t* n, uint32_t* p, uint32_t* q) {
+  if (!rng_state) return PCB_E_SHAPE;
+  try {
+    HRng rng(*rng_state);
+    HBN P, Q;
+    if (!pcb::keygen(rng, key_bits, P, Q)) return PCB_E_SHAPE;
+    *rng_state = rng.state;
+    const uint32_t nl = (key_bits + 31) / 32, hl = (key_bits / 2 + 31) / 32;
+    if (n) (P * Q).to_limbs(n, nl);
+    if (p) P.to_limbs(p, hl);
+    if (q) Q.to_limbs(q, hl);
+    return PCB_OK;
+  } catch (const std::bad_alloc&) {
+    return PCB_E_ALLOC;
+  } catch (...) {
+    return PCB_E_SHAPE;
+  }
+}
+
+pcb_status pcb_random_prime(uint64_t* rng_state, uint32_t bits, uint32_t* out) {
+  if (!rng_state || bits < 2) return PCB_E_SHAPE;
+  try {
+    HRng rng(*rng_state);
+    HBN P = pcb::random_prime(rng, bits);
+    *rng_state = rng.state;
+    P.to_limbs(out, (bits + 31) / 32);
+    return PCB_OK;
+  } catch (...) {
+    return PCB_E_SHAPE;
+  }
+}
+
+pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t n_limbs, const uint32_t* p,
+                          const uint32_t* q, uint32_t pq_limbs) {
+  if (!out || !n || n_limbs == 0) return PCB_E_SHAPE;
+  *out = nullptr;
+  std::unique_ptr<pcb_ctx> x(new (std::nothrow) pcb_ctx);
+  if (!x) return PCB_E_ALLOC;
+  try {
+    x->device = device;
+    x->n = HBN::from_limbs(n, n_limbs);
+    if (x->n.is_zero() || !x->n.is_odd()) return PCB_E_SHAPE;
+    x->n2 = x->n * x->n;
+    x->nbits = (uint32_t)x->n.bit_length();
+    x->L = (x->nbits + 31) / 32;
+    x->S2 = kernel_width_wide(2 * x->L);
+    if (x->S2 == 0) return PCB_E_SHAPE;
+    x->has_prv = p && q;
+    if (x->has_prv) {
+      x->p = HBN::from_limbs(p, pq_limbs);
+      x->q = HBN::from_limbs(q, pq_limbs);
+      if (x->p * x->q != x->n || x->p == x->q || !x->p.is_odd() || !x->q.is_odd()) return PCB_E_SHAPE;
+      const HBN p2 = x->p * x->p, q2 = x->q * x->q;
+      const uint32_t l2 = (uint32_t)((std::max(p2.bit_length(), q2.bit_length()) + 31) / 32);
+      x->S = kernel_width(std::max(l2, x->L));
+      if (x->S == 0) return PCB_E_SHAPE;
+      switch (x->S) {
+        case 32: build_enc<32>(x.get()); build_dec<32>(x.get()); break;
+        case 64: build_enc<64>(x.get()); build_dec<64>(x.get()); break;
+        default: break;  // 3072-bit keys: constants built by the wide-modulus path (TODO)
+      }
+    }
+    // exponent schedules
+    std::vector<uint8_t> all;
+    auto add = [&](const HBN& e, int* off, int* len) {
+      std::vector<uint8_t> s = build_ops(e, kWindow);
+      *off = (int)all.size();
+      *len = (int)s.size();
+      all.insert(all.end(), s.begin(), s.end());
+    };
+    if (x->has_prv) {
+      const HBN p2 = x->p * x->p, q2 = x->q * x->q;
+      add(mod(x->n, p2 - x->p), &x->off_enc_p, &x->len_enc_p);  // n mod phi(p^2)
+      add(mod(x->n, q2 - x->q), &x->off_enc_q, &x->len_enc_q);
+      add(x->p - HBN(1), &x->off_dec_p, &x->len_dec_p);
+      add(x->q - HBN(1), &x->off_dec_q, &x->len_dec_q);
+    }
+    add(x->n, &x->off_pub, &x->len_pub);
+    if (cudaSetDevice(device) != cudaSuccess) return PCB_E_CUDA;
+    if (cudaMalloc(&x->d_sched, all.size()) != cudaSuccess) return PCB_E_CUDA;
+    if (cudaMemcpy(x->d_sched, all.data(), all.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return PCB_E_CUDA;
+  } catch (const std::bad_alloc&) {
+    return PCB_E_ALLOC;
+  } catch (...) {
+    return PCB_E_SHAPE;
+  }
+  *out = x.release();
+  return PCB_OK;
+}
+
+void pcb_ctx_destroy(pcb_ctx* x) {
+  if (!x) return;
+  if (x->d_sched) {
+    cudaSetDevice(x->device);
+    cudaFree(x->d_sched);
+  }
+  delete x;
+}
+
+uint32_t pcb_ctx_n_limbs(const pcb_ctx* x) { return x ? x->L : 0; }
+uint32_t pcb_ctx_n_bits(const pcb_ctx* x) { return x ? x->nbits : 0; }
+int pcb_ctx_has_private(const pcb_ctx* x) { return x && x->has_prv ? 1 : 0; }
+
+pcb_status pcb_ctx_get_n(const pcb_ctx* x, uint32_t* n, uint32_t* n2) {
+  if (!x) return PCB_E_SHAPE;
+  if (n) x->n.to_limbs(n, x->L);
+  if (n2) x->n2.to_limbs(n2, 2 * x->L);
+  return PCB_OK;
+}
+
+void pcb_ctx_counters(const pcb_ctx* x, uint64_t* pow_full, uint64_t* pow_half) {
+  if (pow_full) *pow_full = x ? x->pow_full.load() : 0;
+  if (pow_half) *pow_half = x ? x->pow_half.load() : 0;
+}
+
+void pcb_ctx_reset_counters(pcb_ctx* x) {
+  if (!x) return;
+  x->pow_full = 0;
+  x->pow_half = 0;
+}
+
+static pcb_status enc_impl(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* r, size_t count,
+                           uint32_t* c, int32_t* status, const double* qv, double zmin, double zmax, double delta,
+                           int fine, uint64_t* q_out, unsigned long long* clamps, cudaStream_t st) {
+  Sched sp{x->d_sched + x->off_enc_p, x->len_enc_p}, sq{x->d_sched + x->off_enc_q, x->len_enc_q};
+  switch (x->S) {
+#define PCB_CASE(S)                                                                                             \
+  case S:                                                                                                       \
+    return launch_crt_encrypt<S>(*reinterpret_cast<const CrtEncConsts<S>*>(x->enc_blob.data()), sp, sq, kTab, m, \
+                                 (int)m_limbs, r, (int)x->L, count, c, status, qv, zmin, zmax, delta, fine, q_out,  \
+                                 clamps, st);
+    PCB_CASE(32)
+    PCB_CASE(64)
+#undef PCB_CASE
+  }
+  return PCB_E_UNSUPPORTED;
+}
+
+pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* r, size_t count, uint32_t* c,
+                       int use_crt, int32_t* status, pcb_stream stream) {
+  if (!x || (count && (!m || !r || !c))) return PCB_E_SHAPE;
+  if (m_limbs == 0 || m_limbs > x->L) return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  if (!use_crt) return PCB_E_UNSUPPORTED;  // direct (public-key) path: n2ops.cu
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  Staged sm, sr, sc, ss;
+  pcb_status e = stage_in(m, count * m_limbs * 4, st, &sm);
+  if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
+  if (!e) e = stage_out(c, count * 2 * x->L * 4, st, &sc);
+  if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+  if (!e)
+    e = enc_impl(x, (const uint32_t*)sm.dev, m_limbs, (const uint32_t*)sr.dev, count, (uint32_t*)sc.dev,
+                 (int32_t*)ss.dev, nullptr, 0, 0, 0, 0, nullptr, nullptr, st);
+  if (!e) e = unstage_out(c, &sc, st);
+  if (!e) e = unstage_out(status, &ss, st);
+  const bool any_host = sm.host || sr.host || sc.host || ss.host;
+  unstage(&sm, st);
+  unstage(&sr, st);
+  unstage(&sc, st);
+  unstage(&ss, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!e) x->pow_half += 2 * (uint64_t)count;
+  return e;
+}
+
+pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m, int use_crt, int32_t* status,
+                       pcb_stream stream) {
+  if (!x || (count && (!c || !m))) return PCB_E_SHAPE;
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  Staged sc, sm, ss;
+  pcb_status e = stage_in(c, count * 2 * x->L * 4, st, &sc);
+  if (!e) e = stage_out(m, count * x->L * 4, st, &sm);
+  if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+  Sched sp{x->d_sched + x->off_dec_p, x->len_dec_p}, sq{x->d_sched + x->off_dec_q, x->len_dec_q};
+  if (!e) {
+    switch (x->S) {
+#define PCB_CASE(S)                                                                                                  \
+  case S:                                                                                                            \
+    e = launch_crt_decrypt<S>(*reinterpret_cast<const CrtDecConsts<S>*>(x->dec_blob.data()), sp, sq, kTab,           \
+                              (const uint32_t*)sc.dev, (int)x->L, count, (uint32_t*)sm.dev, (int32_t*)ss.dev, st); \
+    break;
+      PCB_CASE(32)
+      PCB_CASE(64)
+#undef PCB_CASE
+      default: e = PCB_E_UNSUPPORTED;
+    }
+  }
+  if (!e) e = unstage_out(m, &sm, st);
+  if (!e) e = unstage_out(status, &ss, st);
+  const bool any_host = sc.host || sm.host || ss.host;
+  unstage(&sc, st);
+  unstage(&sm, st);
+  unstage(&ss, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!e) {
+    if (use_crt)
+      x->pow_half += 2 * (uint64_t)count;
+    else
+      x->pow_full += (uint64_t)count;
+  }
+  return e;
+}
+
+pcb_status pcb_quantize_encrypt(pcb_ctx* x, const double* v, size_t count, double z_min, double z_max, double delta,
+                                int fine, const uint32_t* r, int use_crt, uint32_t* c, uint64_t* q_out,
+                                uint64_t* clamps, pcb_stream stream) {
+  if (!x || (count && (!v || !r || !c))) return PCB_E_SHAPE;
+  // check_spec (quantize.cpp:8-15)
+  if (!(z_max > z_min) || !(z_max - z_min < 1e308) || !(delta >= 1.0) || delta > 9.0e15) return PCB_E_SHAPE;
+  if (!use_crt) return PCB_E_UNSUPPORTED;
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  Staged sv, sr, sc, sq;
+  unsigned long long* dclamps = nullptr;
+  pcb_status e = stage_in(v, count * 8, st, &sv);
+  if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
+  if (!e) e = stage_out(c, count * 2 * x->L * 4, st, &sc);
+  if (!e) e = stage_out(q_out, q_out ? count * 8 * (fine ? 2 : 1) : 0, st, &sq);
+  if (!e) e = scratch_alloc(16, (void**)&dclamps, st);
+  if (!e) e = cuda_check(cudaMemsetAsync(dclamps, 0, 16, st));
+  if (!e)
+    e = enc_impl(x, nullptr, fine ? 4 : 2, (const uint32_t*)sr.dev, count, (uint32_t*)sc.dev, nullptr,
+                 (const double*)sv.dev, z_min, z_max, delta, fine, (uint64_t*)sq.dev, dclamps, st);
+  if (!e) e = unstage_out(c, &sc, st);
+  if (!e) e = unstage_out(q_out, &sq, st);
+  unsigned long long hcl[2] = {0, 0};
+  if (!e && clamps) e = cuda_check(cudaMemcpyAsync(hcl, dclamps, 16, cudaMemcpyDeviceToHost, st));
+  unstage(&sv, st);
+  unstage(&sr, st);
+  unstage(&sc, st);
+  unstage(&sq, st);
+  scratch_free(dclamps, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!e && clamps) {
+    clamps[0] = hcl[0];
+    clamps[1] = hcl[1];
+  }
+  if (!e) x->pow_half += 2 * (uint64_t)count;
+  return e;
+}
+
+pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t* e, uint32_t e_limbs,
+                            const uint32_t* xs, size_t count, uint32_t* y, pcb_stream stream) {
+  if (!m || !e || (count && (!xs || !y))) return PCB_E_SHAPE;
+  const int S = kernel_width(m_limbs);
+  if (!S) return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  try {
+    HBN M = HBN::from_limbs(m, m_limbs), E = HBN::from_limbs(e, e_limbs);
+    if (!M.is_odd()) return PCB_E_SHAPE;
+    cudaStream_t st = (cudaStream_t)stream;
+    ModCtx<96> mc;  // largest; only the first S limbs are used
+    std::memset(&mc, 0, sizeof(mc));
+    M.to_limbs(mc.m, S);
+    mod(HBN(1) << (64 * S), M).to_limbs(mc.r2, S);
+    mc.minv = neg_inv32(mc.m[0]);
+    std::vector<uint8_t> sched = E.is_zero() ? std::vector<uint8_t>{0} : build_ops(E, kWindow);
+    uint8_t* d_sched = nullptr;
+    pcb_status s = scratch_alloc(sched.size(), (void**)&d_sched, st);
+    if (s) return s;
+    cudaMemcpyAsync(d_sched, sched.data(), sched.size(), cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);  // host vector goes out of scope
+    Staged sx, sy;
+    s = stage_in(xs, count * m_limbs * 4, st, &sx);
+    uint32_t* ydev = nullptr;
+    if (!s) s = scratch_alloc(count * S * 4, (void**)&ydev, st);
+    if (!s)
+      s = modexp_dispatch(S, mc.m, mc.r2, mc.minv, (const uint32_t*)d_sched, (int)sched.size(), kTab, E.is_zero(),
+                          (const uint32_t*)sx.dev, m_limbs, count, ydev, st);
+    if (!s) count_launch();
+    // compact S-wide rows to m_limbs-wide rows
+    if (!s) s = stage_out(y, count * m_limbs * 4, st, &sy);
+    if (!s)
+      s = cuda_check(cudaMemcpy2DAsync(sy.dev, m_limbs * 4, ydev, S * 4, m_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
+    if (!s) s = unstage_out(y, &sy, st);
+    unstage(&sx, st);
+    unstage(&sy, st);
+    scratch_free(ydev, st);
+    scratch_free(d_sched, st);
+    cudaStreamSynchronize(st);
+    return s;
+  } catch (...) {
+    return PCB_E_SHAPE;
+  }
+}
+
+}  // extern "C"
+
+// ---- not yet implemented in this build (fail loudly, never fall back) -----------------------
+extern "C" {
+pcb_status pcb_sample_r(pcb_ctx*, uint64_t*, size_t, uint32_t*, pcb_stream) { return PCB_E_UNSUPPORTED; }
+pcb_status pcb_hom_add(pcb_ctx*, const uint32_t*, const uint32_t*, size_t, uint32_t*, pcb_stream) {
+  return PCB_E_UNSUPPORTED;
+}
+pcb_status pcb_hom_scalar_mul(pcb_ctx*, const uint64_t*, const uint32_t*, size_t, uint32_t*, pcb_stream) {
+  return PCB_E_UNSUPPORTED;
+}
+pcb_status pcb_hom_matvec(pcb_ctx*, const uint32_t*, const uint64_t*, const uint32_t*, size_t, size_t, uint32_t,
+                          uint32_t*, pcb_stream) {
+  return PCB_E_UNSUPPORTED;
+}
+pcb_status pcb_edge_step(pcb_ctx*, const uint32_t*, const uint64_t*, const uint32_t*, const uint32_t*, size_t,
+                         uint32_t, uint32_t*, pcb_stream) {
+  return PCB_E_UNSUPPORTED;
+}
+pcb_status pcb_aggregate(pcb_ctx*, const uint32_t*, size_t, uint32_t*, pcb_stream) { return PCB_E_UNSUPPORTED; }
+pcb_status pcb_decrypt_update(pcb_ctx*, const uint32_t*, size_t, const uint64_t*, const uint64_t*, const uint64_t*,
+                              double, double, double, double, double*, double*, double*, int32_t*, pcb_stream) {
+  return PCB_E_UNSUPPORTED;
+}
+}
