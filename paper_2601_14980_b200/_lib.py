@@ -12,7 +12,7 @@ from pathlib import Path
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libpcb200.so"
+LIB_PATH = Path(os.environ["PCB_LIB"]) if os.environ.get("PCB_LIB") else _PKG / "libpcb200.so"
 
 STATUS = {
     0: "PCB_OK",

@@ -33,7 +33,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC
 SOURCES = [
     "abi.cu",
     "paillier.cu",
-    "modexp.cu",
+    "side.cu",
     "imad_peak.cu",
     "host/hbn.cpp",
 ]
@@ -72,8 +72,11 @@ def compile_one(src: str, dep_hash: str, extra: list[str], verbose: bool) -> Pat
     return out
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False, extra: list[str] | None = None) -> Path:
-    extra = extra or []
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, extra: list[str] | None = None,
+          out: Path | None = None) -> Path:
+    """Compile (cached) and link the library.  `extra` adds nvcc flags (e.g. -DPCB_ROW_UNROLL=32)."""
+    extra = list(extra or []) + os.environ.get("PCB_EXTRA_NVCC", "").split()
+    lib_path = Path(out) if out else LIB
     BUILD.mkdir(exist_ok=True)
     if force:
         for p in BUILD.glob("*.o"):
@@ -83,18 +86,18 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False, e
     with cf.ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(lambda s: compile_one(s, dep, extra, verbose), SOURCES))
     link_key = hashlib.sha256("".join(str(o) for o in objs).encode()).hexdigest()[:16]
-    stamp = BUILD / "link.stamp"
-    if LIB.exists() and stamp.exists() and stamp.read_text() == link_key and not force:
-        return LIB
-    tmp = LIB.with_suffix(".so.tmp")
+    stamp = BUILD / f"link.{lib_path.name}.stamp"
+    if lib_path.exists() and stamp.exists() and stamp.read_text() == link_key and not force:
+        return lib_path
+    tmp = lib_path.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-ccbin", CXX, "-o", str(tmp), *map(str, objs), "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_path)
     stamp.write_text(link_key)
-    return LIB
+    return lib_path
 
 
 def main() -> None:
@@ -102,8 +105,10 @@ def main() -> None:
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", type=int, default=None)
     ap.add_argument("-v", action="store_true")
+    ap.add_argument("-D", action="append", default=[], help="extra preprocessor define for nvcc")
+    ap.add_argument("--out", default=None, help="alternative output .so (experiments)")
     a = ap.parse_args()
-    print(build(force=a.force, jobs=a.j, verbose=a.v))
+    print(build(force=a.force, jobs=a.j, verbose=a.v, extra=[f"-D{d}" for d in a.D], out=a.out))
 
 
 if __name__ == "__main__":

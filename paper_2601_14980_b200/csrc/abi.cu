@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -23,6 +24,16 @@ std::atomic<uint64_t>& launch_counter() {
 
 // ---- scratch + staging ----------------------------------------------------------------------
 pcb_status scratch_alloc(size_t bytes, void** p, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // keep freed scratch in the stream-ordered pool (no re-mapping between batches)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
   *p = nullptr;
   if (bytes == 0) bytes = 16;
   return cudaMallocAsync(p, bytes, st) == cudaSuccess ? PCB_OK : PCB_E_ALLOC;
@@ -155,19 +166,33 @@ struct pcb_ctx {
   int off_enc_p = 0, len_enc_p = 0, off_enc_q = 0, len_enc_q = 0;
   int off_dec_p = 0, len_dec_p = 0, off_dec_q = 0, len_dec_q = 0;
   int off_pub = 0, len_pub = 0;  // exponent n at n^2 (direct encryption)
+  uint32_t* d_n = nullptr;       // n (L limbs), n^2 (2L limbs) for the argument checks
+  uint32_t* d_n2 = nullptr;
+  cudaStream_t side_st[2] = {nullptr, nullptr};  // p-half / q-half streams (fork-join)
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  std::mutex mu;                 // serialises use of the side streams
   std::atomic<uint64_t> pow_full{0}, pow_half{0};
 };
 
 namespace pcb {
-// launchers (paillier.cu / n2ops.cu)
+// launchers (side.cu / paillier.cu)
 template <int S>
-pcb_status launch_crt_encrypt(const CrtEncConsts<S>& k, Sched sp, Sched sq, int ntab, const uint32_t* m,
-                              int m_limbs, const uint32_t* r, int L, size_t count, uint32_t* c, int32_t* st,
-                              const double* qv, double zmin, double zmax, double delta, int fine, uint64_t* q_out,
-                              unsigned long long* clamps, cudaStream_t stream);
+pcb_status launch_side(const ModCtx<S>& mod, const uint32_t* c1, const uint8_t* ops, int nops, int ntab, int mode,
+                       const uint32_t* x, int x_limbs, const uint32_t* m, int m_limbs, const int32_t* skip,
+                       size_t count, uint32_t* y, cudaStream_t st);
 template <int S>
-pcb_status launch_crt_decrypt(const CrtDecConsts<S>& k, Sched sp, Sched sq, int ntab, const uint32_t* c, int L,
-                              size_t count, uint32_t* m, int32_t* st, cudaStream_t stream);
+pcb_status launch_garner(const CrtEncConsts<S>& k, const uint32_t* cp, const uint32_t* cq, const int32_t* st,
+                         uint32_t* c, int L, size_t count, cudaStream_t stream);
+template <int S>
+pcb_status launch_dec_finish(const CrtDecConsts<S>& k, const uint32_t* xp, const uint32_t* xq, int32_t* st,
+                             uint32_t* m, int L, size_t count, cudaStream_t stream);
+pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, double zmin, double zmax, double delta,
+                           int fine, uint32_t* m_out, int m_out_limbs, uint64_t* q_out, unsigned long long* clamps,
+                           const uint32_t* r, const uint32_t* n_dev, int L, int32_t* st, size_t count,
+                           cudaStream_t stream);
+pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int32_t* st, size_t count,
+                           cudaStream_t stream);
+enum SideMode : int { kSideEnc = 0, kSideDec = 1, kSidePow = 2 };
 }  // namespace pcb
 
 namespace {
@@ -341,6 +366,18 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
     }
     add(x->n, &x->off_pub, &x->len_pub);
     if (cudaSetDevice(device) != cudaSuccess) return PCB_E_CUDA;
+    if (cudaMalloc(&x->d_n, x->L * 4) != cudaSuccess) return PCB_E_CUDA;
+    if (cudaMalloc(&x->d_n2, 2 * x->L * 4) != cudaSuccess) return PCB_E_CUDA;
+    {
+      std::vector<uint32_t> nl = x->n.limbs(x->L), n2l = x->n2.limbs(2 * x->L);
+      if (cudaMemcpy(x->d_n, nl.data(), x->L * 4, cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
+      if (cudaMemcpy(x->d_n2, n2l.data(), 2 * x->L * 4, cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
+    }
+    for (int k = 0; k < 2; k++) {
+      if (cudaStreamCreateWithFlags(&x->side_st[k], cudaStreamNonBlocking) != cudaSuccess) return PCB_E_CUDA;
+      if (cudaEventCreateWithFlags(&x->ev_join[k], cudaEventDisableTiming) != cudaSuccess) return PCB_E_CUDA;
+    }
+    if (cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming) != cudaSuccess) return PCB_E_CUDA;
     if (cudaMalloc(&x->d_sched, all.size()) != cudaSuccess) return PCB_E_CUDA;
     if (cudaMemcpy(x->d_sched, all.data(), all.size(), cudaMemcpyHostToDevice) != cudaSuccess)
       return PCB_E_CUDA;
@@ -355,10 +392,15 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
 
 void pcb_ctx_destroy(pcb_ctx* x) {
   if (!x) return;
-  if (x->d_sched) {
-    cudaSetDevice(x->device);
-    cudaFree(x->d_sched);
+  cudaSetDevice(x->device);
+  if (x->d_sched) cudaFree(x->d_sched);
+  if (x->d_n) cudaFree(x->d_n);
+  if (x->d_n2) cudaFree(x->d_n2);
+  for (int k = 0; k < 2; k++) {
+    if (x->side_st[k]) cudaStreamDestroy(x->side_st[k]);
+    if (x->ev_join[k]) cudaEventDestroy(x->ev_join[k]);
   }
+  if (x->ev_fork) cudaEventDestroy(x->ev_fork);
   delete x;
 }
 
@@ -384,22 +426,116 @@ void pcb_ctx_reset_counters(pcb_ctx* x) {
   x->pow_half = 0;
 }
 
-static pcb_status enc_impl(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* r, size_t count,
-                           uint32_t* c, int32_t* status, const double* qv, double zmin, double zmax, double delta,
-                           int fine, uint64_t* q_out, unsigned long long* clamps, cudaStream_t st) {
-  Sched sp{x->d_sched + x->off_enc_p, x->len_enc_p}, sq{x->d_sched + x->off_enc_q, x->len_enc_q};
-  switch (x->S) {
-#define PCB_CASE(S)                                                                                             \
-  case S:                                                                                                       \
-    return launch_crt_encrypt<S>(*reinterpret_cast<const CrtEncConsts<S>*>(x->enc_blob.data()), sp, sq, kTab, m, \
-                                 (int)m_limbs, r, (int)x->L, count, c, status, qv, zmin, zmax, delta, fine, q_out,  \
-                                 clamps, st);
-    PCB_CASE(32)
-    PCB_CASE(64)
-#undef PCB_CASE
+}  // extern "C"
+
+// Runs the two CRT halves concurrently: fork from `st`, side p on side_st[0], side q on
+// side_st[1], join back into `st`.
+template <class FP, class FQ>
+static pcb_status fork_join(pcb_ctx* x, cudaStream_t st, FP&& fp, FQ&& fq) {
+  std::lock_guard<std::mutex> lk(x->mu);
+  pcb_status e = cuda_check(cudaEventRecord(x->ev_fork, st));
+  for (int k = 0; k < 2 && !e; k++) e = cuda_check(cudaStreamWaitEvent(x->side_st[k], x->ev_fork, 0));
+  if (!e) e = fp(x->side_st[0]);
+  if (!e) e = fq(x->side_st[1]);
+  for (int k = 0; k < 2; k++) {
+    cudaEventRecord(x->ev_join[k], x->side_st[k]);
+    cudaStreamWaitEvent(st, x->ev_join[k], 0);
   }
-  return PCB_E_UNSUPPORTED;
+  return e;
 }
+
+// Device-pointer core of CRT encryption (m given as limbs, or v quantized in the prep kernel).
+static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const double* v, double zmin, double zmax,
+                           double delta, int fine, uint64_t* q_out, unsigned long long* clamps, const uint32_t* r,
+                           size_t count, uint32_t* c, int32_t* st_user, cudaStream_t st) {
+  const int S = x->S;
+  int32_t* stv = st_user;
+  uint32_t *mq = nullptr, *yp = nullptr, *yq = nullptr;
+  pcb_status e = PCB_OK;
+  if (!stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+  const int mql = 4;
+  if (!e && v) e = scratch_alloc(count * mql * 4, (void**)&mq, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yp, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yq, st);
+  if (!e)
+    e = launch_enc_prep(m, (int)m_limbs, v, zmin, zmax, delta, fine, mq, mql, q_out, clamps, r, x->d_n, (int)x->L,
+                        stv, count, st);
+  const uint32_t* mm = v ? mq : m;
+  const int ml = v ? mql : (int)m_limbs;
+  const uint8_t* opp = x->d_sched + x->off_enc_p;
+  const uint8_t* opq = x->d_sched + x->off_enc_q;
+  if (!e) {
+    switch (S) {
+#define PCB_CASE(SS)                                                                                                  \
+  case SS: {                                                                                                          \
+    const auto& k = *reinterpret_cast<const CrtEncConsts<SS>*>(x->enc_blob.data());                                   \
+    e = fork_join(                                                                                                    \
+        x, st,                                                                                                        \
+        [&](cudaStream_t s2) {                                                                                        \
+          return launch_side<SS>(k.mp, k.nRp, opp, x->len_enc_p, kTab, kSideEnc, r, (int)x->L, mm, ml, stv, count, yp, s2); \
+        },                                                                                                            \
+        [&](cudaStream_t s2) {                                                                                        \
+          return launch_side<SS>(k.mq, k.nRq, opq, x->len_enc_q, kTab, kSideEnc, r, (int)x->L, mm, ml, stv, count, yq, s2); \
+        });                                                                                                           \
+    if (!e) e = launch_garner<SS>(k, yp, yq, stv, c, (int)x->L, count, st);                                           \
+    break;                                                                                                            \
+  }
+      PCB_CASE(32)
+      PCB_CASE(64)
+#undef PCB_CASE
+      default: e = PCB_E_UNSUPPORTED;
+    }
+  }
+  scratch_free(yp, st);
+  scratch_free(yq, st);
+  scratch_free(mq, st);
+  if (!st_user) scratch_free(stv, st);
+  return e;
+}
+
+static pcb_status dec_core(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m, int32_t* st_user,
+                           cudaStream_t st) {
+  const int S = x->S;
+  int32_t* stv = st_user;
+  uint32_t *yp = nullptr, *yq = nullptr;
+  pcb_status e = PCB_OK;
+  if (!stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yp, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yq, st);
+  if (!e) e = launch_dec_prep(c, x->d_n2, (int)x->L, stv, count, st);
+  const uint8_t* opp = x->d_sched + x->off_dec_p;
+  const uint8_t* opq = x->d_sched + x->off_dec_q;
+  if (!e) {
+    switch (S) {
+#define PCB_CASE(SS)                                                                                                \
+  case SS: {                                                                                                        \
+    const auto& k = *reinterpret_cast<const CrtDecConsts<SS>*>(x->dec_blob.data());                                 \
+    e = fork_join(                                                                                                  \
+        x, st,                                                                                                      \
+        [&](cudaStream_t s2) {                                                                                      \
+          return launch_side<SS>(k.mp, k.r3p, opp, x->len_dec_p, kTab, kSideDec, c, 2 * (int)x->L, nullptr, 0, stv, \
+                                 count, yp, s2);                                                                    \
+        },                                                                                                          \
+        [&](cudaStream_t s2) {                                                                                      \
+          return launch_side<SS>(k.mq, k.r3q, opq, x->len_dec_q, kTab, kSideDec, c, 2 * (int)x->L, nullptr, 0, stv, \
+                                 count, yq, s2);                                                                    \
+        });                                                                                                         \
+    if (!e) e = launch_dec_finish<SS>(k, yp, yq, stv, m, (int)x->L, count, st);                                     \
+    break;                                                                                                          \
+  }
+      PCB_CASE(32)
+      PCB_CASE(64)
+#undef PCB_CASE
+      default: e = PCB_E_UNSUPPORTED;
+    }
+  }
+  scratch_free(yp, st);
+  scratch_free(yq, st);
+  if (!st_user) scratch_free(stv, st);
+  return e;
+}
+
+extern "C" {
 
 pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* r, size_t count, uint32_t* c,
                        int use_crt, int32_t* status, pcb_stream stream) {
@@ -416,8 +552,8 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
   if (!e) e = stage_out(c, count * 2 * x->L * 4, st, &sc);
   if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
   if (!e)
-    e = enc_impl(x, (const uint32_t*)sm.dev, m_limbs, (const uint32_t*)sr.dev, count, (uint32_t*)sc.dev,
-                 (int32_t*)ss.dev, nullptr, 0, 0, 0, 0, nullptr, nullptr, st);
+    e = enc_core(x, (const uint32_t*)sm.dev, m_limbs, nullptr, 0, 0, 0, 0, nullptr, nullptr, (const uint32_t*)sr.dev,
+                 count, (uint32_t*)sc.dev, (int32_t*)ss.dev, st);
   if (!e) e = unstage_out(c, &sc, st);
   if (!e) e = unstage_out(status, &ss, st);
   const bool any_host = sm.host || sr.host || sc.host || ss.host;
@@ -441,20 +577,7 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
   pcb_status e = stage_in(c, count * 2 * x->L * 4, st, &sc);
   if (!e) e = stage_out(m, count * x->L * 4, st, &sm);
   if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
-  Sched sp{x->d_sched + x->off_dec_p, x->len_dec_p}, sq{x->d_sched + x->off_dec_q, x->len_dec_q};
-  if (!e) {
-    switch (x->S) {
-#define PCB_CASE(S)                                                                                                  \
-  case S:                                                                                                            \
-    e = launch_crt_decrypt<S>(*reinterpret_cast<const CrtDecConsts<S>*>(x->dec_blob.data()), sp, sq, kTab,           \
-                              (const uint32_t*)sc.dev, (int)x->L, count, (uint32_t*)sm.dev, (int32_t*)ss.dev, st); \
-    break;
-      PCB_CASE(32)
-      PCB_CASE(64)
-#undef PCB_CASE
-      default: e = PCB_E_UNSUPPORTED;
-    }
-  }
+  if (!e) e = dec_core(x, (const uint32_t*)sc.dev, count, (uint32_t*)sm.dev, (int32_t*)ss.dev, st);
   if (!e) e = unstage_out(m, &sm, st);
   if (!e) e = unstage_out(status, &ss, st);
   const bool any_host = sc.host || sm.host || ss.host;
@@ -476,7 +599,8 @@ pcb_status pcb_quantize_encrypt(pcb_ctx* x, const double* v, size_t count, doubl
                                 uint64_t* clamps, pcb_stream stream) {
   if (!x || (count && (!v || !r || !c))) return PCB_E_SHAPE;
   // check_spec (quantize.cpp:8-15)
-  if (!(z_max > z_min) || !(z_max - z_min < 1e308) || !(delta >= 1.0) || delta > 9.0e15) return PCB_E_SHAPE;
+  if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
+    return PCB_E_SHAPE;
   if (!use_crt) return PCB_E_UNSUPPORTED;
   if (!x->has_prv) return PCB_E_NO_PRIVATE;
   if (count == 0) return PCB_OK;
@@ -491,8 +615,8 @@ pcb_status pcb_quantize_encrypt(pcb_ctx* x, const double* v, size_t count, doubl
   if (!e) e = scratch_alloc(16, (void**)&dclamps, st);
   if (!e) e = cuda_check(cudaMemsetAsync(dclamps, 0, 16, st));
   if (!e)
-    e = enc_impl(x, nullptr, fine ? 4 : 2, (const uint32_t*)sr.dev, count, (uint32_t*)sc.dev, nullptr,
-                 (const double*)sv.dev, z_min, z_max, delta, fine, (uint64_t*)sq.dev, dclamps, st);
+    e = enc_core(x, nullptr, 0, (const double*)sv.dev, z_min, z_max, delta, fine, (uint64_t*)sq.dev, dclamps,
+                 (const uint32_t*)sr.dev, count, (uint32_t*)sc.dev, nullptr, st);
   if (!e) e = unstage_out(c, &sc, st);
   if (!e) e = unstage_out(q_out, &sq, st);
   unsigned long long hcl[2] = {0, 0};
@@ -521,35 +645,50 @@ pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t*
     HBN M = HBN::from_limbs(m, m_limbs), E = HBN::from_limbs(e, e_limbs);
     if (!M.is_odd()) return PCB_E_SHAPE;
     cudaStream_t st = (cudaStream_t)stream;
-    ModCtx<96> mc;  // largest; only the first S limbs are used
-    std::memset(&mc, 0, sizeof(mc));
-    M.to_limbs(mc.m, S);
-    mod(HBN(1) << (64 * S), M).to_limbs(mc.r2, S);
-    mc.minv = neg_inv32(mc.m[0]);
-    std::vector<uint8_t> sched = E.is_zero() ? std::vector<uint8_t>{0} : build_ops(E, kWindow);
-    uint8_t* d_sched = nullptr;
-    pcb_status s = scratch_alloc(sched.size(), (void**)&d_sched, st);
-    if (s) return s;
-    cudaMemcpyAsync(d_sched, sched.data(), sched.size(), cudaMemcpyHostToDevice, st);
-    cudaStreamSynchronize(st);  // host vector goes out of scope
     Staged sx, sy;
-    s = stage_in(xs, count * m_limbs * 4, st, &sx);
-    uint32_t* ydev = nullptr;
-    if (!s) s = scratch_alloc(count * S * 4, (void**)&ydev, st);
-    if (!s)
-      s = modexp_dispatch(S, mc.m, mc.r2, mc.minv, (const uint32_t*)d_sched, (int)sched.size(), kTab, E.is_zero(),
-                          (const uint32_t*)sx.dev, m_limbs, count, ydev, st);
-    if (!s) count_launch();
-    // compact S-wide rows to m_limbs-wide rows
+    pcb_status s = stage_in(xs, count * m_limbs * 4, st, &sx);
     if (!s) s = stage_out(y, count * m_limbs * 4, st, &sy);
-    if (!s)
-      s = cuda_check(cudaMemcpy2DAsync(sy.dev, m_limbs * 4, ydev, S * 4, m_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
+    uint32_t* ydev = nullptr;
+    uint8_t* d_ops = nullptr;
+    if (!s) s = scratch_alloc(count * S * 4, (void**)&ydev, st);
+    if (!s && E.is_zero()) {
+      // x^0 = 1 mod m (0 when m == 1)
+      std::vector<uint32_t> one(count * m_limbs, 0);
+      if (!(M == HBN(1)))
+        for (size_t i = 0; i < count; i++) one[i * m_limbs] = 1;
+      s = cuda_check(cudaMemcpyAsync(sy.dev, one.data(), one.size() * 4, cudaMemcpyHostToDevice, st));
+      cudaStreamSynchronize(st);
+    } else if (!s) {
+      std::vector<uint8_t> ops = build_ops(E, kWindow);
+      s = scratch_alloc(ops.size(), (void**)&d_ops, st);
+      if (!s) s = cuda_check(cudaMemcpyAsync(d_ops, ops.data(), ops.size(), cudaMemcpyHostToDevice, st));
+      if (!s) {
+        switch (S) {
+#define PCB_CASE(SS)                                                                                        \
+  case SS: {                                                                                                \
+    ModCtx<SS> mc;                                                                                          \
+    fill_mod<SS>(mc, M);                                                                                    \
+    s = launch_side<SS>(mc, nullptr, d_ops, (int)ops.size(), kTab, kSidePow, (const uint32_t*)sx.dev,       \
+                        (int)m_limbs, nullptr, 0, nullptr, count, ydev, st);                               \
+    break;                                                                                                  \
+  }
+          PCB_CASE(32)
+          PCB_CASE(64)
+#undef PCB_CASE
+          default: s = PCB_E_UNSUPPORTED;
+        }
+      }
+      if (!s)
+        s = cuda_check(cudaMemcpy2DAsync(sy.dev, m_limbs * 4, ydev, S * 4, m_limbs * 4, count,
+                                         cudaMemcpyDeviceToDevice, st));
+      cudaStreamSynchronize(st);  // `ops` is a host temporary
+    }
     if (!s) s = unstage_out(y, &sy, st);
     unstage(&sx, st);
     unstage(&sy, st);
     scratch_free(ydev, st);
-    scratch_free(d_sched, st);
-    cudaStreamSynchronize(st);
+    scratch_free(d_ops, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && !s) s = PCB_E_CUDA;
     return s;
   } catch (...) {
     return PCB_E_SHAPE;

@@ -55,21 +55,21 @@ __device__ __forceinline__ bool is_zero_words(const uint32_t* a, int na) {
 }
 
 // X = (X + Y) mod M for X, Y < M
-template <int S>
-__device__ __forceinline__ void mod_add(uint32_t (&X)[S], const uint32_t (&Y)[S], const SMod<S>& M) {
+template <int S, class MA>
+__device__ __forceinline__ void mod_add(uint32_t (&X)[S], const uint32_t (&Y)[S], const MA& M) {
   uint32_t T[S + 1];
   asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(T[0]) : "r"(X[0]), "r"(Y[0]));
 #pragma unroll
   for (int j = 1; j < S; j++) asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(T[j]) : "r"(X[j]), "r"(Y[j]));
   asm volatile("addc.u32 %0, 0, 0;" : "=r"(T[S]));
-  cond_sub<S>(T, M);
+  cond_sub<S, MA>(T, M);
 #pragma unroll
   for (int j = 0; j < S; j++) X[j] = T[j];
 }
 
 // X = (X - Y) mod M for X, Y < M
-template <int S>
-__device__ __forceinline__ void mod_sub(uint32_t (&X)[S], const uint32_t (&Y)[S], const SMod<S>& M) {
+template <int S, class MA>
+__device__ __forceinline__ void mod_sub(uint32_t (&X)[S], const uint32_t (&Y)[S], const MA& M) {
   uint32_t br;
   asm volatile("sub.cc.u32 %0, %0, %1;" : "+r"(X[0]) : "r"(Y[0]));
 #pragma unroll
@@ -92,14 +92,14 @@ __device__ __forceinline__ void mod_sub(uint32_t (&X)[S], const uint32_t (&Y)[S]
 }
 
 // X += 1 mod M  (X < M)
-template <int S>
-__device__ __forceinline__ void mod_inc(uint32_t (&X)[S], const SMod<S>& M) {
+template <int S, class MA>
+__device__ __forceinline__ void mod_inc(uint32_t (&X)[S], const MA& M) {
   uint32_t T[S + 1];
   asm volatile("add.cc.u32 %0, %1, 1;" : "=r"(T[0]) : "r"(X[0]));
 #pragma unroll
   for (int j = 1; j < S; j++) asm volatile("addc.cc.u32 %0, %1, 0;" : "=r"(T[j]) : "r"(X[j]));
   asm volatile("addc.u32 %0, 0, 0;" : "=r"(T[S]));
-  cond_sub<S>(T, M);
+  cond_sub<S, MA>(T, M);
 #pragma unroll
   for (int j = 0; j < S; j++) X[j] = T[j];
 }

@@ -1,12 +1,16 @@
-// paillier.cu — batched CRT encryption and decryption kernels (the hot path).
+// paillier.cu — the light kernels around the hot side kernel (side.cu):
 //
-//   crt_encrypt_kernel : Paillier::crt_encrypt_with_r  (/root/reference/proj/src/paillier.cpp:334-344)
-//                        batched as in encrypt_vec (paillier.cpp:495-507)
-//   crt_decrypt_kernel : Paillier::crt_decrypt / decrypt (paillier.cpp:346-361), batched as
-//                        decrypt_vec (paillier.cpp:509-516)
+//   enc_prep_kernel  argument checks of Paillier::crt_encrypt_with_r / encrypt_with_r
+//                    (paillier.cpp:241-243, 322-323, 335-338) and the fused quantize prologue
+//                    (gamma1/gamma2, quantize.cpp:17-41) -> plaintext limbs + status
+//   garner_kernel    combine_halves (paillier.cpp:307-314): c = c_p + p^2 ((c_q - c_p) (p^2)^-1 mod q^2)
+//   dec_prep_kernel  c < n^2 check (paillier.cpp:356)
+//   dec_finish_kernel  L_p / h_p / CRT: m = L(c^eps mod n^2) mu mod n computed as
+//                    m_p = L_p(c^(p-1) mod p^2) h_p mod p,  m = m_p + p ((m_q - m_p) p^-1 mod q);
+//                    non-unit ciphertexts (l_function, paillier.cpp:34-41) -> PCB_E_NOT_UNIT.
 //
-// One element per thread; both CRT halves run in the same thread so the Garner recombination
-// stays in registers.  Every exponent is per-key (n mod phi(p^2), p-1, ...), i.e. warp-uniform.
+// These run O(S^2) work per element against O(S^3) in the side kernel, so they favour simple
+// code: moduli live in block-shared memory (broadcast loads), one element per thread.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -17,27 +21,7 @@
 
 namespace pcb {
 
-
-template <int S>
-struct CrtEncArgs {
-  CrtEncConsts<S> k;
-  Sched sp, sq;          // n mod phi(p^2), n mod phi(q^2)
-  int ntab;
-  uint4* tab;
-  const uint32_t* m;     // count x m_limbs
-  const uint32_t* r;     // count x L
-  uint32_t* c;           // count x 2L
-  int32_t* st;           // count (nullable)
-  int m_limbs, L, count;
-  const double* qv;      // fused quantize prologue (nullable): values -> m
-  double zmin, zmax, delta;
-  int fine;
-  uint64_t* q_out;       // quantized integers (nullable)
-  unsigned long long* clamps;  // [2] device counters (nullable)
-};
-
-// Quantizers, FP64 with the reference's operation order and no contraction
-// (quantize.cpp:31-41; built with --fmad=false).  round() is half-away-from-zero as libm.
+// ---- quantizers (FP64, reference operation order, no contraction: built with --fmad=false)
 __device__ __forceinline__ double clamp_q(double v, double zmin, double zmax, unsigned long long* clamps) {
   if (v < zmin) {
     if (clamps) atomicAdd(&clamps[0], 1ull);
@@ -50,203 +34,173 @@ __device__ __forceinline__ double clamp_q(double v, double zmin, double zmax, un
   return v;
 }
 
-// gamma2: (u64) round(delta * ((clamp(v) - zmin) / R))
+// gamma2 (quantize.cpp:31-35): (u64) round(delta * ((clamp(v) - zmin) / R)), R = zmax - zmin
 __device__ __forceinline__ uint64_t gamma2_dev(double v, double zmin, double zmax, double delta,
                                                unsigned long long* clamps) {
-  double R = __dsub_rn(zmax, zmin);
-  double t = __dmul_rn(delta, __ddiv_rn(__dsub_rn(clamp_q(v, zmin, zmax, clamps), zmin), R));
+  const double R = __dsub_rn(zmax, zmin);
+  const double t = __dmul_rn(delta, __ddiv_rn(__dsub_rn(clamp_q(v, zmin, zmax, clamps), zmin), R));
   return (uint64_t)round(t);
 }
 
-// gamma1: (u128) round((delta*delta) * ((clamp(v) - zmin) / (R*R)))  -> lo/hi u64
+// gamma1 (quantize.cpp:37-41): (u128) round(delta * delta * ((clamp(v) - zmin) / (R * R)))
 __device__ __forceinline__ void gamma1_dev(double v, double zmin, double zmax, double delta,
                                            unsigned long long* clamps, uint64_t& lo, uint64_t& hi) {
-  double R = __dsub_rn(zmax, zmin);
-  double d = __ddiv_rn(__dsub_rn(clamp_q(v, zmin, zmax, clamps), zmin), __dmul_rn(R, R));
-  double t = round(__dmul_rn(__dmul_rn(delta, delta), d));
-  // exact double -> u128 (t is a non-negative integer-valued double, < 2^128)
+  const double R = __dsub_rn(zmax, zmin);
+  const double d = __ddiv_rn(__dsub_rn(clamp_q(v, zmin, zmax, clamps), zmin), __dmul_rn(R, R));
+  const double t = round(__dmul_rn(__dmul_rn(delta, delta), d));
+  // exact double -> u128 (t is a non-negative integer-valued double)
   if (t < 18446744073709551616.0) {
     lo = (uint64_t)t;
     hi = 0;
   } else {
-    double h = floor(t * 5.421010862427522e-20);  // t / 2^64, exact power-of-two scaling
+    const double h = floor(__dmul_rn(t, 0x1p-64));
     hi = (uint64_t)h;
-    lo = (uint64_t)(t - h * 18446744073709551616.0);
+    lo = (uint64_t)__dsub_rn(t, __dmul_rn(h, 0x1p64));
   }
 }
 
-// Slot policy: multiplicand in registers when 3S+4 registers fit next to the kernel state.
-template <int S>
-struct Areg {
-  static constexpr bool value = S <= 64;
+struct EncPrepArgs {
+  const uint32_t* m;  // count x m_limbs, or null when quantizing
+  int m_limbs;
+  const double* v;    // values to quantize (nullable)
+  double zmin, zmax, delta;
+  int fine;
+  uint32_t* m_out;    // count x m_out_limbs (quantized plaintexts), nullable
+  int m_out_limbs;
+  uint64_t* q_out;    // quantized integers for the caller (nullable)
+  unsigned long long* clamps;
+  const uint32_t* r;  // count x L
+  const uint32_t* n;  // L limbs (device)
+  int L;
+  int32_t* st;        // count
+  int count;
 };
 
-// Scratch entries appended to the per-thread power table.
-enum : int { kParkG = 0, kParkCp = 1, kParkA1 = 2, kParkMp = 0, kNumPark = 3 };
-
-// One CRT half of encryption:  C = (1 + m n mod m2) * r^(n mod phi(m2)) mod m2 (plain), left
-// in registers.  (crt_encrypt_with_r per side: g_power_half + half_pow, paillier.cpp:339-342)
-template <int S>
-__device__ __forceinline__ void enc_half(uint32_t (&C)[S], const Slot<S>& Acc, const Slot<S>& Op,
-                                         const GTable<S>& tab, int ntab, const uint32_t* msrc, int m_limbs,
-                                         uint64_t qlo, uint64_t qhi, bool quantized, const uint32_t* rsrc, int L,
-                                         const SMod<S>& M2, const uint32_t* r2, const uint32_t* nR, const Sched& sc) {
-  constexpr bool AR = Areg<S>::value;
-  uint32_t R[S];
-  // g^m = 1 + m n mod m2  (g_power_half, paillier.cpp:263), parked while r^e runs
-  if (quantized) {
-    Acc.store_small(0);
-    uint4 c0 = make_uint4((uint32_t)qlo, (uint32_t)qhi, 0, 0);  // even limbs m0, m2
-    uint4 c1 = make_uint4((uint32_t)(qlo >> 32), (uint32_t)(qhi >> 32), 0, 0);  // odd limbs m1, m3
-    Acc.set_chunk(0, c0);
-    Acc.set_chunk(S / 8, c1);
-  } else {
-    Acc.store_global(msrc, m_limbs);
-  }
-  Op.store_const(nR);
-  mont_mul_ss<S, AR>(R, Acc, Op, M2);  // m n mod m2
-  mod_inc<S>(R, M2);
-  tab.put(ntab + kParkG, R);
-  // r^e
-  Acc.store_global(rsrc, L);
-  Op.store_const(r2);
-  mont_mul_ss<S, AR>(R, Acc, Op, M2);  // r R mod m2 (also reduces r)
-  Acc.store(R);
-  mont_pow<S, AR>(Acc, Op, tab, ntab, sc.ops, sc.n, M2);
-  tab.to_slot(ntab + kParkG, Op);
-  mont_mul_ss<S, AR>(C, Acc, Op, M2);  // r^e (1 + m n): Montgomery x plain = plain
-}
-
-template <int S>
-__global__ void __launch_bounds__(kThreadsPerBlock) crt_encrypt_kernel(const __grid_constant__ CrtEncArgs<S> P) {
-  extern __shared__ __align__(16) uint32_t smem[];
-  constexpr bool AR = Areg<S>::value;
-  const CrtEncConsts<S>& K = P.k;
-  // block-shared moduli (broadcast operands), then two per-thread slots
-  smod_fill<S>(smem, K.mp.m);
-  smod_fill<S>(smem + S, K.mq.m);
-  __syncthreads();
-  const SMod<S> Mp{smem_addr(smem), K.mp.minv}, Mq{smem_addr(smem + S), K.mq.minv};
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* slots = smem + 2 * S;
-  const Slot<S> Acc{smem_addr(slots + warp * (64 * S) + lane * 4)};
-  const Slot<S> Op{smem_addr(slots + warp * (64 * S) + 32 * S + lane * 4)};
-  const uint32_t nthr = gridDim.x * blockDim.x;
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  GTable<S> tab{P.tab, nthr, g};
-
-  for (int i = g; i < P.count; i += nthr) {
-    uint32_t* out = P.c + (size_t)i * 2 * P.L;
-    const uint32_t* rsrc = P.r + (size_t)i * P.L;
-    const uint32_t* msrc = P.m ? P.m + (size_t)i * P.m_limbs : nullptr;
-    // ---- plaintext (optionally quantized in-kernel) and argument checks -------------------
-    uint64_t qlo = 0, qhi = 0;
+__global__ void enc_prep_kernel(const __grid_constant__ EncPrepArgs P) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.count; i += gridDim.x * blockDim.x) {
     int status = PCB_OK;
-    if (P.qv) {  // fused quantize prologue (quantize.cpp:31-41)
-      const double v = P.qv[i];
+    if (P.v) {
+      const double v = P.v[i];
+      uint64_t lo = 0, hi = 0;
       if (!isfinite(v)) {
-        status = PCB_E_SHAPE;  // clamp_in throws invalid_argument (quantize.cpp:18-19)
+        status = PCB_E_SHAPE;  // clamp_in: "non-finite value into quantizer" (quantize.cpp:18-19)
       } else if (P.fine) {
-        gamma1_dev(v, P.zmin, P.zmax, P.delta, P.clamps, qlo, qhi);
-        if (P.q_out) { P.q_out[2 * (size_t)i] = qlo; P.q_out[2 * (size_t)i + 1] = qhi; }
+        gamma1_dev(v, P.zmin, P.zmax, P.delta, P.clamps, lo, hi);
+        if (P.q_out) {
+          P.q_out[2 * (size_t)i] = lo;
+          P.q_out[2 * (size_t)i + 1] = hi;
+        }
       } else {
-        qlo = gamma2_dev(v, P.zmin, P.zmax, P.delta, P.clamps);
-        if (P.q_out) P.q_out[i] = qlo;
+        lo = gamma2_dev(v, P.zmin, P.zmax, P.delta, P.clamps);
+        if (P.q_out) P.q_out[i] = lo;
       }
-      // quantized values are < 2^128 <= n for every supported key; compare anyway
-      if (status == PCB_OK) {
-        uint32_t mw[4] = {(uint32_t)qlo, (uint32_t)(qlo >> 32), (uint32_t)qhi, (uint32_t)(qhi >> 32)};
-        if (!lt_words(mw, 4, K.n, P.L)) status = PCB_E_PLAINTEXT_RANGE;
-      }
-    } else if (!lt_words(msrc, P.m_limbs, K.n, P.L)) {
+      uint32_t w[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
+      uint32_t* mo = P.m_out + (size_t)i * P.m_out_limbs;
+      for (int j = 0; j < P.m_out_limbs; j++) mo[j] = j < 4 ? w[j] : 0u;
+      if (status == PCB_OK && !lt_words(w, 4, P.n, P.L)) status = PCB_E_PLAINTEXT_RANGE;
+    } else if (!lt_words(P.m + (size_t)i * P.m_limbs, P.m_limbs, P.n, P.L)) {
       status = PCB_E_PLAINTEXT_RANGE;  // check_plaintext (paillier.cpp:241-243)
     }
-    if (status == PCB_OK && (is_zero_words(rsrc, P.L) || !lt_words(rsrc, P.L, K.n, P.L)))
-      status = PCB_E_RANDOMNESS_RANGE;  // paillier.cpp:337-338
-    if (P.st) P.st[i] = status;
-    if (status != PCB_OK) {
-      for (int j = 0; j < 2 * P.L; j++) out[j] = 0;
-      continue;
+    if (status == PCB_OK) {
+      const uint32_t* r = P.r + (size_t)i * P.L;
+      if (is_zero_words(r, P.L) || !lt_words(r, P.L, P.n, P.L)) status = PCB_E_RANDOMNESS_RANGE;
     }
-    const bool quant = P.qv != nullptr;
-    {
-      uint32_t C[S];
-      enc_half<S>(C, Acc, Op, tab, P.ntab, msrc, P.m_limbs, qlo, qhi, quant, rsrc, P.L, Mp, K.mp.r2, K.nRp, P.sp);
-      tab.put(P.ntab + kParkCp, C);
-    }
-    uint32_t A2[S];
-    enc_half<S>(A2, Acc, Op, tab, P.ntab, msrc, P.m_limbs, qlo, qhi, quant, rsrc, P.L, Mq, K.mq.r2, K.nRq, P.sq);
-    // ---- Garner (combine_halves, paillier.cpp:307-314): c = cp + p^2 ((cq - cp) (p^2)^-1 mod q^2)
-    Acc.store(A2);
-    Op.store_const(K.mq.r2);
-    mont_mul_ss<S, AR>(A2, Acc, Op, Mq);  // cq R mod q^2
-    tab.put(P.ntab + kParkA1, A2);
-    tab.to_slot(P.ntab + kParkCp, Acc);
-    mont_mul_ss<S, AR>(A2, Acc, Op, Mq);  // cp R mod q^2   (cp < p^2 < R)
-    {
-      uint32_t A1[S];
-      tab.get(P.ntab + kParkA1, A1);
-      mod_sub<S>(A1, A2, Mq);  // (cq - cp) R mod q^2
-      Acc.store(A1);
-    }
-    Op.store_const(K.inv);
-    mont_mul_ss<S, AR>(A2, Acc, Op, Mq);  // t = (cq - cp) (p^2)^-1 mod q^2, plain
-    Op.store(A2);
-    {
-      uint32_t H[S], Cp[S];
-      tab.get(P.ntab + kParkCp, Cp);
-      mul_add_smod<S>(H, Cp, Op, Mp);  // c = cp + p^2 t; low S words left in Op
-      const int cl = 2 * P.L;
-#pragma unroll
-      for (int j = 0; j < S; j++)
-        if (j < cl) out[j] = Op.digit(j);
-#pragma unroll
-      for (int j = 0; j < S; j++)
-        if (S + j < cl) out[S + j] = H[j];
-    }
+    P.st[i] = status;
   }
 }
 
-// ------------------------------------------------------------------------------------------
 template <int S>
-struct CrtDecArgs {
-  CrtDecConsts<S> k;
-  Sched sp, sq;   // p-1, q-1
-  int ntab;
-  uint4* tab;
-  const uint32_t* c;  // count x 2L
-  uint32_t* m;        // count x L
-  int32_t* st;
+struct GarnerArgs {
+  ModCtx<S> mp, mq;
+  uint32_t inv[S];      // (p^2)^-1 mod q^2, plain
+  const uint32_t* cp;   // count x S
+  const uint32_t* cq;   // count x S
+  const int32_t* st;
+  uint32_t* c;          // count x 2L
   int L, count;
 };
 
-// One CRT half of decryption: returns false for a non-unit (p | c).
-//   x = c^(p-1) mod p^2,  u = (x - 1) / p  (exact),  mh = u * h_p mod p.
 template <int S>
-__device__ __forceinline__ bool dec_half(uint32_t (&Mh)[S / 2], const uint32_t* csrc, int cl, const Slot<S>& Acc,
-                                         const Slot<S>& Op, const GTable<S>& tab, int ntab, const Sched& sc,
-                                         const SMod<S>& M2, const uint32_t* r2, const uint32_t* r3, const SMod<S / 2>& M1,
-                                         const uint32_t* inv_lo, const uint32_t* h, const uint32_t* prime) {
-  constexpr int H = S / 2;
-  constexpr bool AR = Areg<S>::value;
-  uint32_t X[S];
-  Acc.store_global(csrc + S, cl - S);  // c_hi
-  Op.store_const(r3);
-  mont_mul_ss<S, AR>(X, Acc, Op, M2);  // c_hi R^2 = (c_hi 2^(32S)) R
-  tab.put(ntab + kParkA1, X);
-  Acc.store_global(csrc, cl < S ? cl : S);  // c_lo
-  Op.store_const(r2);
-  mont_mul_ss<S, AR>(X, Acc, Op, M2);  // c_lo R
-  {
-    uint32_t Y[S];
-    tab.get(ntab + kParkA1, Y);
-    mod_add<S>(X, Y, M2);  // c R mod p^2
+__global__ void __launch_bounds__(kThreadsPerBlock) garner_kernel(const __grid_constant__ GarnerArgs<S> P) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  smod_fill<S>(smem, P.mp.m);
+  smod_fill<S>(smem + S, P.mq.m);
+  __syncthreads();
+  const SMod<S> Mp{smem_addr(smem), P.mp.minv}, Mq{smem_addr(smem + S), P.mq.minv};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* slots = smem + 2 * S;
+  const Slot<S> A{smem_addr(slots + warp * (64 * S) + lane * 4)};
+  const Slot<S> B{smem_addr(slots + warp * (64 * S) + 32 * S + lane * 4)};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.count; i += gridDim.x * blockDim.x) {
+    uint32_t* out = P.c + (size_t)i * 2 * P.L;
+    if (P.st[i] != PCB_OK) {
+      for (int j = 0; j < 2 * P.L; j++) out[j] = 0;
+      continue;
+    }
+    uint32_t T[S], U[S];
+    B.store_const(P.mq.r2);
+    A.store_global(P.cq + (size_t)i * S, S);
+    mont_mul_ss<S, false, SMod<S>>(T, A, B, Mq);  // c_q R mod q^2
+    A.store_global(P.cp + (size_t)i * S, S);
+    mont_mul_ss<S, false, SMod<S>>(U, A, B, Mq);  // c_p R mod q^2 (c_p < p^2 < R)
+    mod_sub<S, SMod<S>>(T, U, Mq);
+    A.store(T);
+    B.store_const(P.inv);
+    mont_mul_ss<S, false, SMod<S>>(T, A, B, Mq);  // t = (c_q - c_p) (p^2)^-1 mod q^2, plain
+    B.store(T);
+    const uint32_t* cps = P.cp + (size_t)i * S;
+#pragma unroll
+    for (int j = 0; j < S; j++) U[j] = cps[j];
+    uint32_t H[S];
+    mul_add_smod<S>(H, U, B, Mp);  // c = c_p + p^2 t; low words left in B
+    const int cl = 2 * P.L;
+#pragma unroll
+    for (int j = 0; j < S; j++)
+      if (j < cl) out[j] = B.digit(j);
+#pragma unroll
+    for (int j = 0; j < S; j++)
+      if (S + j < cl) out[S + j] = H[j];
   }
-  Acc.store(X);
-  mont_pow<S, AR>(Acc, Op, tab, ntab, sc.ops, sc.n, M2);
-  Op.store_small(1);
-  mont_mul_ss<S, AR>(X, Acc, Op, M2);  // x = c^(p-1) mod p^2, plain
-  // x - 1 (x == 0 -> non-unit)
+}
+
+struct DecPrepArgs {
+  const uint32_t* c;   // count x 2L
+  const uint32_t* n2;  // 2L limbs (device)
+  int L;
+  int32_t* st;
+  int count;
+};
+
+__global__ void dec_prep_kernel(const __grid_constant__ DecPrepArgs P) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.count; i += gridDim.x * blockDim.x)
+    P.st[i] = lt_words(P.c + (size_t)i * 2 * P.L, 2 * P.L, P.n2, 2 * P.L) ? PCB_OK : PCB_E_CIPHER_RANGE;
+}
+
+template <int S>
+struct DecFinishArgs {
+  ModCtx<S / 2> sp, sq;     // p, q
+  uint32_t pinv_lo[S / 2];  // p^-1 mod 2^(16 S)
+  uint32_t qinv_lo[S / 2];
+  uint32_t hp[S / 2];       // h_p R_h mod p
+  uint32_t hq[S / 2];
+  uint32_t pinvq[S / 2];    // p^-1 mod q, plain
+  uint32_t p[S / 2], q[S / 2];
+  const uint32_t* xp;       // count x S: c^(p-1) mod p^2
+  const uint32_t* xq;
+  int32_t* st;
+  uint32_t* m;              // count x L
+  int L, count;
+};
+
+// u = (x - 1) / prime exactly (false if prime does not divide x - 1), then mh = u h mod prime.
+template <int S>
+__device__ __forceinline__ bool l_half(uint32_t (&Mh)[S / 2], const uint32_t* xsrc, const uint32_t* inv_lo,
+                                       const uint32_t* prime, const uint32_t* h, const Slot<S / 2>& A,
+                                       const Slot<S / 2>& B, const SMod<S / 2>& M1) {
+  constexpr int H = S / 2;
+  uint32_t X[S];
+#pragma unroll
+  for (int j = 0; j < S; j++) X[j] = xsrc[j];
   bool ok = !is_zero(X);
   uint32_t br;
   asm volatile("sub.cc.u32 %0, %0, 1;" : "+r"(X[0]));
@@ -258,159 +212,146 @@ __device__ __forceinline__ bool dec_half(uint32_t (&Mh)[S / 2], const uint32_t* 
     uint32_t lo[H];
 #pragma unroll
     for (int j = 0; j < H; j++) lo[j] = X[j];
-    mul_lo<H>(U, lo, inv_lo);  // u = (x-1) p^-1 mod 2^(32H)
+    mul_lo<H>(U, lo, inv_lo);  // (x - 1) prime^-1 mod 2^(32H)
   }
-  ok = mul_eq<H>(U, prime, X) && ok;  // exact division <=> x == 1 mod p
-  const Slot<H> Ah{Acc.a}, Oh{Op.a};
-  Ah.store(U);
-  Oh.store_const(h);
-  mont_mul_ss<H, true>(Mh, Ah, Oh, M1);  // u * h_p mod p
+  ok = mul_eq<H>(U, prime, X) && ok;  // exact division  <=>  x == 1 mod prime
+  A.store(U);
+  B.store_const(h);
+  mont_mul_ss<H, true, SMod<H>>(Mh, A, B, M1);  // u h mod prime
   return ok;
 }
 
 template <int S>
-__global__ void __launch_bounds__(kThreadsPerBlock) crt_decrypt_kernel(const __grid_constant__ CrtDecArgs<S> P) {
-  extern __shared__ __align__(16) uint32_t smem[];
+__global__ void __launch_bounds__(kThreadsPerBlock) dec_finish_kernel(const __grid_constant__ DecFinishArgs<S> P) {
   constexpr int H = S / 2;
-  const CrtDecConsts<S>& K = P.k;
-  smod_fill<S>(smem, K.mp.m);
-  smod_fill<S>(smem + S, K.mq.m);
-  smod_fill<H>(smem + 2 * S, K.sp.m);
-  smod_fill<H>(smem + 2 * S + H, K.sq.m);
+  extern __shared__ __align__(16) uint32_t smem[];
+  smod_fill<H>(smem, P.sp.m);
+  smod_fill<H>(smem + H, P.sq.m);
   __syncthreads();
-  const SMod<S> Mp_{smem_addr(smem), K.mp.minv}, Mq_{smem_addr(smem + S), K.mq.minv};
-  const SMod<H> Sp{smem_addr(smem + 2 * S), K.sp.minv}, Sq{smem_addr(smem + 2 * S + H), K.sq.minv};
+  const SMod<H> Sp{smem_addr(smem), P.sp.minv}, Sq{smem_addr(smem + H), P.sq.minv};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* slots = smem + 3 * S;
-  const Slot<S> Acc{smem_addr(slots + warp * (64 * S) + lane * 4)};
-  const Slot<S> Op{smem_addr(slots + warp * (64 * S) + 32 * S + lane * 4)};
-  const uint32_t nthr = gridDim.x * blockDim.x;
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  GTable<S> tab{P.tab, nthr, g};
-
-  for (int i = g; i < P.count; i += nthr) {
-    const uint32_t* src = P.c + (size_t)i * 2 * P.L;
+  uint32_t* slots = smem + 2 * H;
+  const Slot<H> A{smem_addr(slots + warp * (64 * H) + lane * 4)};
+  const Slot<H> B{smem_addr(slots + warp * (64 * H) + 32 * H + lane * 4)};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.count; i += gridDim.x * blockDim.x) {
     uint32_t* out = P.m + (size_t)i * P.L;
-    if (!lt_words(src, 2 * P.L, K.n2, 2 * P.L)) {  // c < n^2 (paillier.cpp:356)
-      if (P.st) P.st[i] = PCB_E_CIPHER_RANGE;
+    if (P.st[i] != PCB_OK) {
       for (int j = 0; j < P.L; j++) out[j] = 0;
       continue;
     }
-    bool ok;
-    {
-      uint32_t Mp[H];
-      ok = dec_half<S>(Mp, src, 2 * P.L, Acc, Op, tab, P.ntab, P.sp, Mp_, K.mp.r2, K.r3p, Sp, K.pinv_lo, K.hp, K.p);
-      uint32_t park[S];
-#pragma unroll
-      for (int j = 0; j < S; j++) park[j] = j < H ? Mp[j] : 0u;
-      tab.put(P.ntab + kParkCp, park);
-    }
-    uint32_t Mq[H];
-    ok = dec_half<S>(Mq, src, 2 * P.L, Acc, Op, tab, P.ntab, P.sq, Mq_, K.mq.r2, K.r3q, Sq, K.qinv_lo, K.hq, K.q) && ok;
+    uint32_t Mp[H], Mq[H];
+    bool ok = l_half<S>(Mp, P.xp + (size_t)i * S, P.pinv_lo, P.p, P.hp, A, B, Sp);
+    ok = l_half<S>(Mq, P.xq + (size_t)i * S, P.qinv_lo, P.q, P.hq, A, B, Sq) && ok;
     if (!ok) {
-      if (P.st) P.st[i] = PCB_E_NOT_UNIT;  // l_function (paillier.cpp:34-41)
+      P.st[i] = PCB_E_NOT_UNIT;  // l_function (paillier.cpp:34-41)
       for (int j = 0; j < P.L; j++) out[j] = 0;
       continue;
     }
-    // m = m_p + p * ((m_q - m_p) p^-1 mod q)
-    const Slot<H> Ah{Acc.a}, Oh{Op.a};
-    uint32_t Mp[H], T[H];
-    {
-      uint32_t park[S];
-      tab.get(P.ntab + kParkCp, park);
-#pragma unroll
-      for (int j = 0; j < H; j++) Mp[j] = park[j];
-    }
-    Oh.store_const(K.sq.r2);
-    Ah.store(Mq);
-    mont_mul_ss<H, true>(T, Ah, Oh, Sq);   // m_q R mod q
-    Ah.store(Mp);
-    mont_mul_ss<H, true>(Mq, Ah, Oh, Sq);  // m_p R mod q (reduces m_p mod q)
-    mod_sub<H>(T, Mq, Sq);
-    Ah.store(T);
-    Oh.store_const(K.pinvq);
-    mont_mul_ss<H, true>(T, Ah, Oh, Sq);   // t = (m_q - m_p) p^-1 mod q, plain
-    Oh.store(T);
+    // m = m_p + p ((m_q - m_p) p^-1 mod q)
+    uint32_t T[H], U[H];
+    B.store_const(P.sq.r2);
+    A.store(Mq);
+    mont_mul_ss<H, true, SMod<H>>(T, A, B, Sq);  // m_q R mod q
+    A.store(Mp);
+    mont_mul_ss<H, true, SMod<H>>(U, A, B, Sq);  // m_p R mod q
+    mod_sub<H, SMod<H>>(T, U, Sq);
+    A.store(T);
+    B.store_const(P.pinvq);
+    mont_mul_ss<H, true, SMod<H>>(T, A, B, Sq);  // t, plain
+    B.store(T);
     uint32_t Hi[H];
-    mul_add_smod<H>(Hi, Mp, Oh, Sp);
+    mul_add_smod<H>(Hi, Mp, B, Sp);
 #pragma unroll
     for (int j = 0; j < H; j++)
-      if (j < P.L) out[j] = Oh.digit(j);
+      if (j < P.L) out[j] = B.digit(j);
 #pragma unroll
     for (int j = 0; j < H; j++)
       if (H + j < P.L) out[H + j] = Hi[j];
-    if (P.st) P.st[i] = PCB_OK;
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// Launchers (called from abi.cu with the per-context constant blobs).
+// Launchers
 // ------------------------------------------------------------------------------------------
-template <int S>
-pcb_status launch_crt_encrypt(const CrtEncConsts<S>& k, Sched sp, Sched sq, int ntab, const uint32_t* m,
-                              int m_limbs, const uint32_t* r, int L, size_t count, uint32_t* c, int32_t* st,
-                              const double* qv, double zmin, double zmax, double delta, int fine, uint64_t* q_out,
-                              unsigned long long* clamps, cudaStream_t stream) {
-  CrtEncArgs<S> P;
-  P.k = k;
-  P.sp = sp;
-  P.sq = sq;
-  P.ntab = ntab;
-  P.m = m;
-  P.r = r;
-  P.c = c;
-  P.st = st;
-  P.m_limbs = m_limbs;
-  P.L = L;
-  P.count = (int)count;
-  P.qv = qv;
-  P.zmin = zmin;
-  P.zmax = zmax;
-  P.delta = delta;
-  P.fine = fine;
-  P.q_out = q_out;
-  P.clamps = clamps;
-  const size_t smem = (size_t)kThreadsPerBlock * S * 8 + 2 * S * 4;  // moduli + two slots per thread
-  int blocks = 0;
-  if (auto e = item_grid(crt_encrypt_kernel<S>, smem, count, &blocks)) return e;
-  const size_t nthr = (size_t)blocks * kThreadsPerBlock;
-  if (auto e = scratch_alloc(nthr * (ntab + kNumPark) * S * 4, (void**)&P.tab, stream)) return e;
-  crt_encrypt_kernel<S><<<blocks, kThreadsPerBlock, smem, stream>>>(P);
+static int small_grid(size_t count) {
+  size_t b = (count + 255) / 256;
+  return (int)(b < 4096 ? (b ? b : 1) : 4096);
+}
+
+pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, double zmin, double zmax, double delta,
+                           int fine, uint32_t* m_out, int m_out_limbs, uint64_t* q_out, unsigned long long* clamps,
+                           const uint32_t* r, const uint32_t* n_dev, int L, int32_t* st, size_t count,
+                           cudaStream_t stream) {
+  EncPrepArgs P{m, m_limbs, v, zmin, zmax, delta, fine, m_out, m_out_limbs, q_out, clamps, r, n_dev, L, st, (int)count};
+  enc_prep_kernel<<<small_grid(count), 256, 0, stream>>>(P);
   count_launch();
-  scratch_free(P.tab, stream);
+  return cuda_check(cudaGetLastError());
+}
+
+pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int32_t* st, size_t count,
+                           cudaStream_t stream) {
+  DecPrepArgs P{c, n2_dev, L, st, (int)count};
+  dec_prep_kernel<<<small_grid(count), 256, 0, stream>>>(P);
+  count_launch();
   return cuda_check(cudaGetLastError());
 }
 
 template <int S>
-pcb_status launch_crt_decrypt(const CrtDecConsts<S>& k, Sched sp, Sched sq, int ntab, const uint32_t* c, int L,
-                              size_t count, uint32_t* m, int32_t* st, cudaStream_t stream) {
-  CrtDecArgs<S> P;
-  P.k = k;
-  P.sp = sp;
-  P.sq = sq;
-  P.ntab = ntab;
-  P.c = c;
-  P.m = m;
+pcb_status launch_garner(const CrtEncConsts<S>& k, const uint32_t* cp, const uint32_t* cq, const int32_t* st,
+                         uint32_t* c, int L, size_t count, cudaStream_t stream) {
+  GarnerArgs<S> P;
+  P.mp = k.mp;
+  P.mq = k.mq;
+  for (int j = 0; j < S; j++) P.inv[j] = k.inv[j];
+  P.cp = cp;
+  P.cq = cq;
   P.st = st;
+  P.c = c;
   P.L = L;
   P.count = (int)count;
-  const size_t smem = (size_t)kThreadsPerBlock * S * 8 + 3 * S * 4;  // moduli + two slots per thread
+  const size_t smem = (size_t)kThreadsPerBlock * S * 8 + 2 * S * 4;
   int blocks = 0;
-  if (auto e = item_grid(crt_decrypt_kernel<S>, smem, count, &blocks)) return e;
-  const size_t nthr = (size_t)blocks * kThreadsPerBlock;
-  if (auto e = scratch_alloc(nthr * (ntab + kNumPark) * S * 4, (void**)&P.tab, stream)) return e;
-  crt_decrypt_kernel<S><<<blocks, kThreadsPerBlock, smem, stream>>>(P);
+  if (auto e = item_grid(garner_kernel<S>, smem, count, &blocks)) return e;
+  garner_kernel<S><<<blocks, kThreadsPerBlock, smem, stream>>>(P);
   count_launch();
-  scratch_free(P.tab, stream);
   return cuda_check(cudaGetLastError());
 }
 
-#define PCB_INSTANTIATE(S)                                                                                          \
-  template pcb_status launch_crt_encrypt<S>(const CrtEncConsts<S>&, Sched, Sched, int, const uint32_t*, int,       \
-                                            const uint32_t*, int, size_t, uint32_t*, int32_t*, const double*, double, \
-                                            double, double, int, uint64_t*, unsigned long long*, cudaStream_t);      \
-  template pcb_status launch_crt_decrypt<S>(const CrtDecConsts<S>&, Sched, Sched, int, const uint32_t*, int, size_t, \
-                                            uint32_t*, int32_t*, cudaStream_t);
+template <int S>
+pcb_status launch_dec_finish(const CrtDecConsts<S>& k, const uint32_t* xp, const uint32_t* xq, int32_t* st,
+                             uint32_t* m, int L, size_t count, cudaStream_t stream) {
+  constexpr int H = S / 2;
+  DecFinishArgs<S> P;
+  P.sp = k.sp;
+  P.sq = k.sq;
+  for (int j = 0; j < H; j++) {
+    P.pinv_lo[j] = k.pinv_lo[j];
+    P.qinv_lo[j] = k.qinv_lo[j];
+    P.hp[j] = k.hp[j];
+    P.hq[j] = k.hq[j];
+    P.pinvq[j] = k.pinvq[j];
+    P.p[j] = k.p[j];
+    P.q[j] = k.q[j];
+  }
+  P.xp = xp;
+  P.xq = xq;
+  P.st = st;
+  P.m = m;
+  P.L = L;
+  P.count = (int)count;
+  const size_t smem = (size_t)kThreadsPerBlock * H * 8 + 2 * H * 4;
+  int blocks = 0;
+  if (auto e = item_grid(dec_finish_kernel<S>, smem, count, &blocks)) return e;
+  dec_finish_kernel<S><<<blocks, kThreadsPerBlock, smem, stream>>>(P);
+  count_launch();
+  return cuda_check(cudaGetLastError());
+}
+
+#define PCB_INSTANTIATE(S)                                                                                         \
+  template pcb_status launch_garner<S>(const CrtEncConsts<S>&, const uint32_t*, const uint32_t*, const int32_t*,  \
+                                       uint32_t*, int, size_t, cudaStream_t);                                      \
+  template pcb_status launch_dec_finish<S>(const CrtDecConsts<S>&, const uint32_t*, const uint32_t*, int32_t*,    \
+                                           uint32_t*, int, size_t, cudaStream_t);
 PCB_INSTANTIATE(32)
 PCB_INSTANTIATE(64)
 

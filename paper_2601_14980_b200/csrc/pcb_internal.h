@@ -77,8 +77,5 @@ inline int kernel_width_wide(uint32_t limbs) {
   return 0;
 }
 
-pcb_status modexp_dispatch(int S, const uint32_t* m, const uint32_t* r2, uint32_t minv, const uint32_t* sched_d,
-                           int nsched, int ntab, bool exp_zero, const uint32_t* x_d, uint32_t x_limbs, size_t count,
-                           uint32_t* y_d, cudaStream_t st);
 
 }  // namespace pcb
