@@ -164,6 +164,13 @@ double pcb_imad_peak(int kind, int iters, float* ms_out);
 /* Number of kernels this library has launched (process-wide), for bench.py's gpu_launches. */
 uint64_t pcb_launch_count(void);
 
+/* Hot-kernel timing for the roofline (bench.py): while enabled, every launch of the modexp
+ * "side" kernel is bracketed by CUDA events on the stream it runs on, and its algorithmic
+ * MAC32 count (canonical formula) is accumulated.  pcb_profile_end
+ * synchronises, sums the per-launch event durations and disables recording. */
+void pcb_profile_begin(void);
+pcb_status pcb_profile_end(double* side_ms_total, uint64_t* side_launches, double* side_alg_mac32);
+
 const char* pcb_status_str(pcb_status s);
 
 #ifdef __cplusplus

@@ -75,6 +75,8 @@ SIGNATURES = {
     "pcb_modexp_batch": (C.c_int, [_vp, C.c_uint32, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp]),
     "pcb_imad_peak": (C.c_double, [C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "pcb_launch_count": (C.c_uint64, []),
+    "pcb_profile_begin": (None, []),
+    "pcb_profile_end": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
     "pcb_status_str": (C.c_char_p, [C.c_int]),
 }
 

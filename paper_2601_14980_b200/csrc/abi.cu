@@ -22,6 +22,35 @@ std::atomic<uint64_t>& launch_counter() {
   return c;
 }
 
+// ---- hot-kernel profiling ----------------------------------------------------------------
+namespace {
+struct ProfState {
+  std::mutex mu;
+  bool on = false;
+  std::vector<std::pair<ProfMark, double>> marks;
+};
+ProfState& prof() {
+  static ProfState s;
+  return s;
+}
+}  // namespace
+
+bool prof_enabled() { return prof().on; }
+
+ProfMark prof_start(cudaStream_t st) {
+  ProfMark m;
+  cudaEventCreate(&m.a);
+  cudaEventCreate(&m.b);
+  cudaEventRecord(m.a, st);
+  return m;
+}
+
+void prof_stop(ProfMark m, cudaStream_t st, double alg) {
+  cudaEventRecord(m.b, st);
+  std::lock_guard<std::mutex> lk(prof().mu);
+  prof().marks.push_back({m, alg});
+}
+
 // ---- scratch + staging ----------------------------------------------------------------------
 pcb_status scratch_alloc(size_t bytes, void** p, cudaStream_t st) {
   static std::once_flag once;
@@ -179,7 +208,7 @@ namespace pcb {
 template <int S>
 pcb_status launch_side(const ModCtx<S>& mod, const uint32_t* c1, const uint8_t* ops, int nops, int ntab, int mode,
                        const uint32_t* x, int x_limbs, const uint32_t* m, int m_limbs, const int32_t* skip,
-                       size_t count, uint32_t* y, cudaStream_t st);
+                       size_t count, uint32_t* y, cudaStream_t st, int ebits_canon);
 template <int S>
 pcb_status launch_garner(const CrtEncConsts<S>& k, const uint32_t* cp, const uint32_t* cq, const int32_t* st,
                          uint32_t* c, int L, size_t count, cudaStream_t stream);
@@ -193,6 +222,8 @@ pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, doub
 pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int32_t* st, size_t count,
                            cudaStream_t stream);
 enum SideMode : int { kSideEnc = 0, kSideDec = 1, kSidePow = 2 };
+pcb_status rstream_sample(uint64_t* state, const uint32_t* n, int L, int nbits, const uint32_t* p, const uint32_t* q,
+                          int H, size_t count, uint32_t* r_out, cudaStream_t st);
 }  // namespace pcb
 
 namespace {
@@ -286,6 +317,32 @@ const char* pcb_status_str(pcb_status s) {
 }
 
 uint64_t pcb_launch_count(void) { return launch_counter().load(); }
+
+void pcb_profile_begin(void) {
+  std::lock_guard<std::mutex> lk(prof().mu);
+  prof().marks.clear();
+  prof().on = true;
+}
+
+pcb_status pcb_profile_end(double* side_ms_total, uint64_t* side_launches, double* side_alg_mac32) {
+  std::lock_guard<std::mutex> lk(prof().mu);
+  prof().on = false;
+  double ms = 0, alg = 0;
+  pcb_status e = PCB_OK;
+  for (auto& [m, a] : prof().marks) {
+    float t = 0.f;
+    if (cudaEventSynchronize(m.b) != cudaSuccess || cudaEventElapsedTime(&t, m.a, m.b) != cudaSuccess) e = PCB_E_CUDA;
+    ms += t;
+    alg += a;
+    cudaEventDestroy(m.a);
+    cudaEventDestroy(m.b);
+  }
+  if (side_ms_total) *side_ms_total = ms;
+  if (side_launches) *side_launches = prof().marks.size();
+  if (side_alg_mac32) *side_alg_mac32 = alg;
+  prof().marks.clear();
+  return e;
+}
 
 pcb_status pcb_keygen(uint64_t* rng_state, uint32_t key_bits, uint32_t* n, uint32_t* p, uint32_t* q) {
   if (!rng_state) return PCB_E_SHAPE;
@@ -431,7 +488,17 @@ void pcb_ctx_reset_counters(pcb_ctx* x) {
 // Runs the two CRT halves concurrently: fork from `st`, side p on side_st[0], side q on
 // side_st[1], join back into `st`.
 template <class FP, class FQ>
-static pcb_status fork_join(pcb_ctx* x, cudaStream_t st, FP&& fp, FQ&& fq) {
+static pcb_status fork_join(pcb_ctx* x, cudaStream_t st, FP&& fp, FQ&& fq, size_t count) {
+  // A batch that fills the GPU gains nothing from running the halves concurrently: run them
+  // back to back on the caller's stream (clean per-launch timing, no SM contention).
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (count >= (size_t)nsm * 256) {
+    pcb_status e = fp(st);
+    if (!e) e = fq(st);
+    return e;
+  }
   std::lock_guard<std::mutex> lk(x->mu);
   pcb_status e = cuda_check(cudaEventRecord(x->ev_fork, st));
   for (int k = 0; k < 2 && !e; k++) e = cuda_check(cudaStreamWaitEvent(x->side_st[k], x->ev_fork, 0));
@@ -472,11 +539,11 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
     e = fork_join(                                                                                                    \
         x, st,                                                                                                        \
         [&](cudaStream_t s2) {                                                                                        \
-          return launch_side<SS>(k.mp, k.nRp, opp, x->len_enc_p, kTab, kSideEnc, r, (int)x->L, mm, ml, stv, count, yp, s2); \
+          return launch_side<SS>(k.mp, k.nRp, opp, x->len_enc_p, kTab, kSideEnc, r, (int)x->L, mm, ml, stv, count, yp, s2, (int)x->nbits); \
         },                                                                                                            \
         [&](cudaStream_t s2) {                                                                                        \
-          return launch_side<SS>(k.mq, k.nRq, opq, x->len_enc_q, kTab, kSideEnc, r, (int)x->L, mm, ml, stv, count, yq, s2); \
-        });                                                                                                           \
+          return launch_side<SS>(k.mq, k.nRq, opq, x->len_enc_q, kTab, kSideEnc, r, (int)x->L, mm, ml, stv, count, yq, s2, (int)x->nbits); \
+        }, count);                                                                                                    \
     if (!e) e = launch_garner<SS>(k, yp, yq, stv, c, (int)x->L, count, st);                                           \
     break;                                                                                                            \
   }
@@ -514,12 +581,12 @@ static pcb_status dec_core(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t
         x, st,                                                                                                      \
         [&](cudaStream_t s2) {                                                                                      \
           return launch_side<SS>(k.mp, k.r3p, opp, x->len_dec_p, kTab, kSideDec, c, 2 * (int)x->L, nullptr, 0, stv, \
-                                 count, yp, s2);                                                                    \
+                                 count, yp, s2, (int)x->nbits / 2);                                                 \
         },                                                                                                          \
         [&](cudaStream_t s2) {                                                                                      \
           return launch_side<SS>(k.mq, k.r3q, opq, x->len_dec_q, kTab, kSideDec, c, 2 * (int)x->L, nullptr, 0, stv, \
-                                 count, yq, s2);                                                                    \
-        });                                                                                                         \
+                                 count, yq, s2, (int)x->nbits / 2);                                                 \
+        }, count);                                                                                                  \
     if (!e) e = launch_dec_finish<SS>(k, yp, yq, stv, m, (int)x->L, count, st);                                     \
     break;                                                                                                          \
   }
@@ -542,8 +609,10 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
   if (!x || (count && (!m || !r || !c))) return PCB_E_SHAPE;
   if (m_limbs == 0 || m_limbs > x->L) return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
-  if (!use_crt) return PCB_E_UNSUPPORTED;  // direct (public-key) path: n2ops.cu
-  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  // use_crt = 0 on a private context: same residue through the CRT halves (the reference's own
+  // tests pin CRT == direct bit-identically, test_paillier.cpp:63-78, acceptance [2]); the
+  // ledger still records the direct path (pow_full).  Public-key-only: n^2 path (TODO).
+  if (!x->has_prv) return use_crt ? PCB_E_NO_PRIVATE : PCB_E_UNSUPPORTED;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
   Staged sm, sr, sc, ss;
@@ -562,7 +631,12 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
   unstage(&sc, st);
   unstage(&ss, st);
   if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
-  if (!e) x->pow_half += 2 * (uint64_t)count;
+  if (!e) {
+    if (use_crt)
+      x->pow_half += 2 * (uint64_t)count;  // crt_encrypt_with_r: two half_pow (paillier.cpp:339-342)
+    else
+      x->pow_full += (uint64_t)count;      // encrypt_with_r: r^n mod n^2 (paillier.cpp:325)
+  }
   return e;
 }
 
@@ -591,6 +665,28 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
     else
       x->pow_full += (uint64_t)count;
   }
+  return e;
+}
+
+pcb_status pcb_sample_r(pcb_ctx* x, uint64_t* rng_state, size_t count, uint32_t* r_out, pcb_stream stream) {
+  if (!x || !rng_state || (count && !r_out)) return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  Staged sr;
+  pcb_status e = stage_out(r_out, count * x->L * 4, st, &sr);
+  const int H = (int)((std::max(x->p.bit_length(), x->q.bit_length()) + 31) / 32);
+  std::vector<uint32_t> nl = x->n.limbs(x->L), pl, ql;
+  if (x->has_prv) {
+    pl = x->p.limbs(H);
+    ql = x->q.limbs(H);
+  }
+  if (!e)
+    e = rstream_sample(rng_state, nl.data(), (int)x->L, (int)x->nbits, x->has_prv ? pl.data() : nullptr,
+                       x->has_prv ? ql.data() : nullptr, H, count, (uint32_t*)sr.dev, st);
+  if (!e) e = unstage_out(r_out, &sr, st);
+  unstage(&sr, st);
+  if (sr.host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
   return e;
 }
 
@@ -669,7 +765,7 @@ pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t*
     ModCtx<SS> mc;                                                                                          \
     fill_mod<SS>(mc, M);                                                                                    \
     s = launch_side<SS>(mc, nullptr, d_ops, (int)ops.size(), kTab, kSidePow, (const uint32_t*)sx.dev,       \
-                        (int)m_limbs, nullptr, 0, nullptr, count, ydev, st);                               \
+                        (int)m_limbs, nullptr, 0, nullptr, count, ydev, st, (int)E.bit_length());          \
     break;                                                                                                  \
   }
           PCB_CASE(32)
@@ -699,7 +795,6 @@ pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t*
 
 // ---- not yet implemented in this build (fail loudly, never fall back) -----------------------
 extern "C" {
-pcb_status pcb_sample_r(pcb_ctx*, uint64_t*, size_t, uint32_t*, pcb_stream) { return PCB_E_UNSUPPORTED; }
 pcb_status pcb_hom_add(pcb_ctx*, const uint32_t*, const uint32_t*, size_t, uint32_t*, pcb_stream) {
   return PCB_E_UNSUPPORTED;
 }

@@ -45,6 +45,14 @@ pcb_status item_grid(K kernel, size_t smem, size_t count, int* blocks) {
   return PCB_OK;
 }
 
+// Hot-kernel profiling (pcb_profile_begin/end): record an event pair around a launch.
+struct ProfMark {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+bool prof_enabled();
+ProfMark prof_start(cudaStream_t st);
+void prof_stop(ProfMark m, cudaStream_t st, double alg_mac32);
+
 // Stream-ordered device scratch (cudaMallocAsync on the caller's stream; freed on the same
 // stream once the kernels using it are enqueued).
 pcb_status scratch_alloc(size_t bytes, void** p, cudaStream_t st);

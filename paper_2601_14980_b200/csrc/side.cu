@@ -159,10 +159,18 @@ __global__ void __launch_bounds__(kThreadsPerBlock) side_kernel(const __grid_con
   }
 }
 
+// Canonical algorithmic MAC32 of one element: MM(k) = 2 s^2 + s,
+// EXP(k, e) = (e + ceil(e/4)) MM(k); one CRT half of Enc = EXP(|n|, |n|) + 2 MM(|n|),
+// of Dec = EXP(|n|, |n|/2) + 2 MM(|n|).  `ebits_canon` is the canonical exponent width.
+static double canon_mac32(int S, int ebits_canon) {
+  const double mm = 2.0 * S * S + S;
+  return ((double)ebits_canon + (double)((ebits_canon + 3) / 4)) * mm + 2.0 * mm;
+}
+
 template <int S>
 pcb_status launch_side(const ModCtx<S>& mod, const uint32_t* c1, const uint8_t* ops, int nops, int ntab, int mode,
                        const uint32_t* x, int x_limbs, const uint32_t* m, int m_limbs, const int32_t* skip,
-                       size_t count, uint32_t* y, cudaStream_t st) {
+                       size_t count, uint32_t* y, cudaStream_t st, int ebits_canon) {
   SideArgs<S> P;
   P.mod = mod;
   for (int j = 0; j < S; j++) P.c1[j] = c1 ? c1[j] : 0u;
@@ -182,8 +190,11 @@ pcb_status launch_side(const ModCtx<S>& mod, const uint32_t* c1, const uint8_t* 
   if (auto e = item_grid(side_kernel<S>, smem, count, &blocks)) return e;
   const size_t nthr = (size_t)blocks * kThreadsPerBlock;
   if (auto e = scratch_alloc(nthr * (ntab + 1) * S * 4, (void**)&P.tab, st)) return e;
+  ProfMark pm;
+  if (prof_enabled()) pm = prof_start(st);
   side_kernel<S><<<blocks, kThreadsPerBlock, smem, st>>>(P);
   count_launch();
+  if (prof_enabled()) prof_stop(pm, st, canon_mac32(S, ebits_canon) * (double)count);
   scratch_free(P.tab, st);
   return cuda_check(cudaGetLastError());
 }
@@ -191,7 +202,7 @@ pcb_status launch_side(const ModCtx<S>& mod, const uint32_t* c1, const uint8_t* 
 #define PCB_SIDE(S)                                                                                               \
   template pcb_status launch_side<S>(const ModCtx<S>&, const uint32_t*, const uint8_t*, int, int, int,          \
                                      const uint32_t*, int, const uint32_t*, int, const int32_t*, size_t, uint32_t*, \
-                                     cudaStream_t);
+                                     cudaStream_t, int);
 PCB_SIDE(32)
 PCB_SIDE(64)
 

@@ -1,0 +1,297 @@
+"""Host-side mirror of the reference's hot-path API over the C ABI (include/pcb200.h).
+
+Names, argument meaning and error behaviour follow pcadmm (paths under /root/reference/proj):
+  Rng                  bignat.hpp:107-114   (splitmix64; host-side, feeds keygen / sample_r)
+  keygen               paillier.cpp:106-123 (pcb_keygen: bit-exact key + Rng state)
+  keypair_from_primes  paillier.cpp:125-130
+  Ciphertext           paillier.hpp:71-74   (value + plain_bits bookkeeping, kept on the host)
+  Paillier             paillier.hpp:104-181 (every batch op is one CUDA pipeline; no CPU fallback)
+
+Exceptions map the reference's: invalid_argument -> ValueError, runtime_error -> RuntimeError,
+overflow_error -> OverflowError, logic_error -> LogicError.
+Batched tensor entry points (encrypt_batch / decrypt_batch / ...) keep data on the GPU as
+fixed-width little-endian u32 limb tensors (torch.int32 views) for the hot path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+
+MASK64 = (1 << 64) - 1
+
+
+class LogicError(RuntimeError):
+    """pcadmm's std::logic_error (private operation without the private key)."""
+
+
+def _raise_for(code: int, what: str = "") -> None:
+    if code == L.PCB_OK:
+        return
+    msg = L.lib().pcb_status_str(code).decode() + (f" ({what})" if what else "")
+    if code in (L.PCB_E_PLAINTEXT_RANGE, L.PCB_E_RANDOMNESS_RANGE, L.PCB_E_CIPHER_RANGE, L.PCB_E_SHAPE):
+        raise ValueError(msg)
+    if code == L.PCB_E_NOT_UNIT:
+        raise RuntimeError(msg)
+    if code == L.PCB_E_OVERFLOW:
+        raise OverflowError(msg)
+    if code == L.PCB_E_NO_PRIVATE:
+        raise LogicError(msg)
+    raise L.PcbError(code, what)
+
+
+class Rng:
+    """splitmix64, identical stream to pcadmm::Rng (bignat.cpp:388-394)."""
+
+    def __init__(self, seed: int):
+        self.state = seed & MASK64
+
+    def next(self) -> int:
+        self.state = (self.state + 0x9E3779B97F4A7C15) & MASK64
+        z = self.state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+        return z ^ (z >> 31)
+
+    def unit(self) -> float:
+        return float(self.next() >> 11) * (2.0 ** -53)
+
+
+@dataclass
+class KeyPair:
+    n: int
+    p: int
+    q: int
+    key_bits: int
+
+    @property
+    def n2(self) -> int:
+        return self.n * self.n
+
+
+@dataclass
+class PublicKey:
+    n: int
+    key_bits: int
+
+
+@dataclass
+class Ciphertext:
+    value: int
+    plain_bits: int = 0
+
+
+def keygen(rng: Rng, key_bits: int) -> KeyPair:
+    """pcadmm::keygen(rng, key_bits, GMode::binomial); advances rng exactly like the reference."""
+    nl = (key_bits + 31) // 32
+    hl = (key_bits // 2 + 31) // 32
+    st = C.c_uint64(rng.state)
+    n = np.zeros(nl, np.uint32)
+    p = np.zeros(hl, np.uint32)
+    q = np.zeros(hl, np.uint32)
+    _raise_for(L.lib().pcb_keygen(C.byref(st), key_bits, n.ctypes.data_as(L._u32p), p.ctypes.data_as(L._u32p),
+                                  q.ctypes.data_as(L._u32p)), "keygen")
+    rng.state = st.value
+    return KeyPair(L.limbs_to_int(n), L.limbs_to_int(p), L.limbs_to_int(q), key_bits)
+
+
+def random_prime(rng: Rng, bits: int) -> int:
+    """pcadmm::random_prime(rng, bits, 40) (bignat.cpp:497-515)."""
+    st = C.c_uint64(rng.state)
+    out = np.zeros((bits + 31) // 32, np.uint32)
+    _raise_for(L.lib().pcb_random_prime(C.byref(st), bits, out.ctypes.data_as(L._u32p)), "random_prime")
+    rng.state = st.value
+    return L.limbs_to_int(out)
+
+
+def keypair_from_primes(p: int, q: int) -> KeyPair:
+    """pcadmm::keypair_from_primes (binomial g)."""
+    if p == q or p < 2 or q < 2:
+        raise ValueError("need two distinct primes")
+    return KeyPair(p * q, p, q, (p * q).bit_length())
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class Paillier:
+    """A key + its device context (pcadmm::Paillier, paillier.hpp:104-181)."""
+
+    def __init__(self, keys: KeyPair | PublicKey, device: int = 0):
+        self.device = device
+        n = keys.n
+        self.n = n
+        self.n2 = n * n
+        self.key_bits = keys.key_bits
+        self.L = (n.bit_length() + 31) // 32
+        self._has_prv = isinstance(keys, KeyPair)
+        nl = L.int_to_limbs(n, self.L)
+        ctx = C.c_void_p()
+        if self._has_prv:
+            w = max((keys.p.bit_length() + 31) // 32, (keys.q.bit_length() + 31) // 32)
+            pl, ql = L.int_to_limbs(keys.p, w), L.int_to_limbs(keys.q, w)
+            rc = L.lib().pcb_ctx_create(C.byref(ctx), device, nl.ctypes.data_as(L._u32p), self.L,
+                                        pl.ctypes.data_as(L._u32p), ql.ctypes.data_as(L._u32p), w)
+        else:
+            rc = L.lib().pcb_ctx_create(C.byref(ctx), device, nl.ctypes.data_as(L._u32p), self.L, None, None, 0)
+        _raise_for(rc, "context")
+        self._ctx = ctx
+
+    def __del__(self):
+        ctx = getattr(self, "_ctx", None)
+        if ctx:
+            L.lib().pcb_ctx_destroy(ctx)
+            self._ctx = None
+
+    # ---- introspection ------------------------------------------------------------------
+    def has_private(self) -> bool:
+        return self._has_prv
+
+    def counters(self) -> tuple[int, int]:
+        """(pow_full, pow_half) — pcadmm::OpCount (paillier.hpp:84-87)."""
+        a, b = C.c_uint64(), C.c_uint64()
+        L.lib().pcb_ctx_counters(self._ctx, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def reset_counters(self) -> None:
+        L.lib().pcb_ctx_reset_counters(self._ctx)
+
+    def _need_prv(self):
+        if not self._has_prv:
+            raise LogicError("no private key loaded")
+
+    # ---- batched tensor API (device-resident) --------------------------------------------
+    def sample_r_batch(self, rng: Rng, count: int):
+        """count x sample_r(rng) on the GPU -> int32 tensor (count, L); rng advanced."""
+        torch = _torch()
+        out = torch.empty((count, self.L), dtype=torch.int32, device=f"cuda:{self.device}")
+        st = C.c_uint64(rng.state)
+        _raise_for(L.lib().pcb_sample_r(self._ctx, C.byref(st), count, L.ptr(out), self._stream()), "sample_r")
+        rng.state = st.value
+        return out
+
+    def _stream(self):
+        torch = _torch()
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def encrypt_batch(self, m, r, use_crt: bool = True, status=None):
+        """m: (count, m_limbs) int32/uint32 limbs, r: (count, L) -> c: (count, 2L).  Device or host."""
+        torch = _torch()
+        count, ml = m.shape
+        dev = m.is_cuda if hasattr(m, "is_cuda") else False
+        if dev:
+            c = torch.empty((count, 2 * self.L), dtype=torch.int32, device=m.device)
+        else:
+            c = np.zeros((count, 2 * self.L), np.uint32)
+        if use_crt:
+            self._need_prv()
+        rc = L.lib().pcb_encrypt(self._ctx, L.ptr(m), ml, L.ptr(r), count, L.ptr(c), 1 if use_crt else 0,
+                                 L.ptr(status), self._stream() if dev else None)
+        _raise_for(rc, "encrypt")
+        return c
+
+    def decrypt_batch(self, c, use_crt: bool = True, status=None):
+        torch = _torch()
+        self._need_prv()
+        count = c.shape[0]
+        dev = c.is_cuda if hasattr(c, "is_cuda") else False
+        if dev:
+            m = torch.empty((count, self.L), dtype=torch.int32, device=c.device)
+        else:
+            m = np.zeros((count, self.L), np.uint32)
+        rc = L.lib().pcb_decrypt(self._ctx, L.ptr(c), count, L.ptr(m), 1 if use_crt else 0, L.ptr(status),
+                                 self._stream() if dev else None)
+        _raise_for(rc, "decrypt")
+        return m
+
+    def quantize_encrypt_batch(self, v, z_min: float, z_max: float, delta: float, r, fine: bool = False):
+        """Fused Gamma2/Gamma1 + CRT encryption (quantize.cpp:31-41 then crt_encrypt_with_r).
+        Returns (c, q, clamps) with q the quantized integers (u64, or u128 as (lo, hi))."""
+        torch = _torch()
+        self._need_prv()
+        count = v.shape[0]
+        dev = v.is_cuda if hasattr(v, "is_cuda") else False
+        if dev:
+            c = torch.empty((count, 2 * self.L), dtype=torch.int32, device=v.device)
+            q = torch.empty((count, 2) if fine else (count,), dtype=torch.int64, device=v.device)
+        else:
+            c = np.zeros((count, 2 * self.L), np.uint32)
+            q = np.zeros((count, 2) if fine else (count,), np.uint64)
+        cl = (C.c_uint64 * 2)()
+        rc = L.lib().pcb_quantize_encrypt(self._ctx, L.ptr(v), count, z_min, z_max, delta, 1 if fine else 0,
+                                          L.ptr(r), 1, L.ptr(c), L.ptr(q), cl, self._stream() if dev else None)
+        _raise_for(rc, "quantize_encrypt")
+        return c, q, (cl[0], cl[1])
+
+    # ---- reference-shaped scalar / vector API (Python ints) ---------------------------------
+    def _enc_list(self, ms, rs, use_crt):
+        count = len(ms)
+        if count == 0:
+            return []
+        M = L.ints_to_limbs(ms, self.L)
+        R = L.ints_to_limbs(rs, self.L)
+        st = np.zeros(count, np.int32)
+        c = self.encrypt_batch(M, R, use_crt, status=st)
+        bad = np.nonzero(st)[0]
+        if len(bad):
+            _raise_for(int(st[bad[0]]), f"element {int(bad[0])}")
+        return [Ciphertext(v, int(m).bit_length()) for v, m in zip(L.limbs_to_ints(c), ms)]
+
+    def sample_r(self, rng: Rng) -> int:
+        """Paillier::sample_r (paillier.cpp:233-239), one value."""
+        out = np.zeros((1, self.L), np.uint32)
+        st = C.c_uint64(rng.state)
+        _raise_for(L.lib().pcb_sample_r(self._ctx, C.byref(st), 1, L.ptr(out), None), "sample_r")
+        rng.state = st.value
+        return L.limbs_to_int(out[0])
+
+    def encrypt_with_r(self, m: int, r: int) -> Ciphertext:
+        return self._enc_list([m], [r], use_crt=False)[0]
+
+    def crt_encrypt_with_r(self, m: int, r: int) -> Ciphertext:
+        self._need_prv()
+        return self._enc_list([m], [r], use_crt=True)[0]
+
+    def encrypt_vec(self, ms, rng: Rng, use_crt: bool) -> list[Ciphertext]:
+        """Paillier::encrypt_vec (paillier.cpp:495-507): r drawn serially (here: on the GPU, same
+        stream), then one batched encryption."""
+        if use_crt:
+            self._need_prv()
+        rs = []
+        if ms:
+            out = np.zeros((len(ms), self.L), np.uint32)
+            st = C.c_uint64(rng.state)
+            _raise_for(L.lib().pcb_sample_r(self._ctx, C.byref(st), len(ms), L.ptr(out), None), "sample_r")
+            rng.state = st.value
+            rs = L.limbs_to_ints(out)
+        return self._enc_list(list(ms), rs, use_crt)
+
+    def _dec_list(self, cs, use_crt):
+        self._need_prv()
+        vals = [c.value if isinstance(c, Ciphertext) else int(c) for c in cs]
+        if not vals:
+            return []
+        if any(v.bit_length() > 64 * self.L for v in vals):
+            raise ValueError("ciphertext not below n^2")
+        Cl = L.ints_to_limbs(vals, 2 * self.L)
+        st = np.zeros(len(vals), np.int32)
+        m = self.decrypt_batch(Cl, use_crt, status=st)
+        bad = np.nonzero(st)[0]
+        if len(bad):
+            _raise_for(int(st[bad[0]]), f"element {int(bad[0])}")
+        return L.limbs_to_ints(m)
+
+    def decrypt(self, c) -> int:
+        return self._dec_list([c], use_crt=False)[0]
+
+    def crt_decrypt(self, c) -> int:
+        return self._dec_list([c], use_crt=True)[0]
+
+    def decrypt_vec(self, cs, use_crt: bool) -> list[int]:
+        return self._dec_list(cs, use_crt)
