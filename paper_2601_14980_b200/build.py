@@ -34,6 +34,7 @@ SOURCES = [
     "abi.cu",
     "paillier.cu",
     "side.cu",
+    "side28.cu",
     "rstream.cu",
     "imad_peak.cu",
     "host/hbn.cpp",

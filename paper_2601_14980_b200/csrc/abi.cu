@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -176,6 +177,36 @@ std::vector<uint8_t> build_ops(const HBN& e, int w) {
   return ops;
 }
 
+// radix-2^r limbs of v (N limbs)
+std::vector<uint32_t> radix_limbs(const HBN& v, int rb, int n) {
+  std::vector<uint32_t> out(n, 0);
+  for (int j = 0; j < n; j++) {
+    uint32_t x = 0;
+    for (int b = 0; b < rb; b++)
+      if (v.bit((size_t)j * rb + b)) x |= 1u << b;
+    out[j] = x;
+  }
+  return out;
+}
+
+// Constants of one modulus for the radix-2^r core: m limbs, R^2, c1 (caller), minv mod 2^r.
+struct R28Mod {
+  std::vector<uint32_t> mlimb, mword, r2;
+  uint32_t minv = 0;
+  int mwords = 0;
+};
+R28Mod r28_mod(const HBN& m, int rb, int n) {
+  R28Mod c;
+  c.mlimb = radix_limbs(m, rb, n);
+  c.mwords = (int)((m.bit_length() + 31) / 32);
+  c.mword = m.limbs(c.mwords);
+  c.r2 = radix_limbs(mod(HBN(1) << (2 * (size_t)rb * n), m), rb, n);
+  uint32_t inv = 1;
+  for (int i = 0; i < 6; i++) inv *= 2u - c.mlimb[0] * inv;  // m^-1 mod 2^32
+  c.minv = (0u - inv) & ((1u << rb) - 1u);
+  return c;
+}
+
 constexpr int kWindow = 5;
 constexpr int kTab = 1 << (kWindow - 1);
 
@@ -222,6 +253,11 @@ pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, doub
 pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int32_t* st, size_t count,
                            cudaStream_t stream);
 enum SideMode : int { kSideEnc = 0, kSideDec = 1, kSidePow = 2 };
+template <int RB, int N, int TPI>
+pcb_status launch_side28(const uint32_t* mlimb, const uint32_t* mword, int mwords, const uint32_t* r2,
+                         const uint32_t* c1, uint32_t minv, const uint8_t* ops, int nops, int ntab, int mode,
+                         const uint32_t* x, int x_words, const uint32_t* m, int m_words, const int32_t* skip,
+                         size_t count, uint32_t* y, int y_words, cudaStream_t st, double alg_mac32_per_elem);
 pcb_status rstream_sample(uint64_t* state, const uint32_t* n, int L, int nbits, const uint32_t* p, const uint32_t* q,
                           int H, size_t count, uint32_t* r_out, cudaStream_t st);
 }  // namespace pcb
@@ -758,7 +794,23 @@ pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t*
       std::vector<uint8_t> ops = build_ops(E, kWindow);
       s = scratch_alloc(ops.size(), (void**)&d_ops, st);
       if (!s) s = cuda_check(cudaMemcpyAsync(d_ops, ops.data(), ops.size(), cudaMemcpyHostToDevice, st));
-      if (!s) {
+      const char* core = getenv("PCB_CORE28");
+      if (!s && core && core[0] == '1' && M.bit_length() + 4 <= 28 * 76) {
+        const int bits = (int)M.bit_length();
+        const int N = bits + 4 <= 28 * 38 ? 38 : 76;
+        R28Mod c = r28_mod(M, 28, N);
+        const double mm = 2.0 * S * S + S;
+        const double alg = ((double)E.bit_length() + (double)((E.bit_length() + 3) / 4)) * mm;
+        const int yw = (int)S;
+        if (N == 38)
+          s = launch_side28<28, 38, 1>(c.mlimb.data(), c.mword.data(), c.mwords, c.r2.data(), nullptr, c.minv, d_ops,
+                                       (int)ops.size(), kTab, 2, (const uint32_t*)sx.dev, (int)m_limbs, nullptr, 0,
+                                       nullptr, count, ydev, yw, st, alg);
+        else
+          s = launch_side28<28, 76, 2>(c.mlimb.data(), c.mword.data(), c.mwords, c.r2.data(), nullptr, c.minv, d_ops,
+                                       (int)ops.size(), kTab, 2, (const uint32_t*)sx.dev, (int)m_limbs, nullptr, 0,
+                                       nullptr, count, ydev, yw, st, alg);
+      } else if (!s) {
         switch (S) {
 #define PCB_CASE(SS)                                                                                        \
   case SS: {                                                                                                \
