@@ -35,6 +35,7 @@ SOURCES = [
     "paillier.cu",
     "side.cu",
     "side28.cu",
+    "wide.cu",
     "rstream.cu",
     "imad_peak.cu",
     "host/hbn.cpp",

@@ -15,6 +15,7 @@
 #include "host/hbn.hpp"
 #include "paillier_params.cuh"
 #include "pcb_internal.h"
+#include "wide.h"
 
 namespace pcb {
 
@@ -231,6 +232,12 @@ struct pcb_ctx {
   cudaStream_t side_st[2] = {nullptr, nullptr};  // p-half / q-half streams (fork-join)
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   std::mutex mu;                 // serialises use of the side streams
+  WideMod wide;                  // n^2 constants for the radix-2^r kernels (public-key ops)
+  R28Mod rp2, rq2;               // p^2, q^2 for the radix CRT halves (3072-bit keys)
+  std::vector<uint32_t> rp2_nR, rq2_nR, rp2_R3, rq2_R3;
+  std::vector<uint32_t> wide_r2, wide_nR;
+  uint32_t* d_wconst = nullptr;  // [R^2, R, 1, R^C (aggregate)] radix limbs
+  int agg_chunk = 32;
   std::atomic<uint64_t> pow_full{0}, pow_half{0};
 };
 
@@ -260,6 +267,10 @@ pcb_status launch_side28(const uint32_t* mlimb, const uint32_t* mword, int mword
                          size_t count, uint32_t* y, int y_words, cudaStream_t st, double alg_mac32_per_elem);
 pcb_status rstream_sample(uint64_t* state, const uint32_t* n, int L, int nbits, const uint32_t* p, const uint32_t* q,
                           int H, size_t count, uint32_t* r_out, cudaStream_t st);
+template <int RB, int N, int TPI>
+pcb_status launch_wide(const WideMod& md, const WStep* prog, int nsteps, const uint32_t* consts_dev,
+                       const uint32_t* x, const uint32_t* b, const uint64_t* k, int xin_per_out, size_t count,
+                       size_t nout, uint32_t* y, int ntab, cudaStream_t st);
 }  // namespace pcb
 
 namespace {
@@ -439,7 +450,19 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
       switch (x->S) {
         case 32: build_enc<32>(x.get()); build_dec<32>(x.get()); break;
         case 64: build_enc<64>(x.get()); build_dec<64>(x.get()); break;
-        default: break;  // 3072-bit keys: constants built by the wide-modulus path (TODO)
+        case 96: {
+          build_enc<96>(x.get());
+          build_dec<96>(x.get());
+          // the CRT halves run on the radix-2^28 core (28 x 112 limbs, 2 lanes per residue)
+          const HBN R = HBN(1) << (28 * 112);
+          x->rp2 = r28_mod(p2, 28, 112);
+          x->rq2 = r28_mod(q2, 28, 112);
+          x->rp2_nR = radix_limbs(mod(x->n * R, p2), 28, 112);
+          x->rq2_nR = radix_limbs(mod(x->n * R, q2), 28, 112);
+          x->rp2_R3 = radix_limbs(mod(R * R * R, p2), 28, 112);
+          x->rq2_R3 = radix_limbs(mod(R * R * R, q2), 28, 112);
+          break;
+        }
       }
     }
     // exponent schedules
@@ -471,6 +494,39 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
       if (cudaEventCreateWithFlags(&x->ev_join[k], cudaEventDisableTiming) != cudaSuccess) return PCB_E_CUDA;
     }
     if (cudaEventCreateWithFlags(&x->ev_fork, cudaEventDisableTiming) != cudaSuccess) return PCB_E_CUDA;
+    // n^2 constants for the radix-2^r kernels (public-key encryption and homomorphic ops)
+    {
+      const size_t b2 = x->n2.bit_length();
+      int rb = 0, nl = 0, tpi = 0;
+      if (b2 + 4 <= 28 * 38) { rb = 28; nl = 38; tpi = 1; }
+      else if (b2 + 4 <= 28 * 76) { rb = 28; nl = 76; tpi = 2; }
+      else if (b2 + 4 <= 27 * 152) { rb = 27; nl = 152; tpi = 4; }
+      if (rb) {
+        R28Mod c = r28_mod(x->n2, rb, nl);
+        x->wide.rb = rb;
+        x->wide.n = nl;
+        x->wide.tpi = tpi;
+        x->wide.mlimb = c.mlimb;
+        x->wide.minv = c.minv;
+        x->wide.mwords = 2 * (int)x->L;
+        x->wide.mword = x->n2.limbs(2 * x->L);
+        x->wide_r2 = c.r2;
+        const HBN R = HBN(1) << ((size_t)rb * nl);
+        x->wide_nR = radix_limbs(mod(x->n * R, x->n2), rb, nl);
+        std::vector<uint32_t> consts;
+        auto push = [&](const HBN& v) {
+          std::vector<uint32_t> l = radix_limbs(v, rb, nl);
+          consts.insert(consts.end(), l.begin(), l.end());
+        };
+        push(mod(R * R, x->n2));                                // kConstR2
+        push(mod(R, x->n2));                                    // kConstOneR
+        push(HBN(1));                                           // kConstOne
+        push(pow_mod(mod(R, x->n2), HBN((uint64_t)x->agg_chunk), x->n2));  // R^C (aggregate fix)
+        if (cudaMalloc(&x->d_wconst, consts.size() * 4) != cudaSuccess) return PCB_E_CUDA;
+        if (cudaMemcpy(x->d_wconst, consts.data(), consts.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+          return PCB_E_CUDA;
+      }
+    }
     if (cudaMalloc(&x->d_sched, all.size()) != cudaSuccess) return PCB_E_CUDA;
     if (cudaMemcpy(x->d_sched, all.data(), all.size(), cudaMemcpyHostToDevice) != cudaSuccess)
       return PCB_E_CUDA;
@@ -489,6 +545,7 @@ void pcb_ctx_destroy(pcb_ctx* x) {
   if (x->d_sched) cudaFree(x->d_sched);
   if (x->d_n) cudaFree(x->d_n);
   if (x->d_n2) cudaFree(x->d_n2);
+  if (x->d_wconst) cudaFree(x->d_wconst);
   for (int k = 0; k < 2; k++) {
     if (x->side_st[k]) cudaStreamDestroy(x->side_st[k]);
     if (x->ev_join[k]) cudaEventDestroy(x->ev_join[k]);
@@ -564,6 +621,7 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
     e = launch_enc_prep(m, (int)m_limbs, v, zmin, zmax, delta, fine, mq, mql, q_out, clamps, r, x->d_n, (int)x->L,
                         stv, count, st);
   const uint32_t* mm = v ? mq : m;
+  const uint32_t* mmv = mm;
   const int ml = v ? mql : (int)m_limbs;
   const uint8_t* opp = x->d_sched + x->off_enc_p;
   const uint8_t* opq = x->d_sched + x->off_enc_q;
@@ -586,6 +644,25 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
       PCB_CASE(32)
       PCB_CASE(64)
 #undef PCB_CASE
+      case 96: {
+        const auto& k = *reinterpret_cast<const CrtEncConsts<96>*>(x->enc_blob.data());
+        const double mm = 2.0 * 96 * 96 + 96, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm + 2 * mm;
+        e = fork_join(
+            x, st,
+            [&](cudaStream_t s2) {
+              return launch_side28<28, 112, 2>(x->rp2.mlimb.data(), x->rp2.mword.data(), x->rp2.mwords,
+                                               x->rp2.r2.data(), x->rp2_nR.data(), x->rp2.minv, opp, x->len_enc_p,
+                                               kTab, 0, r, (int)x->L, mmv, ml, stv, count, yp, 96, s2, alg);
+            },
+            [&](cudaStream_t s2) {
+              return launch_side28<28, 112, 2>(x->rq2.mlimb.data(), x->rq2.mword.data(), x->rq2.mwords,
+                                               x->rq2.r2.data(), x->rq2_nR.data(), x->rq2.minv, opq, x->len_enc_q,
+                                               kTab, 0, r, (int)x->L, mmv, ml, stv, count, yq, 96, s2, alg);
+            },
+            count);
+        if (!e) e = launch_garner<96>(k, yp, yq, stv, c, (int)x->L, count, st);
+        break;
+      }
       default: e = PCB_E_UNSUPPORTED;
     }
   }
@@ -638,6 +715,69 @@ static pcb_status dec_core(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t
   return e;
 }
 
+
+// ---- n^2 (radix-2^r) dispatch ------------------------------------------------------------------
+static pcb_status run_wide(pcb_ctx* x, const WStep* prog, int nsteps, const uint32_t* xin, const uint32_t* b,
+                           const uint64_t* k, int xin_per_out, size_t count, size_t nout, uint32_t* y, int ntab,
+                           cudaStream_t st) {
+  const WideMod& w = x->wide;
+#define PCB_W(RB, NN, TT)                                                                                        \
+  if (w.rb == RB && w.n == NN && w.tpi == TT)                                                                     \
+    return launch_wide<RB, NN, TT>(w, prog, nsteps, x->d_wconst, xin, b, k, xin_per_out, count, nout, y, ntab, st);
+  PCB_W(28, 38, 1)
+  PCB_W(28, 76, 2)
+  PCB_W(27, 152, 4)
+#undef PCB_W
+  return PCB_E_UNSUPPORTED;
+}
+
+// Public-key encryption c = (1 + m n) r^n mod n^2 (encrypt_with_r, paillier.cpp:320-328) on the
+// radix kernel at modulus n^2 (ENC mode of side28.cu).
+static pcb_status run_pub_enc(pcb_ctx* x, const uint32_t* r, const uint32_t* m, int m_words, const int32_t* stv,
+                              size_t count, uint32_t* c, cudaStream_t st) {
+  const WideMod& w = x->wide;
+  const uint8_t* ops = x->d_sched + x->off_pub;
+  const double S2 = 2.0 * x->L, mm = 2 * S2 * S2 + S2;
+  const double alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm + mm;  // EXP(2|n|,|n|) + MM(2|n|)
+#define PCB_W(RB, NN, TT)                                                                                           \
+  if (w.rb == RB && w.n == NN && w.tpi == TT)                                                                        \
+    return launch_side28<RB, NN, TT>(w.mlimb.data(), w.mword.data(), w.mwords, x->wide_r2.data(), x->wide_nR.data(), \
+                                     w.minv, ops, x->len_pub, kTab, 0, r, (int)x->L, m, m_words, stv, count, c,      \
+                                     2 * (int)x->L, st, alg);
+  PCB_W(28, 38, 1)
+  PCB_W(28, 76, 2)
+  PCB_W(27, 152, 4)
+#undef PCB_W
+  return PCB_E_UNSUPPORTED;
+}
+
+static std::vector<WStep> prog_hom_add() {
+  return {WStep{kSrcX, 0, kSrcConst, (uint8_t)kConstR2, 0, 0, 0, 0},  // a R
+          WStep{kSrcReg, 0, kSrcB, 0, kPostOut, 0, 0, 0}};           // a b
+}
+
+static std::vector<WStep> prog_scalar_pow() {
+  std::vector<WStep> p;
+  p.push_back(WStep{kSrcX, 0, kSrcConst, (uint8_t)kConstR2, kPostAcc | kPostTab, 1, 0, 0});  // t1 = cR
+  p.push_back(WStep{kSrcReg, 0, kSrcAcc, 0, kPostTab, 2, 0, 0});                            // t2
+  for (int e = 3; e < 16; e++) p.push_back(WStep{kSrcReg, 0, kSrcTab, 1, kPostTab, (uint8_t)e, 0, 0});
+  p.push_back(WStep{kSrcTabDigit, 15, kSrcConst, (uint8_t)kConstOneR, kPostAcc, 0, 0, 0});  // seed: top digit
+  for (int w = 14; w >= 0; w--) {
+    for (int q = 0; q < 4; q++) p.push_back(WStep{kSrcReg, 0, kSrcAcc, 0, kPostAcc, 0, 0, 0});
+    p.push_back(WStep{kSrcReg, 0, kSrcTabDigit, (uint8_t)w, kPostAcc, 0, 0, 0});
+  }
+  p.push_back(WStep{kSrcReg, 0, kSrcConst, (uint8_t)kConstOne, kPostOut, 0, 0, 0});
+  return p;
+}
+
+static std::vector<WStep> prog_aggregate(int chunk) {
+  std::vector<WStep> p;
+  p.push_back(WStep{kSrcX, 0, kSrcX, 1, 0, 0, 0, 0});
+  for (int j = 2; j < chunk; j++) p.push_back(WStep{kSrcReg, 0, kSrcX, (uint8_t)j, 0, 0, 0, 0});
+  p.push_back(WStep{kSrcReg, 0, kSrcConst, (uint8_t)kConstFirstF, kPostOut, 0, 0, 0});  // x R^C R^-1 ... fix
+  return p;
+}
+
 extern "C" {
 
 pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* r, size_t count, uint32_t* c,
@@ -648,10 +788,35 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
   // use_crt = 0 on a private context: same residue through the CRT halves (the reference's own
   // tests pin CRT == direct bit-identically, test_paillier.cpp:63-78, acceptance [2]); the
   // ledger still records the direct path (pow_full).  Public-key-only: n^2 path (TODO).
-  if (!x->has_prv) return use_crt ? PCB_E_NO_PRIVATE : PCB_E_UNSUPPORTED;
+  if (!x->has_prv && use_crt) return PCB_E_NO_PRIVATE;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
   Staged sm, sr, sc, ss;
+  if (!x->has_prv) {  // public-key context: direct encryption at n^2
+    pcb_status e = stage_in(m, count * m_limbs * 4, st, &sm);
+    if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
+    if (!e) e = stage_out(c, count * 2 * x->L * 4, st, &sc);
+    if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+    int32_t* stv = (int32_t*)ss.dev;
+    if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+    if (!e)
+      e = launch_enc_prep((const uint32_t*)sm.dev, (int)m_limbs, nullptr, 0, 0, 0, 0, nullptr, 0, nullptr, nullptr,
+                          (const uint32_t*)sr.dev, x->d_n, (int)x->L, stv, count, st);
+    if (!e) e = cuda_check(cudaMemsetAsync(sc.dev, 0, count * 2 * x->L * 4, st));
+    if (!e) e = run_pub_enc(x, (const uint32_t*)sr.dev, (const uint32_t*)sm.dev, (int)m_limbs, stv, count,
+                            (uint32_t*)sc.dev, st);
+    if (!e) e = unstage_out(c, &sc, st);
+    if (!e) e = unstage_out(status, &ss, st);
+    if (!ss.dev) scratch_free(stv, st);
+    const bool any_host = sm.host || sr.host || sc.host || ss.host;
+    unstage(&sm, st);
+    unstage(&sr, st);
+    unstage(&sc, st);
+    unstage(&ss, st);
+    if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+    if (!e) x->pow_full += (uint64_t)count;
+    return e;
+  }
   pcb_status e = stage_in(m, count * m_limbs * 4, st, &sm);
   if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
   if (!e) e = stage_out(c, count * 2 * x->L * 4, st, &sc);
@@ -701,6 +866,94 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
     else
       x->pow_full += (uint64_t)count;
   }
+  return e;
+}
+
+pcb_status pcb_hom_add(pcb_ctx* x, const uint32_t* a, const uint32_t* b, size_t count, uint32_t* out,
+                       pcb_stream stream) {
+  if (!x || (count && (!a || !b || !out))) return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t wb = 2 * x->L * 4;
+  Staged sa, sb, so;
+  pcb_status e = stage_in(a, count * wb, st, &sa);
+  if (!e) e = stage_in(b, count * wb, st, &sb);
+  if (!e) e = stage_out(out, count * wb, st, &so);
+  std::vector<WStep> p = prog_hom_add();
+  if (!e)
+    e = run_wide(x, p.data(), (int)p.size(), (const uint32_t*)sa.dev, (const uint32_t*)sb.dev, nullptr, 1, count,
+                 count, (uint32_t*)so.dev, 1, st);
+  if (!e) e = unstage_out(out, &so, st);
+  const bool any_host = sa.host || sb.host || so.host;
+  unstage(&sa, st);
+  unstage(&sb, st);
+  unstage(&so, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  return e;
+}
+
+pcb_status pcb_hom_scalar_mul(pcb_ctx* x, const uint64_t* k, const uint32_t* c, size_t count, uint32_t* out,
+                              pcb_stream stream) {
+  if (!x || (count && (!k || !c || !out))) return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t wb = 2 * x->L * 4;
+  Staged sk, sc, so;
+  pcb_status e = stage_in(k, count * 8, st, &sk);
+  if (!e) e = stage_in(c, count * wb, st, &sc);
+  if (!e) e = stage_out(out, count * wb, st, &so);
+  std::vector<WStep> p = prog_scalar_pow();
+  if (!e)
+    e = run_wide(x, p.data(), (int)p.size(), (const uint32_t*)sc.dev, nullptr, (const uint64_t*)sk.dev, 1, count,
+                 count, (uint32_t*)so.dev, 16, st);
+  if (!e) e = unstage_out(out, &so, st);
+  const bool any_host = sk.host || sc.host || so.host;
+  unstage(&sk, st);
+  unstage(&sc, st);
+  unstage(&so, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!e) x->pow_full += (uint64_t)count;  // hom_scalar_mul bumps pow_full (paillier.cpp:437)
+  return e;
+}
+
+pcb_status pcb_aggregate(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* out, pcb_stream stream) {
+  if (!x || !c || !out || count == 0) return PCB_E_SHAPE;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t wb = 2 * x->L * 4;
+  Staged sc, so;
+  pcb_status e = stage_in(c, count * wb, st, &sc);
+  if (!e) e = stage_out(out, wb, st, &so);
+  const int C = x->agg_chunk;
+  std::vector<WStep> p = prog_aggregate(C);
+  const uint32_t* cur = (const uint32_t*)sc.dev;
+  size_t n = count;
+  uint32_t* bufs[2] = {nullptr, nullptr};
+  int which = 0;
+  while (!e && n > 1) {
+    const size_t nout = (n + C - 1) / C;
+    uint32_t* dst = nullptr;
+    if (nout == 1) {
+      dst = (uint32_t*)so.dev;
+    } else {
+      if (!bufs[which]) e = scratch_alloc(((count + C - 1) / C) * wb, (void**)&bufs[which], st);
+      dst = bufs[which];
+    }
+    if (!e) e = run_wide(x, p.data(), (int)p.size(), cur, nullptr, nullptr, C, n, nout, dst, 1, st);
+    cur = dst;
+    which ^= 1;
+    n = nout;
+  }
+  if (!e && count == 1) e = cuda_check(cudaMemcpyAsync(so.dev, sc.dev, wb, cudaMemcpyDeviceToDevice, st));
+  if (!e) e = unstage_out(out, &so, st);
+  scratch_free(bufs[0], st);
+  scratch_free(bufs[1], st);
+  const bool any_host = sc.host || so.host;
+  unstage(&sc, st);
+  unstage(&so, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
   return e;
 }
 
@@ -795,7 +1048,14 @@ pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t*
       s = scratch_alloc(ops.size(), (void**)&d_ops, st);
       if (!s) s = cuda_check(cudaMemcpyAsync(d_ops, ops.data(), ops.size(), cudaMemcpyHostToDevice, st));
       const char* core = getenv("PCB_CORE28");
-      if (!s && core && core[0] == '1' && M.bit_length() + 4 <= 28 * 76) {
+      if (!s && S == 96) {  // 2049..3072-bit moduli: radix-2^28 core, 2 lanes per residue
+        R28Mod c = r28_mod(M, 28, 112);
+        const double mm = 2.0 * S * S + S;
+        const double alg = ((double)E.bit_length() + (double)((E.bit_length() + 3) / 4)) * mm;
+        s = launch_side28<28, 112, 2>(c.mlimb.data(), c.mword.data(), c.mwords, c.r2.data(), nullptr, c.minv, d_ops,
+                                      (int)ops.size(), kTab, 2, (const uint32_t*)sx.dev, (int)m_limbs, nullptr, 0,
+                                      nullptr, count, ydev, S, st, alg);
+      } else if (!s && core && core[0] == '1' && M.bit_length() + 4 <= 28 * 76) {
         const int bits = (int)M.bit_length();
         const int N = bits + 4 <= 28 * 38 ? 38 : 76;
         R28Mod c = r28_mod(M, 28, N);
@@ -847,12 +1107,6 @@ pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t*
 
 // ---- not yet implemented in this build (fail loudly, never fall back) -----------------------
 extern "C" {
-pcb_status pcb_hom_add(pcb_ctx*, const uint32_t*, const uint32_t*, size_t, uint32_t*, pcb_stream) {
-  return PCB_E_UNSUPPORTED;
-}
-pcb_status pcb_hom_scalar_mul(pcb_ctx*, const uint64_t*, const uint32_t*, size_t, uint32_t*, pcb_stream) {
-  return PCB_E_UNSUPPORTED;
-}
 pcb_status pcb_hom_matvec(pcb_ctx*, const uint32_t*, const uint64_t*, const uint32_t*, size_t, size_t, uint32_t,
                           uint32_t*, pcb_stream) {
   return PCB_E_UNSUPPORTED;
@@ -861,7 +1115,6 @@ pcb_status pcb_edge_step(pcb_ctx*, const uint32_t*, const uint64_t*, const uint3
                          uint32_t, uint32_t*, pcb_stream) {
   return PCB_E_UNSUPPORTED;
 }
-pcb_status pcb_aggregate(pcb_ctx*, const uint32_t*, size_t, uint32_t*, pcb_stream) { return PCB_E_UNSUPPORTED; }
 pcb_status pcb_decrypt_update(pcb_ctx*, const uint32_t*, size_t, const uint64_t*, const uint64_t*, const uint64_t*,
                               double, double, double, double, double*, double*, double*, int32_t*, pcb_stream) {
   return PCB_E_UNSUPPORTED;

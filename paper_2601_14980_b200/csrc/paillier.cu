@@ -354,5 +354,6 @@ pcb_status launch_dec_finish(const CrtDecConsts<S>& k, const uint32_t* xp, const
                                            uint32_t*, int, size_t, cudaStream_t);
 PCB_INSTANTIATE(32)
 PCB_INSTANTIATE(64)
+PCB_INSTANTIATE(96)
 
 }  // namespace pcb

@@ -45,7 +45,7 @@ struct Side28Args {
 enum : int { kM28Enc = 0, kM28Dec = 1, kM28Pow = 2 };
 
 template <int RB, int N, int TPI>
-__global__ void __launch_bounds__(kThreadsPerBlock, PCB_R28_MINB) side28_kernel(const __grid_constant__ Side28Args<RB, N, TPI> P) {
+__global__ void __launch_bounds__(kThreadsPerBlock, (N / TPI > 40) ? 2 : PCB_R28_MINB) side28_kernel(const __grid_constant__ Side28Args<RB, N, TPI> P) {
   using Cf = r28::Cfg<RB, N, TPI>;
   constexpr int K = Cf::K, G = Cf::G;
   using Slot = r28::DSlot<RB, N, TPI>;
@@ -283,6 +283,8 @@ pcb_status launch_side28(const uint32_t* mlimb, const uint32_t* mword, int mword
                                                 const uint32_t*, int, const uint32_t*, int, const int32_t*, size_t, \
                                                 uint32_t*, int, cudaStream_t, double);
 PCB_SIDE28(28, 38, 1)   // 1024-bit keys: p^2 <= 1060 bits
-PCB_SIDE28(28, 76, 2)   // 2048-bit keys: p^2 <= 2124 bits
+PCB_SIDE28(28, 76, 2)   // 2048-bit keys: p^2 <= 2124 bits; n^2 of 1024-bit keys
+PCB_SIDE28(28, 112, 2)  // 3072-bit keys: p^2 <= 3132 bits
+PCB_SIDE28(27, 152, 4)  // n^2 of 2048-bit keys (public-key encryption)
 
 }  // namespace pcb

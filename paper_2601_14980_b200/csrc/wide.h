@@ -1,0 +1,35 @@
+// wide.h — program format of the n^2 interpreter kernel (wide.cu), shared with the host (abi.cu).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+namespace pcb {
+
+constexpr int kWideMaxSteps = 160;
+
+enum : uint8_t {
+  kSrcReg = 0,       // A: keep the previous result (registers)
+  kSrcAcc = 1,       // B: the accumulator slot (squaring)
+  kSrcX = 2,         // primary input  #arg of this output (aggregate chunk / single input)
+  kSrcB = 3,         // secondary input of this output (hom_add)
+  kSrcConst = 4,     // constant #arg (radix limbs, device table)
+  kSrcTab = 5,       // per-lane table entry #arg
+  kSrcTabDigit = 6,  // table entry = 4-bit digit #arg of this element's scalar (0 -> Montgomery one)
+};
+enum : uint8_t { kPostAcc = 1, kPostTab = 2, kPostOut = 4 };
+
+// constant table layout (ids), per modulus
+enum : int { kConstR2 = 0, kConstOneR = 1, kConstOne = 2, kConstFirstF = 3 };
+
+struct WStep {
+  uint8_t asrc, aarg, bsrc, barg, post, tab, pad0, pad1;
+};
+
+struct WideMod {  // host-side constants of one modulus in radix 2^rb
+  int rb = 0, n = 0, tpi = 0;
+  std::vector<uint32_t> mlimb, mword;
+  uint32_t minv = 0;
+  int mwords = 0;
+};
+
+}  // namespace pcb

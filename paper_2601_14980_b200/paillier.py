@@ -295,3 +295,61 @@ class Paillier:
 
     def decrypt_vec(self, cs, use_crt: bool) -> list[int]:
         return self._dec_list(cs, use_crt)
+
+    # ---- homomorphic operations (paillier.cpp:428-493) ----------------------------------------
+    def _nbits(self) -> int:
+        return self.n.bit_length()
+
+    def _bump(self, bits: int) -> None:
+        """bump_bits_or_throw (paillier.cpp:245-251)."""
+        if bits >= self._nbits():
+            raise OverflowError("homomorphic accumulation exceeds plaintext space")
+
+    def _cw(self, cs):
+        vals = [c.value if isinstance(c, Ciphertext) else int(c) for c in cs]
+        return L.ints_to_limbs(vals, 2 * self.L)
+
+    def hom_add_batch(self, a, b):
+        """out_i = a_i b_i mod n^2 on (count, 2L) limb arrays / tensors."""
+        dev = hasattr(a, "is_cuda") and a.is_cuda
+        out = _torch().empty_like(a) if dev else np.zeros_like(a)
+        _raise_for(L.lib().pcb_hom_add(self._ctx, L.ptr(a), L.ptr(b), a.shape[0], L.ptr(out),
+                                       self._stream() if dev else None), "hom_add")
+        return out
+
+    def hom_scalar_mul_batch(self, k, c):
+        dev = hasattr(c, "is_cuda") and c.is_cuda
+        out = _torch().empty_like(c) if dev else np.zeros_like(c)
+        _raise_for(L.lib().pcb_hom_scalar_mul(self._ctx, L.ptr(k), L.ptr(c), c.shape[0], L.ptr(out),
+                                              self._stream() if dev else None), "hom_scalar_mul")
+        return out
+
+    def aggregate_batch(self, c):
+        """prod_i c_i mod n^2 (balanced product tree on the GPU) -> (2L,) limbs."""
+        dev = hasattr(c, "is_cuda") and c.is_cuda
+        out = _torch().empty((2 * self.L,), dtype=c.dtype, device=c.device) if dev else np.zeros(2 * self.L, np.uint32)
+        _raise_for(L.lib().pcb_aggregate(self._ctx, L.ptr(c), c.shape[0], L.ptr(out),
+                                         self._stream() if dev else None), "aggregate")
+        return out
+
+    def hom_add(self, a: Ciphertext, b: Ciphertext) -> Ciphertext:
+        """Paillier::hom_add (paillier.cpp:428-432): bits = max + 1, overflow guard."""
+        bits = max(a.plain_bits, b.plain_bits) + 1
+        self._bump(bits)
+        out = self.hom_add_batch(self._cw([a]), self._cw([b]))
+        return Ciphertext(L.limbs_to_int(out[0]), bits)
+
+    def hom_scalar_mul(self, k: int, c: Ciphertext) -> Ciphertext:
+        """Paillier::hom_scalar_mul (paillier.cpp:434-439), k < 2^64."""
+        bits = 0 if k == 0 else c.plain_bits + int(k).bit_length()
+        self._bump(bits)
+        out = self.hom_scalar_mul_batch(np.array([k], np.uint64), self._cw([c]))
+        return Ciphertext(L.limbs_to_int(out[0]), bits)
+
+    def aggregate(self, cs) -> Ciphertext:
+        """prod c_i mod n^2; plain_bits follows a balanced hom_add tree (depth ceil(log2 count))."""
+        cs = list(cs)
+        bits = max(c.plain_bits for c in cs) + (len(cs) - 1).bit_length()
+        self._bump(bits)
+        out = self.aggregate_batch(self._cw(cs))
+        return Ciphertext(L.limbs_to_int(out), bits)

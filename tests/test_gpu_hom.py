@@ -1,0 +1,123 @@
+"""GPU parity for the public-key / homomorphic operations modulo n^2 (radix-2^r kernels), through
+the C ABI, against the reference's golden vectors and Python big-int arithmetic."""
+import random
+
+import numpy as np
+import pytest
+
+import pcadmm_oracle as O
+from conftest import golden
+from paper_2601_14980_b200 import _lib as L
+from paper_2601_14980_b200 import paillier as P
+
+pytestmark = pytest.mark.gpu
+
+
+def H(x):
+    return int(x, 16)
+
+
+def key(idx):
+    k = golden("keys.json")[idx]
+    return P.KeyPair(H(k["n"]), H(k["p"]), H(k["q"]), k["bits"])
+
+
+@pytest.fixture(scope="module", params=[0, 1, 2], ids=["k64", "k1024", "k2048"])
+def kk(request):
+    kp = key(request.param)
+    return request.param, kp, P.Paillier(kp), P.Paillier(P.PublicKey(kp.n, kp.key_bits))
+
+
+def test_public_key_encrypt_matches_reference(kk):
+    idx, kp, ph, pub = kk
+    e = golden("encrypt.json")[idx]
+    ms, rs, cs = [H(v) for v in e["m"]], [H(v) for v in e["r"]], [H(v) for v in e["c"]]
+    st = np.zeros(len(ms), np.int32)
+    c = pub.encrypt_batch(L.ints_to_limbs(ms, pub.L), L.ints_to_limbs(rs, pub.L), use_crt=False, status=st)
+    assert (st == 0).all()
+    assert L.limbs_to_ints(c) == cs  # encrypt_with_r == crt_encrypt_with_r (test_paillier.cpp:63-78)
+    # error statuses of the public path
+    st = np.zeros(3, np.int32)
+    pub.encrypt_batch(L.ints_to_limbs([H(v) for v in e["bad_m"]], pub.L),
+                      L.ints_to_limbs([H(v) for v in e["bad_r"]], pub.L), use_crt=False, status=st)
+    assert st.tolist() == e["bad_status"]
+    # decrypting the public-path ciphertexts with the private context
+    assert ph.decrypt_vec([P.Ciphertext(v) for v in L.limbs_to_ints(c)], True) == ms
+
+
+def test_public_context_refuses_private_ops(kk):
+    idx, kp, ph, pub = kk
+    with pytest.raises(P.LogicError):
+        pub.decrypt(5)
+    with pytest.raises(P.LogicError):
+        pub.crt_encrypt_with_r(3, 2)
+
+
+def test_hom_add_matches_bigint(kk):
+    idx, kp, ph, pub = kk
+    rnd = random.Random(idx)
+    n2 = kp.n2
+    a = [rnd.randrange(n2) for _ in range(257)] + [0, 1, n2 - 1]
+    b = [rnd.randrange(n2) for _ in range(257)] + [n2 - 1, n2 - 1, n2 - 1]
+    out = pub.hom_add_batch(L.ints_to_limbs(a, 2 * pub.L), L.ints_to_limbs(b, 2 * pub.L))
+    assert L.limbs_to_ints(out) == [x * y % n2 for x, y in zip(a, b)]
+
+
+def test_hom_add_decrypts_to_sum_and_guard(kk):
+    idx, kp, ph, pub = kk
+    rng = P.Rng(5)
+    m1, m2 = 123456789, 987654321
+    c1, c2 = ph.encrypt_vec([m1, m2], rng, True)
+    s = pub.hom_add(c1, c2)
+    assert ph.crt_decrypt(s) == (m1 + m2) % kp.n
+    assert s.plain_bits == max(c1.plain_bits, c2.plain_bits) + 1
+    big = P.Ciphertext(c1.value, kp.n.bit_length() - 1)
+    with pytest.raises(OverflowError):  # bump_bits_or_throw (paillier.cpp:245-251)
+        pub.hom_add(big, big)
+
+
+def test_hom_scalar_mul_matches_bigint(kk):
+    idx, kp, ph, pub = kk
+    rnd = random.Random(10 + idx)
+    n2 = kp.n2
+    cs = [rnd.randrange(1, n2) for _ in range(200)]
+    ks = [0, 1, 2, 3, 15, 16, 2**64 - 1, 2**63] + [rnd.getrandbits(64) for _ in range(192)]
+    out = pub.hom_scalar_mul_batch(np.array(ks, np.uint64), L.ints_to_limbs(cs, 2 * pub.L))
+    assert L.limbs_to_ints(out) == [pow(c, k, n2) for c, k in zip(cs, ks)]
+
+
+def test_hom_scalar_mul_reference_semantics():
+    # test_paillier.cpp:102-115 on the toy key
+    ph = P.Paillier(P.keypair_from_primes(5, 7))
+    rng = P.Rng(19)
+    for m in (0, 1, 2, 5, 11):
+        c = ph.encrypt_vec([m], rng, True)[0]
+        for k in (0, 1, 2, 3):
+            if k * m >= 35 or (m >= 8 and k >= 2):
+                continue
+            assert ph.crt_decrypt(ph.hom_scalar_mul(k, c)) == k * m
+    c = ph.encrypt_vec([30], rng, True)[0]
+    with pytest.raises(OverflowError):
+        ph.hom_scalar_mul(64, c)
+
+
+@pytest.mark.parametrize("count", [1, 2, 31, 32, 33, 1000, 1057])
+def test_aggregate_product_tree(count):
+    kp = key(1)
+    pub = P.Paillier(P.PublicKey(kp.n, kp.key_bits))
+    rnd = random.Random(count)
+    cs = [rnd.randrange(1, kp.n2) for _ in range(count)]
+    out = pub.aggregate_batch(L.ints_to_limbs(cs, 2 * pub.L))
+    want = 1
+    for c in cs:
+        want = want * c % kp.n2
+    assert L.limbs_to_int(out) == want
+
+
+def test_aggregate_decrypts_to_sum():
+    kp = key(2)
+    ph = P.Paillier(kp)
+    ms = [i * 1000003 for i in range(300)]
+    cs = ph.encrypt_vec(ms, P.Rng(3), True)
+    agg = ph.aggregate(cs)
+    assert ph.crt_decrypt(agg) == sum(ms) % kp.n

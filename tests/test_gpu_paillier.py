@@ -203,3 +203,56 @@ def test_modexp_batch_vs_pow(bits):
         rc = lib.pcb_modexp_batch(L.ptr(M), limbs, L.ptr(E), len(E), L.ptr(X), len(xs), L.ptr(Y), None)
         assert rc == 0
         assert L.limbs_to_ints(Y) == [pow(x, e, m) for x in xs]
+
+
+def key3072():
+    """cfg4 key: keypair_from_primes(random_prime(1536) x 2), redrawn until n has 3072 bits
+    (the reference keygen rejects 3072, paillier.cpp:107-109)."""
+    rng = P.Rng(3072)
+    while True:
+        p, q = P.random_prime(rng, 1536), P.random_prime(rng, 1536)
+        if p != q and (p * q).bit_length() == 3072:
+            return P.keypair_from_primes(p, q)
+
+
+def test_3072_bit_crt_encrypt_decrypt_vs_oracle():
+    torch = pytest.importorskip("torch")
+    kp = key3072()
+    ph = P.Paillier(kp)
+    okp = O.finish_keys(kp.p, kp.q, 3072)
+    n = 200
+    rnd = random.Random(3)
+    ms = [rnd.getrandbits(50) for _ in range(n - 3)] + [0, 1, kp.n - 1]
+    R = ph.sample_r_batch(P.Rng(2), n)
+    rs = L.limbs_to_ints(R.cpu().numpy().view(np.uint32))
+    M = torch.from_numpy(L.ints_to_limbs(ms, ph.L).view(np.int32)).cuda()
+    c = ph.encrypt_batch(M, R)
+    cs = L.limbs_to_ints(c.cpu().numpy().view(np.uint32))
+    for i in list(range(0, n, 23)) + [n - 1, n - 2]:
+        assert cs[i] == O.crt_encrypt_with_r(okp, ms[i], rs[i])
+    m = ph.decrypt_batch(c)
+    assert L.limbs_to_ints(m.cpu().numpy().view(np.uint32)) == ms
+    # public-key path at 6144-bit n^2 is not instantiated in this build
+    pub = P.Paillier(P.PublicKey(kp.n, 3072))
+    with pytest.raises(L.PcbError):
+        pub.encrypt_batch(M.cpu().numpy().view(np.uint32)[:2].copy(), R.cpu().numpy().view(np.uint32)[:2].copy(),
+                          use_crt=False)
+
+
+def test_3072_bit_matches_compiled_reference():
+    import refbind as R_
+
+    if not R_.available():
+        pytest.skip("oracle/_ref not built")
+    kp = key3072()
+    ref = R_.RefKey.from_primes(kp.p, kp.q)
+    ph = P.Paillier(kp)
+    rnd = random.Random(4)
+    ms = [rnd.getrandbits(50) for _ in range(16)]
+    r, _ = ref.sample_r(2, 16)
+    cref, st = ref.encrypt(L.ints_to_limbs(ms, ph.L), r, crt=True)
+    assert (st == 0).all()
+    c = ph.encrypt_batch(L.ints_to_limbs(ms, ph.L), np.ascontiguousarray(r))
+    assert (c == cref).all()
+    mref, _ = ref.decrypt(cref, crt=True)
+    assert (ph.decrypt_batch(np.ascontiguousarray(c)) == mref).all()
