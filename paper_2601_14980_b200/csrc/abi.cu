@@ -270,7 +270,7 @@ pcb_status rstream_sample(uint64_t* state, const uint32_t* n, int L, int nbits, 
 template <int RB, int N, int TPI>
 pcb_status launch_wide(const WideMod& md, const WStep* prog, int nsteps, const uint32_t* consts_dev,
                        const uint32_t* x, const uint32_t* b, const uint64_t* k, int xin_per_out, size_t count,
-                       size_t nout, uint32_t* y, int ntab, cudaStream_t st);
+                       size_t nout, uint32_t* y, int ntab, cudaStream_t st, const MatvecGeom* mg);
 }  // namespace pcb
 
 namespace {
@@ -719,11 +719,11 @@ static pcb_status dec_core(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t
 // ---- n^2 (radix-2^r) dispatch ------------------------------------------------------------------
 static pcb_status run_wide(pcb_ctx* x, const WStep* prog, int nsteps, const uint32_t* xin, const uint32_t* b,
                            const uint64_t* k, int xin_per_out, size_t count, size_t nout, uint32_t* y, int ntab,
-                           cudaStream_t st) {
+                           cudaStream_t st, const MatvecGeom* mg = nullptr) {
   const WideMod& w = x->wide;
 #define PCB_W(RB, NN, TT)                                                                                        \
   if (w.rb == RB && w.n == NN && w.tpi == TT)                                                                     \
-    return launch_wide<RB, NN, TT>(w, prog, nsteps, x->d_wconst, xin, b, k, xin_per_out, count, nout, y, ntab, st);
+    return launch_wide<RB, NN, TT>(w, prog, nsteps, x->d_wconst, xin, b, k, xin_per_out, count, nout, y, ntab, st, mg);
   PCB_W(28, 38, 1)
   PCB_W(28, 76, 2)
   PCB_W(27, 152, 4)
@@ -767,6 +767,43 @@ static std::vector<WStep> prog_scalar_pow() {
     p.push_back(WStep{kSrcReg, 0, kSrcTabDigit, (uint8_t)w, kPostAcc, 0, 0, 0});
   }
   p.push_back(WStep{kSrcReg, 0, kSrcConst, (uint8_t)kConstOne, kPostOut, 0, 0, 0});
+  return p;
+}
+
+// matvec phase A, window w: T[col][w][d] = zv_col^(d 64^w) (Montgomery form), d = 1..63
+static std::vector<WStep> prog_mat_table(int w) {
+  std::vector<WStep> p;
+  const int nsq = kMatWin * w;
+  const uint8_t first_post = nsq == 0 ? (kPostAcc | kPostOp | kPostGTab) : kPostAcc;
+  p.push_back(WStep{kSrcX, 0, kSrcConst, (uint8_t)kConstR2, first_post, 1, 0, 0});
+  for (int q = 1; q <= nsq; q++)
+    p.push_back(WStep{kSrcReg, 0, kSrcAcc, 0, (uint8_t)(q == nsq ? (kPostAcc | kPostOp | kPostGTab) : kPostAcc), 1, 0, 0});
+  for (int d = 2; d < 64; d++) p.push_back(WStep{kSrcReg, 0, kSrcOpKeep, 0, kPostGTab, (uint8_t)d, 0, 0});
+  return p;
+}
+
+// matvec phase B: product of the table entries of cc columns x nwin windows (Montgomery form)
+static std::vector<WStep> prog_mat_prod(int cc, int nwin) {
+  std::vector<WStep> p;
+  std::vector<uint8_t> ids;
+  for (int j = 0; j < cc; j++)
+    for (int w = 0; w < nwin; w++) ids.push_back((uint8_t)(j * 16 + w));
+  if (ids.size() == 1) {
+    p.push_back(WStep{kSrcMatTab, ids[0], kSrcConst, (uint8_t)kConstOneR, kPostOut, 0, 0, 0});
+    return p;
+  }
+  p.push_back(WStep{kSrcMatTab, ids[0], kSrcMatTab, ids[1], 0, 0, 0, 0});
+  for (size_t q = 2; q < ids.size(); q++) p.push_back(WStep{kSrcReg, 0, kSrcMatTab, ids[q], 0, 0, 0, 0});
+  p.back().post = kPostOut;
+  return p;
+}
+
+// matvec phase C: out_i = alpha_i * prod_c P_{i,c}  (inputs per row: nch Montgomery partials, then alpha)
+static std::vector<WStep> prog_mat_combine(int nch) {
+  std::vector<WStep> p;
+  p.push_back(WStep{kSrcX, 0, kSrcX, 1, 0, 0, 0, 0});
+  for (int q = 2; q <= nch; q++) p.push_back(WStep{kSrcReg, 0, kSrcX, (uint8_t)q, 0, 0, 0, 0});
+  p.back().post = kPostOut;
   return p;
 }
 
@@ -957,6 +994,135 @@ pcb_status pcb_aggregate(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* 
   return e;
 }
 
+// hom_matvec core on device pointers; expo_host is the host copy (for the window count).
+static pcb_status matvec_core(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo_dev, const uint64_t* expo_host,
+                              const uint32_t* zv, size_t rows, size_t cols, uint32_t* out, cudaStream_t st) {
+  const size_t wb = 2 * x->L * 4;
+  if (rows == 0) return PCB_OK;
+  if (cols == 0) return cuda_check(cudaMemcpyAsync(out, alpha, rows * wb, cudaMemcpyDeviceToDevice, st));
+  int maxbits = 0;
+  for (size_t i = 0; i < rows * cols; i++) {
+    const int b = expo_host[i] ? 64 - __builtin_clzll(expo_host[i]) : 0;
+    if (b > maxbits) maxbits = b;
+  }
+  const int nwin = maxbits ? (maxbits + kMatWin - 1) / kMatWin : 1;
+  const int cc = std::max(1, std::min(16, (kWideMaxSteps - 1) / nwin));
+  const int nch = (int)((cols + cc - 1) / cc);
+  const int N = x->wide.n;
+  MatvecGeom g;
+  g.expo = expo_dev;
+  g.cols = (int)cols;
+  g.nwin = nwin;
+  g.cc = cc;
+  g.nch = nch;
+  uint32_t *part = nullptr, *combo = nullptr;
+  pcb_status e = scratch_alloc(cols * (size_t)nwin * 64 * N * 4, (void**)&g.mtab, st);
+  for (int w = 0; !e && w < nwin; w++) {  // phase A: power tables, one launch per window position
+    std::vector<WStep> p = prog_mat_table(w);
+    g.wcur = w;
+    e = run_wide(x, p.data(), (int)p.size(), zv, nullptr, nullptr, 1, cols, cols, nullptr, 1, st, &g);
+  }
+  if (!e) e = scratch_alloc(rows * (size_t)nch * wb, (void**)&part, st);
+  if (!e) {  // phase B: table products per (row, column chunk)
+    std::vector<WStep> p = prog_mat_prod(cc, nwin);
+    e = run_wide(x, p.data(), (int)p.size(), nullptr, nullptr, nullptr, 1, rows * nch, rows * nch, part, 1, st, &g);
+  }
+  if (!e) e = scratch_alloc(rows * (size_t)(nch + 1) * wb, (void**)&combo, st);
+  if (!e)
+    e = cuda_check(cudaMemcpy2DAsync(combo, (nch + 1) * wb, part, nch * wb, nch * wb, rows, cudaMemcpyDeviceToDevice, st));
+  if (!e)
+    e = cuda_check(cudaMemcpy2DAsync((uint8_t*)combo + nch * wb, (nch + 1) * wb, alpha, wb, wb, rows,
+                                     cudaMemcpyDeviceToDevice, st));
+  if (!e) {  // phase C: alpha_i * prod_c P_{i,c}
+    std::vector<WStep> p = prog_mat_combine(nch);
+    e = run_wide(x, p.data(), (int)p.size(), combo, nullptr, nullptr, nch + 1, rows * (nch + 1), rows, out, 1, st);
+  }
+  scratch_free(g.mtab, st);
+  scratch_free(part, st);
+  scratch_free(combo, st);
+  if (!e) x->pow_full += rows;  // hom_matvec counts one full exponentiation per row (paillier.cpp:476)
+  return e;
+}
+
+pcb_status pcb_hom_matvec(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo, const uint32_t* zv, size_t rows,
+                          size_t cols, uint32_t window, uint32_t* out, pcb_stream stream) {
+  if (!x || (rows && (!alpha || !out)) || (rows && cols && (!expo || !zv))) return PCB_E_SHAPE;
+  if (window < 1 || window > 8) return PCB_E_SHAPE;  // paillier.cpp:449
+  if (rows == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t wb = 2 * x->L * 4;
+  std::vector<uint64_t> eh(rows * cols);
+  Staged sa, se, sz, so;
+  pcb_status e = stage_in(alpha, rows * wb, st, &sa);
+  if (!e) e = stage_in(expo, rows * cols * 8, st, &se);
+  if (!e) e = stage_in(zv, cols * wb, st, &sz);
+  if (!e) e = stage_out(out, rows * wb, st, &so);
+  if (!e && cols) {
+    e = cuda_check(cudaMemcpyAsync(eh.data(), se.dev, rows * cols * 8, cudaMemcpyDeviceToHost, st));
+    if (!e) e = cuda_check(cudaStreamSynchronize(st));
+  }
+  if (!e)
+    e = matvec_core(x, (const uint32_t*)sa.dev, (const uint64_t*)se.dev, eh.data(), (const uint32_t*)sz.dev, rows,
+                    cols, (uint32_t*)so.dev, st);
+  if (!e) e = unstage_out(out, &so, st);
+  unstage(&sa, st);
+  unstage(&se, st);
+  unstage(&sz, st);
+  unstage(&so, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  return e;
+}
+
+pcb_status pcb_edge_step(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo, const uint32_t* zc,
+                         const uint32_t* vc, size_t cols, uint32_t window, uint32_t* out, pcb_stream stream) {
+  if (!x || (cols && (!alpha || !expo || !zc || !vc || !out))) return PCB_E_SHAPE;
+  if (window < 1 || window > 8) return PCB_E_SHAPE;
+  if (cols == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t wb = 2 * x->L * 4;
+  std::vector<uint64_t> eh(cols * cols);
+  Staged sa, se, sz, sv, so;
+  int32_t* stv = nullptr;
+  uint32_t* zvd = nullptr;
+  pcb_status e = stage_in(alpha, cols * wb, st, &sa);
+  if (!e) e = stage_in(expo, cols * cols * 8, st, &se);
+  if (!e) e = stage_in(zc, cols * wb, st, &sz);
+  if (!e) e = stage_in(vc, cols * wb, st, &sv);
+  if (!e) e = stage_out(out, cols * wb, st, &so);
+  // protocol.cpp:264-266: every z_j, v_j must be < n^2 ("ciphertext outside the group")
+  if (!e) e = scratch_alloc(2 * cols * 4, (void**)&stv, st);
+  if (!e) e = launch_dec_prep((const uint32_t*)sz.dev, x->d_n2, (int)x->L, stv, cols, st);
+  if (!e) e = launch_dec_prep((const uint32_t*)sv.dev, x->d_n2, (int)x->L, stv + cols, cols, st);
+  std::vector<int32_t> hst(2 * cols);
+  if (!e) e = cuda_check(cudaMemcpyAsync(hst.data(), stv, 2 * cols * 4, cudaMemcpyDeviceToHost, st));
+  if (!e) e = cuda_check(cudaMemcpyAsync(eh.data(), se.dev, cols * cols * 8, cudaMemcpyDeviceToHost, st));
+  if (!e) e = cuda_check(cudaStreamSynchronize(st));
+  if (!e)
+    for (int32_t v : hst)
+      if (v != PCB_OK) e = PCB_E_CIPHER_RANGE;
+  // zv_j = z_j * v_j mod n^2 (hom_add, protocol.cpp:268-269), then the matvec (270-271)
+  if (!e) e = scratch_alloc(cols * wb, (void**)&zvd, st);
+  std::vector<WStep> pa = prog_hom_add();
+  if (!e)
+    e = run_wide(x, pa.data(), (int)pa.size(), (const uint32_t*)sz.dev, (const uint32_t*)sv.dev, nullptr, 1, cols, cols,
+                 zvd, 1, st);
+  if (!e)
+    e = matvec_core(x, (const uint32_t*)sa.dev, (const uint64_t*)se.dev, eh.data(), zvd, cols, cols,
+                    (uint32_t*)so.dev, st);
+  if (!e) e = unstage_out(out, &so, st);
+  scratch_free(stv, st);
+  scratch_free(zvd, st);
+  unstage(&sa, st);
+  unstage(&se, st);
+  unstage(&sz, st);
+  unstage(&sv, st);
+  unstage(&so, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  return e;
+}
+
 pcb_status pcb_sample_r(pcb_ctx* x, uint64_t* rng_state, size_t count, uint32_t* r_out, pcb_stream stream) {
   if (!x || !rng_state || (count && !r_out)) return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
@@ -1107,14 +1273,6 @@ pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t*
 
 // ---- not yet implemented in this build (fail loudly, never fall back) -----------------------
 extern "C" {
-pcb_status pcb_hom_matvec(pcb_ctx*, const uint32_t*, const uint64_t*, const uint32_t*, size_t, size_t, uint32_t,
-                          uint32_t*, pcb_stream) {
-  return PCB_E_UNSUPPORTED;
-}
-pcb_status pcb_edge_step(pcb_ctx*, const uint32_t*, const uint64_t*, const uint32_t*, const uint32_t*, size_t,
-                         uint32_t, uint32_t*, pcb_stream) {
-  return PCB_E_UNSUPPORTED;
-}
 pcb_status pcb_decrypt_update(pcb_ctx*, const uint32_t*, size_t, const uint64_t*, const uint64_t*, const uint64_t*,
                               double, double, double, double, double*, double*, double*, int32_t*, pcb_stream) {
   return PCB_E_UNSUPPORTED;

@@ -37,6 +37,10 @@ struct WideArgs {
   int nout;
   uint32_t* tab;          // per-lane scratch table (16 entries)
   uint32_t* y;            // nout x mwords
+  // hom_matvec
+  uint32_t* mtab;         // power tables: entry (col, w, d) at ((col * nwin + w) * 64 + d) * N words
+  const uint64_t* expo;   // rows x cols exponents (row-major)
+  int cols, nwin, cc, nch, wcur;
 };
 
 template <int RB, int N, int TPI>
@@ -83,6 +87,19 @@ __global__ void __launch_bounds__(kThreadsPerBlock) wide_kernel(const __grid_con
       } else if (src == kSrcTab) {
 #pragma unroll
         for (int j = 0; j < K; j++) v[j] = tab_at(arg, j);
+      } else if (src == kSrcMatTab) {  // group o = (row, chunk); entry (col, w, digit of E[row][col])
+        const int jl = arg >> 4, w = arg & 15;
+        const int row = o / P.nch, col = (o % P.nch) * P.cc + jl;
+        int d = 0;
+        if (col < P.cols) d = (int)((P.expo[(size_t)row * P.cols + col] >> (kMatWin * w)) & ((1u << kMatWin) - 1));
+        if (d == 0) {
+#pragma unroll
+          for (int j = 0; j < K; j++) v[j] = P.consts[kConstOneR * N + t * K + j];
+        } else {
+          const uint32_t* e = P.mtab + ((size_t)(col * P.nwin + w) * 64 + d) * N + t * K;
+#pragma unroll
+          for (int j = 0; j < K; j++) v[j] = e[j];
+        }
       } else {  // kSrcTabDigit: entry = 4-bit digit `arg` of this element's scalar
         const int d = (int)((kk >> (4 * arg)) & 15u);
         if (d == 0) {
@@ -99,7 +116,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) wide_kernel(const __grid_con
       const WStep st = P.prog[s];
       if (st.asrc != kSrcReg) fetch(A, st.asrc, st.aarg);
       const bool b_acc = st.bsrc == kSrcAcc;
-      if (!b_acc) {
+      if (!b_acc && st.bsrc != kSrcOpKeep) {
         uint32_t v[K];
         fetch(v, st.bsrc, st.barg);
 #pragma unroll
@@ -112,6 +129,12 @@ __global__ void __launch_bounds__(kThreadsPerBlock) wide_kernel(const __grid_con
 #pragma unroll
       for (int j = 0; j < K; j++) A[j] = R[j];
       if (st.post & kPostAcc) Acc.store(R, t);
+      if (st.post & kPostOp) Op.store(R, t);
+      if (st.post & kPostGTab) {  // matvec table build: group o = column, window P.wcur, digit st.tab
+        uint32_t* e = P.mtab + ((size_t)(o * P.nwin + P.wcur) * 64 + st.tab) * N + t * K;
+#pragma unroll
+        for (int j = 0; j < K; j++) e[j] = R[j];
+      }
       if (st.post & kPostTab) {
 #pragma unroll
         for (int j = 0; j < K; j++) tab_at(st.tab, j) = R[j];
@@ -144,7 +167,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) wide_kernel(const __grid_con
 template <int RB, int N, int TPI>
 pcb_status launch_wide(const WideMod& md, const WStep* prog, int nsteps, const uint32_t* consts_dev,
                        const uint32_t* x, const uint32_t* b, const uint64_t* k, int xin_per_out, size_t count,
-                       size_t nout, uint32_t* y, int ntab, cudaStream_t st) {
+                       size_t nout, uint32_t* y, int ntab, cudaStream_t st, const MatvecGeom* mg) {
   using Args = WideArgs<RB, N, TPI>;
   if (nsteps > kWideMaxSteps) return PCB_E_SHAPE;
   Args P;
@@ -162,6 +185,13 @@ pcb_status launch_wide(const WideMod& md, const WStep* prog, int nsteps, const u
   P.count = (int)count;
   P.nout = (int)nout;
   P.y = y;
+  P.mtab = mg ? mg->mtab : nullptr;
+  P.expo = mg ? mg->expo : nullptr;
+  P.cols = mg ? mg->cols : 0;
+  P.nwin = mg ? mg->nwin : 0;
+  P.cc = mg ? mg->cc : 1;
+  P.nch = mg ? mg->nch : 1;
+  P.wcur = mg ? mg->wcur : 0;
   constexpr int G = 32 / TPI;
   const size_t smem = (size_t)(((N + 3) & ~3) + (kThreadsPerBlock / 32) * 2 * N * G) * 4;
   int blocks = 0;
@@ -177,7 +207,7 @@ pcb_status launch_wide(const WideMod& md, const WStep* prog, int nsteps, const u
 #define PCB_WIDE(RB, N, TPI)                                                                                      \
   template pcb_status launch_wide<RB, N, TPI>(const WideMod&, const WStep*, int, const uint32_t*, const uint32_t*, \
                                               const uint32_t*, const uint64_t*, int, size_t, size_t, uint32_t*, int, \
-                                              cudaStream_t);
+                                              cudaStream_t, const MatvecGeom*);
 PCB_WIDE(28, 38, 1)   // n^2 <= 1060 bits (toy / 64-bit keys)
 PCB_WIDE(28, 76, 2)   // n^2 <= 2124 bits (1024-bit keys)
 PCB_WIDE(27, 152, 4)  // n^2 <= 4100 bits (2048-bit keys)

@@ -15,14 +15,23 @@ enum : uint8_t {
   kSrcConst = 4,     // constant #arg (radix limbs, device table)
   kSrcTab = 5,       // per-lane table entry #arg
   kSrcTabDigit = 6,  // table entry = 4-bit digit #arg of this element's scalar (0 -> Montgomery one)
+  kSrcOpKeep = 7,    // B: the Op slot as left by the previous step (kPostOp)
+  kSrcMatTab = 8,    // matvec power-table entry of (column j, window w), arg = j * 16 + w, digit of E[i][col]
 };
-enum : uint8_t { kPostAcc = 1, kPostTab = 2, kPostOut = 4 };
+enum : uint8_t { kPostAcc = 1, kPostTab = 2, kPostOut = 4, kPostOp = 8, kPostGTab = 16 };
+constexpr int kMatWin = 6;  // matvec window bits (table of 2^6 powers per column and window)
 
 // constant table layout (ids), per modulus
 enum : int { kConstR2 = 0, kConstOneR = 1, kConstOne = 2, kConstFirstF = 3 };
 
 struct WStep {
   uint8_t asrc, aarg, bsrc, barg, post, tab, pad0, pad1;
+};
+
+struct MatvecGeom {
+  uint32_t* mtab = nullptr;
+  const uint64_t* expo = nullptr;
+  int cols = 0, nwin = 0, cc = 1, nch = 1, wcur = 0;
 };
 
 struct WideMod {  // host-side constants of one modulus in radix 2^rb

@@ -346,6 +346,47 @@ class Paillier:
         out = self.hom_scalar_mul_batch(np.array([k], np.uint64), self._cw([c]))
         return Ciphertext(L.limbs_to_int(out[0]), bits)
 
+    def hom_matvec_batch(self, alpha, expo, zv, window: int = 6):
+        """out_i = alpha_i prod_j zv_j^expo[i][j] mod n^2 on limb arrays; expo (rows, cols) uint64."""
+        rows = alpha.shape[0]
+        cols = zv.shape[0]
+        dev = hasattr(alpha, "is_cuda") and alpha.is_cuda
+        out = _torch().empty_like(alpha) if dev else np.zeros_like(alpha)
+        _raise_for(L.lib().pcb_hom_matvec(self._ctx, L.ptr(alpha), L.ptr(expo), L.ptr(zv), rows, cols, window,
+                                          L.ptr(out), self._stream() if dev else None), "hom_matvec")
+        return out
+
+    def hom_matvec(self, alpha, expo, zv, window: int = 6) -> list[Ciphertext]:
+        """Paillier::hom_matvec (paillier.cpp:441-493) incl. shape checks and plain_bits rules."""
+        rows, cols = len(alpha), len(zv)
+        if len(expo) != rows:
+            raise ValueError("exponent row count")
+        if any(len(r) != cols for r in expo):
+            raise ValueError("exponent row width")
+        if window < 1 or window > 8:
+            raise ValueError("window in [1,8]")
+        max_bits = max((int(k).bit_length() for r in expo for k in r), default=0)
+        zv_bits = max((c.plain_bits for c in zv), default=0)
+        sum_bits = max_bits + zv_bits + cols.bit_length() if cols else 0
+        bits = [max(a.plain_bits, sum_bits) + 1 for a in alpha]
+        for b in bits:
+            self._bump(b)
+        if rows == 0:
+            return []
+        E = np.array(expo, dtype=np.uint64).reshape(rows, cols)
+        out = self.hom_matvec_batch(self._cw(alpha), E, self._cw(zv) if cols else np.zeros((0, 2 * self.L), np.uint32),
+                                    window)
+        return [Ciphertext(v, b) for v, b in zip(L.limbs_to_ints(out), bits)]
+
+    def edge_step_batch(self, alpha, expo, zc, vc, window: int = 6):
+        """protocol.cpp:264-271: range check, zv = hom_add(z, v), then hom_matvec (square block)."""
+        cols = zc.shape[0]
+        dev = hasattr(alpha, "is_cuda") and alpha.is_cuda
+        out = _torch().empty_like(alpha) if dev else np.zeros_like(alpha)
+        _raise_for(L.lib().pcb_edge_step(self._ctx, L.ptr(alpha), L.ptr(expo), L.ptr(zc), L.ptr(vc), cols, window,
+                                         L.ptr(out), self._stream() if dev else None), "edge_step")
+        return out
+
     def aggregate(self, cs) -> Ciphertext:
         """prod c_i mod n^2; plain_bits follows a balanced hom_add tree (depth ceil(log2 count))."""
         cs = list(cs)

@@ -121,3 +121,92 @@ def test_aggregate_decrypts_to_sum():
     cs = ph.encrypt_vec(ms, P.Rng(3), True)
     agg = ph.aggregate(cs)
     assert ph.crt_decrypt(agg) == sum(ms) % kp.n
+
+
+def test_matvec_reference_recurrence_64bit():
+    # test_paillier.cpp:285-321: rows 5, cols 4, 14-bit exponents, a zero entry and a zero row
+    rng = P.Rng(77)
+    kp = P.keygen(rng, 64)
+    ph = P.Paillier(kp)
+    ork = O.Rng(77)
+    O.keygen(ork, 64)
+    n = kp.n
+    rows, cols = 5, 4
+    alpha_m = [ork.below(1 << 20) for _ in range(rows)]
+    zv_m = [ork.below(1 << 16) for _ in range(cols)]
+    expo = [[ork.below(1 << 14) for _ in range(cols)] for _ in range(rows)]
+    expo[2][1] = 0
+    expo[4] = [0, 0, 0, 0]
+    rng.state = ork.state
+    alpha = ph.encrypt_vec(alpha_m, rng, True)
+    zv = ph.encrypt_vec(zv_m, rng, True)
+    for window in (1, 3, 6):
+        ph.reset_counters()
+        out = ph.hom_matvec(alpha, expo, zv, window)
+        assert ph.counters()[0] == rows
+        for i in range(rows):
+            want = alpha_m[i]
+            for j in range(cols):
+                want = (want + expo[i][j] * zv_m[j] % n) % n
+            assert ph.crt_decrypt(out[i]) == want
+            assert out[i].plain_bits < n.bit_length()
+    ragged = [list(r) for r in expo]
+    ragged[1].pop()
+    with pytest.raises(ValueError):
+        ph.hom_matvec(alpha, ragged, zv)
+    with pytest.raises(ValueError):
+        ph.hom_matvec(alpha, expo, zv, 9)
+
+
+@pytest.mark.parametrize("idx,rows,cols", [(1, 17, 23), (2, 9, 40)])
+def test_matvec_matches_bigint_and_reference(idx, rows, cols):
+    kp = key(idx)
+    pub = P.Paillier(P.PublicKey(kp.n, kp.key_bits))
+    rnd = random.Random(rows * cols)
+    n2 = kp.n2
+    alpha = [rnd.randrange(1, n2) for _ in range(rows)]
+    zv = [rnd.randrange(1, n2) for _ in range(cols)]
+    expo = [[rnd.getrandbits(50) for _ in range(cols)] for _ in range(rows)]
+    expo[0] = [0] * cols
+    E = np.array(expo, np.uint64)
+    out = pub.hom_matvec_batch(L.ints_to_limbs(alpha, 2 * pub.L), E, L.ints_to_limbs(zv, 2 * pub.L))
+    got = L.limbs_to_ints(out)
+    for i in range(rows):
+        want = alpha[i]
+        for j in range(cols):
+            want = want * pow(zv[j], expo[i][j], n2) % n2
+        assert got[i] == want
+    import refbind as R_
+
+    if R_.available():
+        import ctypes as C
+
+        ref = R_.RefKey.keygen(golden("keys.json")[idx]["seed"], kp.key_bits)
+        A, Z = L.ints_to_limbs(alpha, 2 * pub.L), L.ints_to_limbs(zv, 2 * pub.L)
+        o = np.zeros_like(A)
+        rc = R_.lib().pcref_hom_matvec(ref.h, R_.a(A), None, R_.a(E), R_.a(Z), None, rows, cols, 6, 2 * pub.L,
+                                       R_.a(o), None, 1)
+        assert rc == 0 and (o == out).all()
+
+
+def test_edge_step_matches_bigint():
+    kp = key(1)
+    ph = P.Paillier(kp)
+    rnd = random.Random(5)
+    cols = 12
+    zc = [rnd.randrange(1, kp.n2) for _ in range(cols)]
+    vc = [rnd.randrange(1, kp.n2) for _ in range(cols)]
+    alpha = [rnd.randrange(1, kp.n2) for _ in range(cols)]
+    E = np.array([[rnd.getrandbits(50) for _ in range(cols)] for _ in range(cols)], np.uint64)
+    W = 2 * ph.L
+    out = ph.edge_step_batch(L.ints_to_limbs(alpha, W), E, L.ints_to_limbs(zc, W), L.ints_to_limbs(vc, W))
+    got = L.limbs_to_ints(out)
+    for i in range(cols):
+        want = alpha[i]
+        for j in range(cols):
+            want = want * pow(zc[j] * vc[j] % kp.n2, int(E[i, j]), kp.n2) % kp.n2
+        assert got[i] == want
+    bad = list(zc)
+    bad[3] = kp.n2  # protocol.cpp:264-266
+    with pytest.raises(ValueError):
+        ph.edge_step_batch(L.ints_to_limbs(alpha, W), E, L.ints_to_limbs(bad, W), L.ints_to_limbs(vc, W))
