@@ -134,12 +134,19 @@ pcb_status pcb_aggregate(pcb_ctx* ctx, const uint32_t* c, size_t count, uint32_t
 /* ---- fused quantize / dequantize (quantize.cpp, FP64 without contraction) ------------------ */
 
 /* Gamma2 (fine = 0, quantize.cpp:31-35) or Gamma1 (fine = 1, 37-41) of count doubles, then
- * encryption with r (as pcb_encrypt).  q_out (nullable) receives the quantized integers
+ * encryption with r (as pcb_encrypt; use_crt = 0 is the public-key form the edge uses for
+ * alpha, protocol.cpp:207-212).  q_out (nullable) receives the quantized integers
  * (u64, or u128 as lo/hi pairs when fine); clamps (nullable, host) receives {low, high}. */
 pcb_status pcb_quantize_encrypt(pcb_ctx* ctx, const double* v, size_t count, double z_min,
                                 double z_max, double delta, int fine, const uint32_t* r,
                                 int use_crt, uint32_t* c, uint64_t* q_out, uint64_t* clamps,
                                 pcb_stream stream);
+
+/* gamma2_vec / gamma1_vec (quantize.cpp:52-64) on the GPU: q_out gets u64 (fine = 0) or u128 as
+ * (lo, hi) pairs (fine = 1); clamps (nullable, host) receives {low, high}.  A non-finite value
+ * returns PCB_E_SHAPE (clamp_in throws invalid_argument, quantize.cpp:18-19). */
+pcb_status pcb_quantize(const double* v, size_t count, double z_min, double z_max, double delta, int fine,
+                        uint64_t* q_out, uint64_t* clamps, pcb_stream stream);
 
 /* Master block update (protocol.cpp:494-511): decrypt count updates, range-gate them
  * (check_update_range, protocol.cpp:20-27), inverse_quantize_x (quantize.cpp:84-112) with the

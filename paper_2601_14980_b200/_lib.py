@@ -70,6 +70,7 @@ SIGNATURES = {
     "pcb_aggregate": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _vp]),
     "pcb_quantize_encrypt": (C.c_int, [_vp, _vp, C.c_size_t, C.c_double, C.c_double, C.c_double, C.c_int, _vp,
                                        C.c_int, _vp, _vp, _u64p, _vp]),
+    "pcb_quantize": (C.c_int, [_vp, C.c_size_t, C.c_double, C.c_double, C.c_double, C.c_int, _vp, _u64p, _vp]),
     "pcb_decrypt_update": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double,
                                      C.c_double, _vp, _vp, _vp, _vp, _vp]),
     "pcb_modexp_batch": (C.c_int, [_vp, C.c_uint32, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp]),

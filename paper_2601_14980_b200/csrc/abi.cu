@@ -259,6 +259,9 @@ pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, doub
                            cudaStream_t stream);
 pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int32_t* st, size_t count,
                            cudaStream_t stream);
+pcb_status launch_update(const uint32_t* m, int L, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
+                         double zmin, double zmax, double delta, double kappa, double* x, double* z, double* v,
+                         int32_t* st, size_t count, cudaStream_t stream);
 enum SideMode : int { kSideEnc = 0, kSideDec = 1, kSidePow = 2 };
 template <int RB, int N, int TPI>
 pcb_status launch_side28(const uint32_t* mlimb, const uint32_t* mword, int mwords, const uint32_t* r2,
@@ -1123,6 +1126,107 @@ pcb_status pcb_edge_step(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo
   return e;
 }
 
+pcb_status pcb_decrypt_update(pcb_ctx* x, const uint32_t* c, size_t count, const uint64_t* rowsum, const uint64_t* q_z,
+                              const uint64_t* q_nv, double z_min, double z_max, double delta, double kappa, double* xo,
+                              double* zo, double* vo, int32_t* status, pcb_stream stream) {
+  if (!x || (count && (!c || !rowsum || !q_z || !q_nv || !xo || !zo || !vo))) return PCB_E_SHAPE;
+  if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
+    return PCB_E_SHAPE;  // check_spec (quantize.cpp:8-15)
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  Staged sc, sr, sz, sn, sx, szz, sv, ss;
+  uint32_t* m = nullptr;
+  int32_t* stv = nullptr;
+  pcb_status e = stage_in(c, count * 2 * x->L * 4, st, &sc);
+  if (!e) e = stage_in(rowsum, count * 8, st, &sr);
+  if (!e) e = stage_in(q_z, count * 8, st, &sz);
+  if (!e) e = stage_in(q_nv, count * 8, st, &sn);
+  if (!e) e = stage_in(xo, count * 8, st, &sx);  // in/out: staged in and copied back
+  if (!e) e = stage_in(zo, count * 8, st, &szz);
+  if (!e) e = stage_in(vo, count * 8, st, &sv);
+  if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+  stv = (int32_t*)ss.dev;
+  if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = scratch_alloc(count * x->L * 4, (void**)&m, st);
+  if (!e) e = dec_core(x, (const uint32_t*)sc.dev, count, m, stv, st);
+  if (!e)
+    e = launch_update(m, (int)x->L, (const uint64_t*)sr.dev, (const uint64_t*)sz.dev, (const uint64_t*)sn.dev, z_min,
+                      z_max, delta, kappa, (double*)sx.dev, (double*)szz.dev, (double*)sv.dev, stv, count, st);
+  std::vector<int32_t> hst(count);
+  if (!e) e = cuda_check(cudaMemcpyAsync(hst.data(), stv, count * 4, cudaMemcpyDeviceToHost, st));
+  for (auto* p : {&sx, &szz, &sv}) {
+    if (!e && p->host) {
+      p->bytes = count * 8;
+      e = cuda_check(cudaMemcpyAsync(p == &sx ? (void*)xo : p == &szz ? (void*)zo : (void*)vo, p->dev, count * 8,
+                                     cudaMemcpyDeviceToHost, st));
+    }
+  }
+  if (!e) e = unstage_out(status, &ss, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!ss.dev) scratch_free(stv, st);
+  scratch_free(m, st);
+  for (auto* p : {&sc, &sr, &sz, &sn, &sx, &szz, &sv, &ss}) unstage(p, st);
+  cudaStreamSynchronize(st);
+  if (!e) {
+    x->pow_half += 2 * (uint64_t)count;
+    for (int32_t v : hst)
+      if (v != PCB_OK) return (pcb_status)v;  // first failure, like the reference's throw
+  }
+  return e;
+}
+
+pcb_status pcb_quantize(const double* v, size_t count, double z_min, double z_max, double delta, int fine,
+                        uint64_t* q_out, uint64_t* clamps, pcb_stream stream) {
+  if (count && (!v || !q_out)) return PCB_E_SHAPE;
+  if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
+    return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Staged sv, sq;
+  unsigned long long* dclamps = nullptr;
+  int32_t* stv = nullptr;
+  uint32_t* dummy_r = nullptr;
+  uint32_t* dn = nullptr;
+  pcb_status e = stage_in(v, count * 8, st, &sv);
+  if (!e) e = stage_out(q_out, count * 8 * (fine ? 2 : 1), st, &sq);
+  if (!e) e = scratch_alloc(16, (void**)&dclamps, st);
+  if (!e) e = cuda_check(cudaMemsetAsync(dclamps, 0, 16, st));
+  if (!e) e = scratch_alloc(count * 4, (void**)&stv, st);
+  // the prep kernel also range-checks r against n: give it r = 1 and n = 2^128 so only the
+  // quantizer's own status (non-finite input) can fail
+  if (!e) e = scratch_alloc(count * 4, (void**)&dummy_r, st);
+  if (!e) e = scratch_alloc(5 * 4, (void**)&dn, st);
+  if (!e) {
+    std::vector<uint32_t> ones(count, 1), n128 = {0, 0, 0, 0, 1};
+    e = cuda_check(cudaMemcpyAsync(dummy_r, ones.data(), count * 4, cudaMemcpyHostToDevice, st));
+    if (!e) e = cuda_check(cudaMemcpyAsync(dn, n128.data(), 20, cudaMemcpyHostToDevice, st));
+    if (!e)
+      e = launch_enc_prep(nullptr, 0, (const double*)sv.dev, z_min, z_max, delta, fine, nullptr, 0, (uint64_t*)sq.dev,
+                          dclamps, dummy_r, dn, 1, stv, count, st);
+    if (!e) e = cuda_check(cudaStreamSynchronize(st));  // host vectors above are temporaries
+  }
+  if (!e) e = unstage_out(q_out, &sq, st);
+  unsigned long long hcl[2] = {0, 0};
+  std::vector<int32_t> hst(count);
+  if (!e) e = cuda_check(cudaMemcpyAsync(hcl, dclamps, 16, cudaMemcpyDeviceToHost, st));
+  if (!e) e = cuda_check(cudaMemcpyAsync(hst.data(), stv, count * 4, cudaMemcpyDeviceToHost, st));
+  if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  for (void* p : {(void*)dclamps, (void*)stv, (void*)dummy_r, (void*)dn}) scratch_free(p, st);
+  unstage(&sv, st);
+  unstage(&sq, st);
+  cudaStreamSynchronize(st);
+  if (!e && clamps) {
+    clamps[0] = hcl[0];
+    clamps[1] = hcl[1];
+  }
+  if (!e)
+    for (int32_t s2 : hst)
+      if (s2 != PCB_OK) return PCB_E_SHAPE;
+  return e;
+}
+
 pcb_status pcb_sample_r(pcb_ctx* x, uint64_t* rng_state, size_t count, uint32_t* r_out, pcb_stream stream) {
   if (!x || !rng_state || (count && !r_out)) return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
@@ -1152,13 +1256,51 @@ pcb_status pcb_quantize_encrypt(pcb_ctx* x, const double* v, size_t count, doubl
   // check_spec (quantize.cpp:8-15)
   if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
     return PCB_E_SHAPE;
-  if (!use_crt) return PCB_E_UNSUPPORTED;
-  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (use_crt && !x->has_prv) return PCB_E_NO_PRIVATE;
   if (count == 0) return PCB_OK;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
   Staged sv, sr, sc, sq;
   unsigned long long* dclamps = nullptr;
+  if (!use_crt) {  // public-key form: prep (quantize + checks) then n^2 encryption
+    uint32_t* mq = nullptr;
+    int32_t* stv = nullptr;
+    pcb_status e = stage_in(v, count * 8, st, &sv);
+    if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
+    if (!e) e = stage_out(c, count * 2 * x->L * 4, st, &sc);
+    if (!e) e = stage_out(q_out, q_out ? count * 8 * (fine ? 2 : 1) : 0, st, &sq);
+    if (!e) e = scratch_alloc(16, (void**)&dclamps, st);
+    if (!e) e = cuda_check(cudaMemsetAsync(dclamps, 0, 16, st));
+    if (!e) e = scratch_alloc(count * 4 * 4, (void**)&mq, st);
+    if (!e) e = scratch_alloc(count * 4, (void**)&stv, st);
+    if (!e)
+      e = launch_enc_prep(nullptr, 0, (const double*)sv.dev, z_min, z_max, delta, fine, mq, 4, (uint64_t*)sq.dev,
+                          dclamps, (const uint32_t*)sr.dev, x->d_n, (int)x->L, stv, count, st);
+    if (!e) e = cuda_check(cudaMemsetAsync(sc.dev, 0, count * 2 * x->L * 4, st));
+    if (!e) e = run_pub_enc(x, (const uint32_t*)sr.dev, mq, 4, stv, count, (uint32_t*)sc.dev, st);
+    if (!e) e = unstage_out(c, &sc, st);
+    if (!e) e = unstage_out(q_out, &sq, st);
+    unsigned long long hcl[2] = {0, 0};
+    std::vector<int32_t> hst(count);
+    if (!e && clamps) e = cuda_check(cudaMemcpyAsync(hcl, dclamps, 16, cudaMemcpyDeviceToHost, st));
+    if (!e) e = cuda_check(cudaMemcpyAsync(hst.data(), stv, count * 4, cudaMemcpyDeviceToHost, st));
+    if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+    scratch_free(mq, st);
+    scratch_free(stv, st);
+    scratch_free(dclamps, st);
+    for (auto* p : {&sv, &sr, &sc, &sq}) unstage(p, st);
+    cudaStreamSynchronize(st);
+    if (!e && clamps) {
+      clamps[0] = hcl[0];
+      clamps[1] = hcl[1];
+    }
+    if (!e) {
+      x->pow_full += (uint64_t)count;
+      for (int32_t s2 : hst)
+        if (s2 != PCB_OK) return (pcb_status)s2;
+    }
+    return e;
+  }
   pcb_status e = stage_in(v, count * 8, st, &sv);
   if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
   if (!e) e = stage_out(c, count * 2 * x->L * 4, st, &sc);
@@ -1273,8 +1415,4 @@ pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t*
 
 // ---- not yet implemented in this build (fail loudly, never fall back) -----------------------
 extern "C" {
-pcb_status pcb_decrypt_update(pcb_ctx*, const uint32_t*, size_t, const uint64_t*, const uint64_t*, const uint64_t*,
-                              double, double, double, double, double*, double*, double*, int32_t*, pcb_stream) {
-  return PCB_E_UNSUPPORTED;
-}
 }

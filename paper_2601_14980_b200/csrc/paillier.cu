@@ -11,6 +11,7 @@
 //
 // These run O(S^2) work per element against O(S^3) in the side kernel, so they favour simple
 // code: moduli live in block-shared memory (broadcast loads), one element per thread.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -95,8 +96,10 @@ __global__ void enc_prep_kernel(const __grid_constant__ EncPrepArgs P) {
         if (P.q_out) P.q_out[i] = lo;
       }
       uint32_t w[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
-      uint32_t* mo = P.m_out + (size_t)i * P.m_out_limbs;
-      for (int j = 0; j < P.m_out_limbs; j++) mo[j] = j < 4 ? w[j] : 0u;
+      if (P.m_out) {
+        uint32_t* mo = P.m_out + (size_t)i * P.m_out_limbs;
+        for (int j = 0; j < P.m_out_limbs; j++) mo[j] = j < 4 ? w[j] : 0u;
+      }
       if (status == PCB_OK && !lt_words(w, 4, P.n, P.L)) status = PCB_E_PLAINTEXT_RANGE;
     } else if (!lt_words(P.m + (size_t)i * P.m_limbs, P.m_limbs, P.n, P.L)) {
       status = PCB_E_PLAINTEXT_RANGE;  // check_plaintext (paillier.cpp:241-243)
@@ -268,6 +271,112 @@ __global__ void __launch_bounds__(kThreadsPerBlock) dec_finish_kernel(const __gr
     for (int j = 0; j < H; j++)
       if (H + j < P.L) out[H + j] = Hi[j];
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// Master block update (protocol.cpp:494-511): range gate, inverse quantization, soft threshold.
+// FP64 in the reference's operation order (built with --fmad=false).
+// ------------------------------------------------------------------------------------------
+// (double)u128, correctly rounded (__floatuntidf semantics)
+__device__ __forceinline__ double u128_to_double_rn(uint64_t lo, uint64_t hi) {
+  if (hi == 0) return __ull2double_rn(lo);
+  const int sh = 64 - __clzll((long long)hi);            // bits held by hi (1..64)
+  uint64_t top = (hi << (64 - sh)) | (sh == 64 ? 0ull : (lo >> sh));
+  if (sh == 64) top = hi;
+  const uint64_t rest = sh == 64 ? lo : (lo << (64 - sh));
+  top |= rest != 0 ? 1ull : 0ull;                          // sticky bit below the rounding point
+  return scalbn(__ull2double_rn(top), sh);
+}
+
+// BigNat::to_double (bignat.cpp:56-60): limb-wise v = v * 2^64 + (double)limb, top limb first
+__device__ __forceinline__ double bignat_to_double(uint64_t lo, uint64_t hi) {
+  double v = 0.0;
+  if (hi) v = __dadd_rn(__dmul_rn(v, 18446744073709551616.0), __ull2double_rn(hi));
+  return __dadd_rn(__dmul_rn(v, 18446744073709551616.0), __ull2double_rn(lo));
+}
+
+struct UpdateArgs {
+  const uint32_t* m;       // decrypted updates, count x L
+  int L;
+  const uint64_t* rowsum;  // Gamma2(B) row sums
+  const uint64_t* q_z;
+  const uint64_t* q_nv;
+  const double* sum_zv;    // device scalar (sequential sum, computed by sumzv_kernel)
+  double zmin, zmax, delta, kappa;
+  double* x;
+  double* z;
+  double* v;
+  int32_t* st;
+  int count;
+};
+
+// sum_j (2 zmin + step (q_z[j] + q_nv[j])) in the reference's sequential order (quantize.cpp:96-99)
+__global__ void sumzv_kernel(const uint64_t* q_z, const uint64_t* q_nv, int cols, double zmin, double zmax,
+                             double delta, double* out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const double step = __ddiv_rn(__dsub_rn(zmax, zmin), delta);
+  double s = 0.0;
+  for (int j = 0; j < cols; j++)
+    s = __dadd_rn(s, __dadd_rn(__dmul_rn(2.0, zmin),
+                               __dmul_rn(step, __dadd_rn(__ull2double_rn(q_z[j]), __ull2double_rn(q_nv[j])))));
+  *out = s;
+}
+
+__global__ void update_kernel(const __grid_constant__ UpdateArgs P) {
+  const double range = __dsub_rn(P.zmax, P.zmin);
+  const double step = __ddiv_rn(range, P.delta);
+  const double step2 = __dmul_rn(step, step);
+  const double cols = (double)P.count;
+  // check_update_range cap (protocol.cpp:23-24)
+  const double cap = __dadd_rn(__ddiv_rn(__dmul_rn(P.delta, P.delta), range),
+                               __dmul_rn(__dmul_rn(__dmul_rn(cols, P.delta), 2.0), P.delta));
+  const double lim = __dadd_rn(__dmul_rn(cap, 1.000001), 4.0);
+  const double szv = *P.sum_zv;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.count; i += gridDim.x * blockDim.x) {
+    if (P.st[i] != PCB_OK) continue;  // decryption already failed
+    const uint32_t* w = P.m + (size_t)i * P.L;
+    bool wide = false;
+    for (int j = 4; j < P.L; j++) wide = wide || w[j] != 0;
+    const uint64_t lo = (uint64_t)w[0] | ((uint64_t)(P.L > 1 ? w[1] : 0) << 32);
+    const uint64_t hi = (uint64_t)(P.L > 2 ? w[2] : 0) | ((uint64_t)(P.L > 3 ? w[3] : 0) << 32);
+    if (wide || (hi >> 63) || bignat_to_double(lo, hi) > lim) {  // bit_length > 127 or above the cap
+      P.st[i] = PCB_E_RANGE_UPDATE;
+      continue;
+    }
+    // inverse_quantize_x (quantize.cpp:105-110)
+    const double rowsum_b = __dadd_rn(__dmul_rn(cols, P.zmin), __dmul_rn(step, __ull2double_rn(P.rowsum[i])));
+    const double xi = __dsub_rn(
+        __dadd_rn(__dmul_rn(u128_to_double_rn(lo, hi), step2),
+                  __dmul_rn(P.zmin, __dadd_rn(__dadd_rn(1.0, __dmul_rn(2.0, rowsum_b)), szv))),
+        __dmul_rn(__dmul_rn(__dmul_rn(2.0, P.zmin), P.zmin), cols));
+    // protocol.cpp:504-511 + soft_threshold (admm.cpp:18-22)
+    const double xv = __dadd_rn(xi, P.v[i]);
+    double zz;
+    if (xv > P.kappa)
+      zz = __dsub_rn(xv, P.kappa);
+    else if (xv < -P.kappa)
+      zz = __dadd_rn(xv, P.kappa);
+    else
+      zz = 0.0;
+    P.x[i] = xi;
+    P.z[i] = zz;
+    P.v[i] = __dsub_rn(xv, zz);
+  }
+}
+
+pcb_status launch_update(const uint32_t* m, int L, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
+                         double zmin, double zmax, double delta, double kappa, double* x, double* z, double* v,
+                         int32_t* st, size_t count, cudaStream_t stream) {
+  double* szv = nullptr;
+  if (auto e = scratch_alloc(8, (void**)&szv, stream)) return e;
+  sumzv_kernel<<<1, 32, 0, stream>>>(q_z, q_nv, (int)count, zmin, zmax, delta, szv);
+  count_launch();
+  UpdateArgs P{m, L, rowsum, q_z, q_nv, szv, zmin, zmax, delta, kappa, x, z, v, st, (int)count};
+  const int grid = (int)std::min<size_t>((count + 255) / 256, 4096);
+  update_kernel<<<grid > 0 ? grid : 1, 256, 0, stream>>>(P);
+  count_launch();
+  scratch_free(szv, stream);
+  return cuda_check(cudaGetLastError());
 }
 
 // ------------------------------------------------------------------------------------------
