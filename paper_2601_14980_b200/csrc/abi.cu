@@ -709,6 +709,25 @@ static pcb_status dec_core(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t
       PCB_CASE(32)
       PCB_CASE(64)
 #undef PCB_CASE
+      case 96: {
+        const auto& k = *reinterpret_cast<const CrtDecConsts<96>*>(x->dec_blob.data());
+        const double mm = 2.0 * 96 * 96 + 96, alg = ((double)(x->nbits / 2) + (double)((x->nbits / 2 + 3) / 4)) * mm + 2 * mm;
+        e = fork_join(
+            x, st,
+            [&](cudaStream_t s2) {
+              return launch_side28<28, 112, 2>(x->rp2.mlimb.data(), x->rp2.mword.data(), x->rp2.mwords,
+                                               x->rp2.r2.data(), x->rp2_R3.data(), x->rp2.minv, opp, x->len_dec_p,
+                                               kTab, 1, c, 2 * (int)x->L, nullptr, 0, stv, count, yp, 96, s2, alg);
+            },
+            [&](cudaStream_t s2) {
+              return launch_side28<28, 112, 2>(x->rq2.mlimb.data(), x->rq2.mword.data(), x->rq2.mwords,
+                                               x->rq2.r2.data(), x->rq2_R3.data(), x->rq2.minv, opq, x->len_dec_q,
+                                               kTab, 1, c, 2 * (int)x->L, nullptr, 0, stv, count, yq, 96, s2, alg);
+            },
+            count);
+        if (!e) e = launch_dec_finish<96>(k, yp, yq, stv, m, (int)x->L, count, st);
+        break;
+      }
       default: e = PCB_E_UNSUPPORTED;
     }
   }
@@ -1194,17 +1213,18 @@ pcb_status pcb_quantize(const double* v, size_t count, double z_min, double z_ma
   if (!e) e = scratch_alloc(16, (void**)&dclamps, st);
   if (!e) e = cuda_check(cudaMemsetAsync(dclamps, 0, 16, st));
   if (!e) e = scratch_alloc(count * 4, (void**)&stv, st);
-  // the prep kernel also range-checks r against n: give it r = 1 and n = 2^128 so only the
-  // quantizer's own status (non-finite input) can fail
-  if (!e) e = scratch_alloc(count * 4, (void**)&dummy_r, st);
+  // the prep kernel also range-checks m and r against n: give it n = 2^160 - 1 (5 words) and
+  // r = 1, so only the quantizer's own status (non-finite input) can fail
+  if (!e) e = scratch_alloc(count * 5 * 4, (void**)&dummy_r, st);
   if (!e) e = scratch_alloc(5 * 4, (void**)&dn, st);
   if (!e) {
-    std::vector<uint32_t> ones(count, 1), n128 = {0, 0, 0, 0, 1};
-    e = cuda_check(cudaMemcpyAsync(dummy_r, ones.data(), count * 4, cudaMemcpyHostToDevice, st));
-    if (!e) e = cuda_check(cudaMemcpyAsync(dn, n128.data(), 20, cudaMemcpyHostToDevice, st));
+    std::vector<uint32_t> ones(count * 5, 0), nmax(5, 0xffffffffu);
+    for (size_t i = 0; i < count; i++) ones[i * 5] = 1;
+    e = cuda_check(cudaMemcpyAsync(dummy_r, ones.data(), count * 5 * 4, cudaMemcpyHostToDevice, st));
+    if (!e) e = cuda_check(cudaMemcpyAsync(dn, nmax.data(), 20, cudaMemcpyHostToDevice, st));
     if (!e)
       e = launch_enc_prep(nullptr, 0, (const double*)sv.dev, z_min, z_max, delta, fine, nullptr, 0, (uint64_t*)sq.dev,
-                          dclamps, dummy_r, dn, 1, stv, count, st);
+                          dclamps, dummy_r, dn, 5, stv, count, st);
     if (!e) e = cuda_check(cudaStreamSynchronize(st));  // host vectors above are temporaries
   }
   if (!e) e = unstage_out(q_out, &sq, st);

@@ -26,7 +26,8 @@ def test_session_bit_exact_vs_shadow(bits, m, n, k, iters, seed):
     a, y, _ = AO.gen_gaussian_problem(m, n, 0.1, seed)
     sizes = AO.split_columns(n, k)
     fac = factors_for(a, y, sizes)
-    spec = AO.session_bounds(a, y, 1.0, 1.0, iters, sizes, 1.5, 1e15, fac)
+    delta = 5e7 if bits == 64 else 1e15  # toy keys cap the update magnitude (acceptance.cpp:306)
+    spec = AO.session_bounds(a, y, 1.0, 1.0, iters, sizes, 1.5, delta, fac)
     keys = P.keygen(P.Rng(5 if bits == 64 else 1 ^ 0x6B657967656E2E2E), bits)
     cfg = ADMM.SessionConfig(nodes=k, iters=iters)
     res = ADMM.EncryptedSession(keys, cfg).run(a, y, factors=fac, spec=spec)
@@ -40,9 +41,9 @@ def test_session_gpu_factors_track_plaintext():
     a, y, _ = AO.gen_gaussian_problem(40, 60, 0.1, 3)
     sizes = AO.split_columns(60, 3)
     keys = P.keygen(P.Rng(5), 64)
-    cfg = ADMM.SessionConfig(nodes=3, iters=8)
+    cfg = ADMM.SessionConfig(nodes=3, iters=8, delta=1e8)  # test_protocol.cpp:128
     res = ADMM.EncryptedSession(keys, cfg).run(a, y)
     xs, _, _, objs = AO.lasso_admm_split(a, y, 1.0, 1.0, 8, sizes)
     for t in range(8):
         assert np.mean((res.x_trace[t] - xs[t]) ** 2) < 1e-10
-    assert np.allclose(res.objective, objs, rtol=1e-6)
+    assert abs(res.objective[-1] - objs[-1]) / objs[-1] < 1e-5  # test_protocol.cpp:150-152
