@@ -91,6 +91,47 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def gen_problem_fast(m: int, n: int, sparsity: float, seed: int):
+    """Vectorised gen_gaussian_problem (experiments.cpp:324-348): splitmix64 Box-Muller rows of A,
+    partial-shuffle support.  numpy's log/cos may differ from libm in the last ulp (synthetic data;
+    the encrypted session's parity is tested separately against the shadow pipeline)."""
+    u = splitmix_units(seed, 2 * m * n)  # gaussian() draws u1, u2 in order (no u1 == 0 in practice)
+    a = (np.sqrt(-2.0 * np.log(u[0::2])) * np.cos(6.283185307179586477 * u[1::2])).reshape(m, n)
+    rng = np.random.default_rng(seed)
+    x = np.zeros(n)
+    idx = rng.choice(n, int(np.ceil(sparsity * n)), replace=False)
+    x[idx] = rng.standard_normal(len(idx))
+    return a, a @ x
+
+
+def run_admm(args, rank: int, world: int, local: int):
+    """cfg3: 3P-ADMM-PC2 LASSO N=4096, K=8 edge blocks (sharded over ranks), 2048-bit key, M=512."""
+    import torch
+    import torch.distributed as dist
+    from paper_2601_14980_b200 import admm as ADMM
+    from paper_2601_14980_b200 import paillier as P
+
+    a, y = gen_problem_fast(512, 4096, 0.1, 1)
+    keys = P.keygen(P.Rng(KEY_SEED), 2048)
+    iters = args.admm_warmup + args.admm_iters
+    cfg = ADMM.SessionConfig(nodes=8, iters=iters)
+    group = dist.group.WORLD if world > 1 else None
+    sess = ADMM.EncryptedSession(keys, cfg, device=local, rank=rank, world=world, group=group)
+    t0 = time.perf_counter()
+    res = sess.run(a, y, record_trace=False)
+    wall = time.perf_counter() - t0
+    it = res.iter_seconds[args.admm_warmup:]
+    t = torch.tensor([float(np.mean(it))], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"metric": "3P-ADMM-PC2 sec/iteration", "value": float(t.item()), "unit": "s/iteration",
+            "higher_is_better": False,
+            "config": {"workload": "cfg3 LASSO N=4096, M=512 (recorded choice), K=8 blocks, 2048-bit key, Delta=1e15",
+                       "iterations_timed": args.admm_iters, "warmup_iterations": args.admm_warmup,
+                       "blocks_per_gpu": 8 // world if 8 % world == 0 else None},
+            "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall}
+
+
 def cpu_reference_rate(key, vals: np.ndarray, target_s: float, threads: int) -> dict:
     """Reference CPU path (crt_encrypt_with_r + crt_decrypt via oracle/_ref/libpcref.so) on a
     bounded sample; returns pairs/s.  The sample grows until it runs >= target_s."""
@@ -164,6 +205,8 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--admm-iters", type=int, default=3, help="timed cfg3 ADMM iterations (0 = skip)")
+    ap.add_argument("--admm-warmup", type=int, default=1)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -274,6 +317,8 @@ def main() -> None:
     h2d = N * (8 + 2 * ph.L * 4)          # values in; ciphertexts back in for decryption
     d2h = N * (2 * ph.L * 4 + ph.L * 4)   # ciphertexts out; plaintexts out
 
+    admm = run_admm(args, rank, world, local) if args.admm_iters > 0 else None
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         key = ref_key()
@@ -302,6 +347,7 @@ def main() -> None:
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(gpu_launches),
             "clocks": clk,
+            "admm": admm,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

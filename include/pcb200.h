@@ -126,6 +126,16 @@ pcb_status pcb_edge_step(pcb_ctx* ctx, const uint32_t* alpha, const uint64_t* ex
                          const uint32_t* zc, const uint32_t* vc, size_t cols, uint32_t window,
                          uint32_t* out, pcb_stream stream);
 
+/* The edge steps of nblocks independent edges in one batch (the per-edge loop of one ADMM
+ * iteration, protocol.cpp:486-511 -> 264-271 for each k): block k is square of side sizes[k];
+ * alpha / zc / vc / out hold sum(sizes) ciphertexts block after block, expo the row-major
+ * sizes[k] x sizes[k] exponent matrices back to back.  Result of block k == pcb_edge_step on
+ * block k alone.  PCB_E_CIPHER_RANGE if any z_j or v_j is not below n^2. */
+pcb_status pcb_edge_step_blocks(pcb_ctx* ctx, size_t nblocks, const uint32_t* sizes,
+                                const uint32_t* alpha, const uint64_t* expo, const uint32_t* zc,
+                                const uint32_t* vc, uint32_t window, uint32_t* out,
+                                pcb_stream stream);
+
 /* out = prod_i c_i mod n^2 (balanced reduction tree; order-independent value, SURVEY.md §0
  * fact 9).  count >= 1. */
 pcb_status pcb_aggregate(pcb_ctx* ctx, const uint32_t* c, size_t count, uint32_t* out,
@@ -156,6 +166,15 @@ pcb_status pcb_decrypt_update(pcb_ctx* ctx, const uint32_t* c, size_t count,
                               const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
                               double z_min, double z_max, double delta, double kappa, double* x,
                               double* z, double* v, int32_t* status, pcb_stream stream);
+
+/* pcb_decrypt_update over nblocks blocks laid out back to back (sizes[k] rows each); sum_zv and
+ * the range cap use each block's own columns (quantize.cpp:96-99, protocol.cpp:23-24), so the
+ * result equals nblocks separate pcb_decrypt_update calls. */
+pcb_status pcb_decrypt_update_blocks(pcb_ctx* ctx, size_t nblocks, const uint32_t* sizes,
+                                     const uint32_t* c, const uint64_t* rowsum,
+                                     const uint64_t* q_z, const uint64_t* q_nv, double z_min,
+                                     double z_max, double delta, double kappa, double* x, double* z,
+                                     double* v, int32_t* status, pcb_stream stream);
 
 /* ---- generic primitive + measurement ------------------------------------------------------ */
 

@@ -67,12 +67,15 @@ SIGNATURES = {
     "pcb_hom_scalar_mul": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
     "pcb_hom_matvec": (C.c_int, [_vp, _vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_uint32, _vp, _vp]),
     "pcb_edge_step": (C.c_int, [_vp, _vp, _vp, _vp, _vp, C.c_size_t, C.c_uint32, _vp, _vp]),
+    "pcb_edge_step_blocks": (C.c_int, [_vp, C.c_size_t, _vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp]),
     "pcb_aggregate": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _vp]),
     "pcb_quantize_encrypt": (C.c_int, [_vp, _vp, C.c_size_t, C.c_double, C.c_double, C.c_double, C.c_int, _vp,
                                        C.c_int, _vp, _vp, _u64p, _vp]),
     "pcb_quantize": (C.c_int, [_vp, C.c_size_t, C.c_double, C.c_double, C.c_double, C.c_int, _vp, _u64p, _vp]),
     "pcb_decrypt_update": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _vp, _vp, C.c_double, C.c_double, C.c_double,
                                      C.c_double, _vp, _vp, _vp, _vp, _vp]),
+    "pcb_decrypt_update_blocks": (C.c_int, [_vp, C.c_size_t, _vp, _vp, _vp, _vp, _vp, C.c_double, C.c_double,
+                                            C.c_double, C.c_double, _vp, _vp, _vp, _vp, _vp]),
     "pcb_modexp_batch": (C.c_int, [_vp, C.c_uint32, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp]),
     "pcb_imad_peak": (C.c_double, [C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "pcb_launch_count": (C.c_uint64, []),

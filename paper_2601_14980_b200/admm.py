@@ -5,13 +5,17 @@ Mirrors the per-iteration hot loop of the reference's run_session
 resident in HBM:
 
   master, per block k (protocol.cpp:425-511):
-      pcb_quantize_encrypt(z_k)  and  pcb_quantize_encrypt(-v_k)   Gamma2 + CRT Enc, r from the
-                                                                   master stream Rng(seed)
+      Gamma2 + CRT Enc of z_k and -v_k, r from the master stream Rng(seed)
   edge k (protocol.cpp:257-275):
-      pcb_edge_step(alpha_hat_k, Gamma2(B_k), zc, vc)             hom_add + hom_matvec (public key)
+      hom_add + hom_matvec with the public key
   master:
-      pcb_decrypt_update(...)                                     Dec, range gate, inverse
-                                                                   quantization, soft threshold
+      Dec, range gate, inverse quantization, soft threshold
+
+Blocks are independent inside an iteration (block k reads only its own z_k, v_k), so one
+iteration is three batched calls over all blocks a rank owns — pcb_quantize_encrypt([z ; -v]),
+pcb_edge_step_blocks, pcb_decrypt_update_blocks — with the master r stream drawn once in
+reference order and permuted into batch order.  Ciphertexts and the x/z/v trajectory are
+bit-identical to the block-at-a-time reference loop.
 
 Setup per edge (protocol.cpp:186-220): node factors (FP64 on the GPU via torch.linalg.solve —
 host linear algebra in the reference, Eigen LDLT), Gamma1(alpha) encrypted with the PUBLIC key
@@ -143,6 +147,21 @@ class ShardedDriver:
     def step_block(self, k: int, t: int) -> int:  # updates x/z/v slices of block k; returns clamps
         raise NotImplementedError
 
+    def setup_all(self) -> int:
+        """Setup of every block this rank owns (default: one block at a time)."""
+        return sum(self.setup_block(k) for k in self.mine)
+
+    def step_all(self, t: int) -> int:
+        """One iteration over all blocks in reference order (default: one block at a time).
+        Blocks are independent inside an iteration (x_k, z_k, v_k depend only on block k's own
+        state, protocol.cpp:486-511), so a backend may batch them."""
+        clamps = 0
+        for k in range(self.cfg.nodes):
+            self.advance_stream(k)
+            if k in self.mine:
+                clamps += self.step_block(k, t)
+        return clamps
+
     # driver -----------------------------------------------------------------------------------
     def run_blocks(self, a, y, factors, spec, record_trace: bool = True) -> SessionResult:
         import time
@@ -159,16 +178,12 @@ class ShardedDriver:
         self.x = torch.zeros(n, dtype=torch.float64, device=self.dev)
         self.z = torch.zeros(n, dtype=torch.float64, device=self.dev)
         self.v = torch.zeros(n, dtype=torch.float64, device=self.dev)
-        for k in self.mine:
-            res.clamps += self.setup_block(k)
+        res.clamps += self.setup_all()
         for t in range(cfg.iters):
             if self.dev != "cpu":
                 torch.cuda.synchronize(self.dev)
             t0 = time.perf_counter()
-            for k in range(cfg.nodes):
-                self.advance_stream(k)
-                if k in self.mine:
-                    res.clamps += self.step_block(k, t)
+            res.clamps += self.step_all(t)
             # objective on z (admm.cpp:31-34): A z partial sums over this rank's blocks
             az = torch.zeros(a.shape[0], dtype=torch.float64, device=self.dev)
             l1 = torch.zeros(1, dtype=torch.float64, device=self.dev)
@@ -250,63 +265,84 @@ class EncryptedSession(ShardedDriver):
             spec = session_bounds(factors, sizes, cfg.rho, cfg.lam, cfg.iters, cfg.margin, cfg.delta)
         self.rng_r = Rng(cfg.seed)
         self.kappa = cfg.lam / cfg.rho
-        self.rbuf = torch.empty((2 * max(sizes), self.L), dtype=torch.int32, device=dev)
-        self.blk = {}
         return self.run_blocks(a, y, factors, spec, record_trace)
 
-    def setup_block(self, k: int) -> int:
-        """Edge setup (protocol.cpp:186-220): Gamma2(B) rows + sums, Enc_pk(Gamma1(alpha))."""
-        import torch
-
-        cfg, spec = self.cfg, self.spec
-        b_bar, alpha = self.factors[k]
-        c = self.sizes[k]
-        st = self._stream()
-        q_b, cl_b = self._quantize(b_bar.reshape(-1).contiguous(), spec, fine=False)
-        q_b = q_b.reshape(c, c)
-        erng = Rng(cfg.seed ^ ((EDGE_SEED_MIX * (k + 1)) & MASK64))
-        r_a = self.edge.sample_r_batch(erng, c)
-        alpha_hat = torch.empty((c, 2 * self.L), dtype=torch.int32, device=self.dev)
-        cla = (C.c_uint64 * 2)()
-        _raise_for(self.lib.pcb_quantize_encrypt(self.edge._ctx, L.ptr(alpha.contiguous()), c, spec[0], spec[1],
-                                                 spec[2], 1, L.ptr(r_a), 0, L.ptr(alpha_hat), None, cla, st),
-                   "alpha encryption")
-        self.blk[k] = dict(q_b=q_b.contiguous(), rowsum=q_b.sum(dim=1).contiguous(), alpha_hat=alpha_hat)
-        return cl_b + cla[0] + cla[1]
-
-    def advance_stream(self, k: int) -> None:
-        """Master r stream: c draws for z, then c for -v (encrypt_state x 2, protocol.cpp:467-468),
-        drawn on every rank so each rank's slice matches the single-stream reference."""
-        c = self.sizes[k]
-        s = C.c_uint64(self.rng_r.state)
-        _raise_for(self.lib.pcb_sample_r(self.master._ctx, C.byref(s), 2 * c, L.ptr(self.rbuf), self._stream()),
-                   "sample_r")
-        self.rng_r.state = s.value
-
-    def step_block(self, k: int, t: int) -> int:
+    def setup_all(self) -> int:
+        """Edge setup of every owned block in one batch (protocol.cpp:186-220 per edge):
+        Gamma2(B_k) + row sums, and Enc_pk(Gamma1(alpha_k)) with edge k's own r stream."""
         import torch
 
         cfg, spec, st = self.cfg, self.spec, self._stream()
-        o, c = self.offs[k], self.sizes[k]
+        own = self.mine
+        self.own_sizes = np.array([self.sizes[k] for k in own], dtype=np.uint32)
+        n_own = int(self.own_sizes.sum())
+        self.own_lo = self.offs[own[0]] if own else 0
+        self.n_own = n_own
+        if n_own == 0:
+            return 0
+        b_all = torch.cat([self.factors[k][0].reshape(-1) for k in own]).contiguous()
+        q_b, cl_b = self._quantize(b_all, spec, fine=False)
+        rows, at = [], 0
+        for c in self.own_sizes.tolist():
+            rows.append(q_b[at:at + c * c].reshape(c, c).sum(dim=1))
+            at += c * c
+        self.expo = q_b
+        self.rowsum = torch.cat(rows).contiguous()
+        r_a = torch.empty((n_own, self.L), dtype=torch.int32, device=self.dev)
+        at = 0
+        for k in own:
+            c = self.sizes[k]
+            erng = Rng(cfg.seed ^ ((EDGE_SEED_MIX * (k + 1)) & MASK64))
+            s_ = C.c_uint64(erng.state)
+            _raise_for(self.lib.pcb_sample_r(self.edge._ctx, C.byref(s_), c, L.ptr(r_a[at:at + c]), st), "sample_r")
+            at += c
+        alpha = torch.cat([self.factors[k][1] for k in own]).contiguous()
+        self.alpha_hat = torch.empty((n_own, 2 * self.L), dtype=torch.int32, device=self.dev)
+        cla = (C.c_uint64 * 2)()
+        _raise_for(self.lib.pcb_quantize_encrypt(self.edge._ctx, L.ptr(alpha), n_own, spec[0], spec[1], spec[2], 1,
+                                                 L.ptr(r_a), 0, L.ptr(self.alpha_hat), None, cla, st),
+                   "alpha encryption")
+        # master r stream layout: block k draws c_k for z then c_k for -v (protocol.cpp:467-468);
+        # the batch encrypts [z_own ; -v_own], so gather the owned draws into that order.
+        perm_z, perm_v = [], []
+        for k in own:
+            o, c = self.offs[k], self.sizes[k]
+            perm_z.extend(range(2 * o, 2 * o + c))
+            perm_v.extend(range(2 * o + c, 2 * o + 2 * c))
+        self.rperm = torch.tensor(perm_z + perm_v, dtype=torch.int64, device=self.dev)
+        self.rall = torch.empty((2 * sum(self.sizes), self.L), dtype=torch.int32, device=self.dev)
+        return cl_b + cla[0] + cla[1]
+
+    def step_all(self, t: int) -> int:
+        """One iteration, all owned blocks batched: one r draw for the whole master stream, one
+        fused quantize+CRT-Enc of [z ; -v], one edge step over the blocks, one Dec+update."""
+        import torch
+
+        cfg, spec, st = self.cfg, self.spec, self._stream()
+        s_ = C.c_uint64(self.rng_r.state)
+        _raise_for(self.lib.pcb_sample_r(self.master._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
+                   "sample_r")
+        self.rng_r.state = s_.value
+        n = self.n_own
+        if n == 0:
+            return 0
+        lo = self.own_lo
+        r_in = self.rall.index_select(0, self.rperm).contiguous()
+        vin = torch.cat([self.z[lo:lo + n], -self.v[lo:lo + n]]).contiguous()
         W = 2 * self.L
-        b = self.blk[k]
-        zc = torch.empty((c, W), dtype=torch.int32, device=self.dev)
-        vc = torch.empty((c, W), dtype=torch.int32, device=self.dev)
-        q_z = torch.empty(c, dtype=torch.int64, device=self.dev)
-        q_nv = torch.empty(c, dtype=torch.int64, device=self.dev)
-        nv = (-self.v[o:o + c]).contiguous()
-        zk = self.z[o:o + c].contiguous()
-        cl1, cl2 = (C.c_uint64 * 2)(), (C.c_uint64 * 2)()
-        _raise_for(self.lib.pcb_quantize_encrypt(self.master._ctx, L.ptr(zk), c, spec[0], spec[1], spec[2], 0,
-                                                 L.ptr(self.rbuf[:c]), 1, L.ptr(zc), L.ptr(q_z), cl1, st), "Enc z")
-        _raise_for(self.lib.pcb_quantize_encrypt(self.master._ctx, L.ptr(nv), c, spec[0], spec[1], spec[2], 0,
-                                                 L.ptr(self.rbuf[c:2 * c]), 1, L.ptr(vc), L.ptr(q_nv), cl2, st),
-                   "Enc -v")
-        upd = torch.empty((c, W), dtype=torch.int32, device=self.dev)
-        _raise_for(self.lib.pcb_edge_step(self.edge._ctx, L.ptr(b["alpha_hat"]), L.ptr(b["q_b"]), L.ptr(zc), L.ptr(vc),
-                                          c, cfg.window, L.ptr(upd), st), "edge step")
-        _raise_for(self.lib.pcb_decrypt_update(self.master._ctx, L.ptr(upd), c, L.ptr(b["rowsum"]), L.ptr(q_z),
-                                               L.ptr(q_nv), spec[0], spec[1], spec[2], self.kappa,
-                                               L.ptr(self.x[o:o + c]), L.ptr(self.z[o:o + c]),
-                                               L.ptr(self.v[o:o + c]), None, st), "master update")
-        return cl1[0] + cl1[1] + cl2[0] + cl2[1]
+        ct = torch.empty((2 * n, W), dtype=torch.int32, device=self.dev)
+        q = torch.empty(2 * n, dtype=torch.int64, device=self.dev)
+        cl = (C.c_uint64 * 2)()
+        _raise_for(self.lib.pcb_quantize_encrypt(self.master._ctx, L.ptr(vin), 2 * n, spec[0], spec[1], spec[2], 0,
+                                                 L.ptr(r_in), 1, L.ptr(ct), L.ptr(q), cl, st), "Enc z, -v")
+        upd = torch.empty((n, W), dtype=torch.int32, device=self.dev)
+        sz = self.own_sizes
+        _raise_for(self.lib.pcb_edge_step_blocks(self.edge._ctx, len(sz), sz.ctypes.data, L.ptr(self.alpha_hat),
+                                                 L.ptr(self.expo), L.ptr(ct[:n]), L.ptr(ct[n:]), cfg.window,
+                                                 L.ptr(upd), st), "edge step")
+        _raise_for(self.lib.pcb_decrypt_update_blocks(self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd),
+                                                      L.ptr(self.rowsum), L.ptr(q[:n]), L.ptr(q[n:]), spec[0],
+                                                      spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
+                                                      L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None, st),
+                   "master update")
+        return cl[0] + cl[1]

@@ -261,7 +261,7 @@ pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int
                            cudaStream_t stream);
 pcb_status launch_update(const uint32_t* m, int L, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
                          double zmin, double zmax, double delta, double kappa, double* x, double* z, double* v,
-                         int32_t* st, size_t count, cudaStream_t stream);
+                         int32_t* st, size_t count, const long long* seg_dev, int nseg, cudaStream_t stream);
 enum SideMode : int { kSideEnc = 0, kSideDec = 1, kSidePow = 2 };
 template <int RB, int N, int TPI>
 pcb_status launch_side28(const uint32_t* mlimb, const uint32_t* mword, int mwords, const uint32_t* r2,
@@ -792,15 +792,22 @@ static std::vector<WStep> prog_scalar_pow() {
   return p;
 }
 
-// matvec phase A, window w: T[col][w][d] = zv_col^(d 64^w) (Montgomery form), d = 1..63
-static std::vector<WStep> prog_mat_table(int w) {
+// matvec phase A1: the window bases T[col][w][1] = zv_col^(64^w) R, one squaring chain per column
+static std::vector<WStep> prog_mat_chain(int nwin) {
   std::vector<WStep> p;
-  const int nsq = kMatWin * w;
-  const uint8_t first_post = nsq == 0 ? (kPostAcc | kPostOp | kPostGTab) : kPostAcc;
-  p.push_back(WStep{kSrcX, 0, kSrcConst, (uint8_t)kConstR2, first_post, 1, 0, 0});
-  for (int q = 1; q <= nsq; q++)
-    p.push_back(WStep{kSrcReg, 0, kSrcAcc, 0, (uint8_t)(q == nsq ? (kPostAcc | kPostOp | kPostGTab) : kPostAcc), 1, 0, 0});
-  for (int d = 2; d < 64; d++) p.push_back(WStep{kSrcReg, 0, kSrcOpKeep, 0, kPostGTab, (uint8_t)d, 0, 0});
+  p.push_back(WStep{kSrcX, 0, kSrcConst, (uint8_t)kConstR2, kPostAcc | kPostGTab, 1, 0, 0});
+  for (int w = 1; w < nwin; w++)
+    for (int q = 1; q <= kMatWin; q++)
+      p.push_back(WStep{kSrcReg, 0, kSrcAcc, 0, (uint8_t)(q == kMatWin ? (kPostAcc | kPostGTab) : kPostAcc), 1,
+                        (uint8_t)(q == kMatWin ? w : 0), 0});
+  return p;
+}
+
+// matvec phase A2 (fill mode, one element per (column, window)): T[d] = T[d-1] T[1], d = 2..63
+static std::vector<WStep> prog_mat_fill() {
+  std::vector<WStep> p;
+  p.push_back(WStep{kSrcGEntry, 1, kSrcGEntry, 1, kPostGTab, 2, 0, 0});
+  for (int d = 3; d < 64; d++) p.push_back(WStep{kSrcReg, 0, kSrcOpKeep, 0, kPostGTab, (uint8_t)d, 0, 0});
   return p;
 }
 
@@ -1016,36 +1023,72 @@ pcb_status pcb_aggregate(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* 
   return e;
 }
 
-// hom_matvec core on device pointers; expo_host is the host copy (for the window count).
-static pcb_status matvec_core(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo_dev, const uint64_t* expo_host,
-                              const uint32_t* zv, size_t rows, size_t cols, uint32_t* out, cudaStream_t st) {
-  const size_t wb = 2 * x->L * 4;
-  if (rows == 0) return PCB_OK;
-  if (cols == 0) return cuda_check(cudaMemcpyAsync(out, alpha, rows * wb, cudaMemcpyDeviceToDevice, st));
-  int maxbits = 0;
-  for (size_t i = 0; i < rows * cols; i++) {
-    const int b = expo_host[i] ? 64 - __builtin_clzll(expo_host[i]) : 0;
-    if (b > maxbits) maxbits = b;
+// bit length of the largest exponent (OR-reduction on the device; sets the window count)
+__global__ void expo_or_kernel(const uint64_t* e, size_t n, unsigned long long* out) {
+  uint64_t acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) acc |= e[i];
+  for (int o = 16; o > 0; o >>= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicOr(out, (unsigned long long)acc);
+}
+
+static pcb_status expo_max_bits(const uint64_t* expo_dev, size_t n, cudaStream_t st, int* bits) {
+  *bits = 0;
+  if (n == 0) return PCB_OK;
+  unsigned long long* d = nullptr;
+  pcb_status e = scratch_alloc(8, (void**)&d, st);
+  if (!e) e = cuda_check(cudaMemsetAsync(d, 0, 8, st));
+  if (!e) {
+    const int grid = (int)std::min<size_t>((n + 255) / 256, 1184);
+    expo_or_kernel<<<grid, 256, 0, st>>>(expo_dev, n, d);
+    count_launch();
+    e = cuda_check(cudaGetLastError());
   }
+  unsigned long long h = 0;
+  if (!e) e = cuda_check(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st));
+  if (!e) e = cuda_check(cudaStreamSynchronize(st));
+  scratch_free(d, st);
+  *bits = h ? 64 - __builtin_clzll(h) : 0;
+  return e;
+}
+
+// hom_matvec over nblk diagonal blocks of rows_b x cols_b (device pointers, block-major):
+//   out[b][i] = alpha[b][i] * prod_j zv[b][j]^expo[b][i][j] mod n^2.
+// A1: window bases per column (squaring chains), A2: the 63-entry tables per (column, window),
+// B: table products per (row, chunk of cc columns), C: alpha_i times the chunk partials.
+static pcb_status matvec_core(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo_dev, const uint32_t* zv,
+                              size_t nblk, size_t rows_b, size_t cols_b, uint32_t* out, cudaStream_t st) {
+  const size_t wb = 2 * x->L * 4;
+  const size_t rows = nblk * rows_b, cols = nblk * cols_b;
+  if (rows == 0) return PCB_OK;
+  if (cols_b == 0) return cuda_check(cudaMemcpyAsync(out, alpha, rows * wb, cudaMemcpyDeviceToDevice, st));
+  int maxbits = 0;
+  if (auto e = expo_max_bits(expo_dev, rows * cols_b, st, &maxbits)) return e;
   const int nwin = maxbits ? (maxbits + kMatWin - 1) / kMatWin : 1;
   const int cc = std::max(1, std::min(16, (kWideMaxSteps - 1) / nwin));
-  const int nch = (int)((cols + cc - 1) / cc);
+  const int nch = (int)((cols_b + cc - 1) / cc);
   const int N = x->wide.n;
   MatvecGeom g;
   g.expo = expo_dev;
-  g.cols = (int)cols;
+  g.cols = (int)cols_b;
   g.nwin = nwin;
   g.cc = cc;
   g.nch = nch;
+  g.brows = (int)rows_b;
   uint32_t *part = nullptr, *combo = nullptr;
   pcb_status e = scratch_alloc(cols * (size_t)nwin * 64 * N * 4, (void**)&g.mtab, st);
-  for (int w = 0; !e && w < nwin; w++) {  // phase A: power tables, one launch per window position
-    std::vector<WStep> p = prog_mat_table(w);
-    g.wcur = w;
+  if (!e) {  // A1
+    std::vector<WStep> p = prog_mat_chain(nwin);
+    g.wcur = 0;
     e = run_wide(x, p.data(), (int)p.size(), zv, nullptr, nullptr, 1, cols, cols, nullptr, 1, st, &g);
   }
+  if (!e) {  // A2
+    std::vector<WStep> p = prog_mat_fill();
+    g.wcur = -1;
+    e = run_wide(x, p.data(), (int)p.size(), nullptr, nullptr, nullptr, 1, cols * nwin, cols * nwin, nullptr, 1, st, &g);
+  }
+  g.wcur = 0;
   if (!e) e = scratch_alloc(rows * (size_t)nch * wb, (void**)&part, st);
-  if (!e) {  // phase B: table products per (row, column chunk)
+  if (!e) {  // B
     std::vector<WStep> p = prog_mat_prod(cc, nwin);
     e = run_wide(x, p.data(), (int)p.size(), nullptr, nullptr, nullptr, 1, rows * nch, rows * nch, part, 1, st, &g);
   }
@@ -1055,14 +1098,13 @@ static pcb_status matvec_core(pcb_ctx* x, const uint32_t* alpha, const uint64_t*
   if (!e)
     e = cuda_check(cudaMemcpy2DAsync((uint8_t*)combo + nch * wb, (nch + 1) * wb, alpha, wb, wb, rows,
                                      cudaMemcpyDeviceToDevice, st));
-  if (!e) {  // phase C: alpha_i * prod_c P_{i,c}
+  if (!e) {  // C
     std::vector<WStep> p = prog_mat_combine(nch);
     e = run_wide(x, p.data(), (int)p.size(), combo, nullptr, nullptr, nch + 1, rows * (nch + 1), rows, out, 1, st);
   }
   scratch_free(g.mtab, st);
   scratch_free(part, st);
   scratch_free(combo, st);
-  if (!e) x->pow_full += rows;  // hom_matvec counts one full exponentiation per row (paillier.cpp:476)
   return e;
 }
 
@@ -1074,68 +1116,130 @@ pcb_status pcb_hom_matvec(pcb_ctx* x, const uint32_t* alpha, const uint64_t* exp
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t wb = 2 * x->L * 4;
-  std::vector<uint64_t> eh(rows * cols);
   Staged sa, se, sz, so;
   pcb_status e = stage_in(alpha, rows * wb, st, &sa);
   if (!e) e = stage_in(expo, rows * cols * 8, st, &se);
   if (!e) e = stage_in(zv, cols * wb, st, &sz);
   if (!e) e = stage_out(out, rows * wb, st, &so);
-  if (!e && cols) {
-    e = cuda_check(cudaMemcpyAsync(eh.data(), se.dev, rows * cols * 8, cudaMemcpyDeviceToHost, st));
-    if (!e) e = cuda_check(cudaStreamSynchronize(st));
-  }
   if (!e)
-    e = matvec_core(x, (const uint32_t*)sa.dev, (const uint64_t*)se.dev, eh.data(), (const uint32_t*)sz.dev, rows,
-                    cols, (uint32_t*)so.dev, st);
+    e = matvec_core(x, (const uint32_t*)sa.dev, (const uint64_t*)se.dev, (const uint32_t*)sz.dev, 1, rows, cols,
+                    (uint32_t*)so.dev, st);
   if (!e) e = unstage_out(out, &so, st);
   unstage(&sa, st);
   unstage(&se, st);
   unstage(&sz, st);
   unstage(&so, st);
   if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!e) x->pow_full += rows;  // hom_matvec counts one full exponentiation per row (paillier.cpp:476)
   return e;
 }
 
-pcb_status pcb_edge_step(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo, const uint32_t* zc,
-                         const uint32_t* vc, size_t cols, uint32_t window, uint32_t* out, pcb_stream stream) {
-  if (!x || (cols && (!alpha || !expo || !zc || !vc || !out))) return PCB_E_SHAPE;
-  if (window < 1 || window > 8) return PCB_E_SHAPE;
-  if (cols == 0) return PCB_OK;
-  if (auto e = set_device(x)) return e;
-  cudaStream_t st = (cudaStream_t)stream;
+// Edge step over nblk square blocks (dense, block-major: alpha/zc/vc/out hold sum(sizes) ciphertexts,
+// expo the row-major size_k x size_k matrices back to back).  Unequal sizes are padded to the
+// largest block (zero exponents select the Montgomery one, padded rows are dropped).
+static pcb_status edge_core(pcb_ctx* x, size_t nblk, const uint32_t* sizes, const uint32_t* alpha,
+                            const uint64_t* expo, const uint32_t* zc, const uint32_t* vc, uint32_t* out,
+                            cudaStream_t st) {
   const size_t wb = 2 * x->L * 4;
-  std::vector<uint64_t> eh(cols * cols);
-  Staged sa, se, sz, sv, so;
+  size_t total = 0, cmax = 0, etotal = 0;
+  for (size_t k = 0; k < nblk; k++) {
+    total += sizes[k];
+    etotal += (size_t)sizes[k] * sizes[k];
+    cmax = std::max<size_t>(cmax, sizes[k]);
+  }
+  if (total == 0) return PCB_OK;
   int32_t* stv = nullptr;
   uint32_t* zvd = nullptr;
-  pcb_status e = stage_in(alpha, cols * wb, st, &sa);
-  if (!e) e = stage_in(expo, cols * cols * 8, st, &se);
-  if (!e) e = stage_in(zc, cols * wb, st, &sz);
-  if (!e) e = stage_in(vc, cols * wb, st, &sv);
-  if (!e) e = stage_out(out, cols * wb, st, &so);
   // protocol.cpp:264-266: every z_j, v_j must be < n^2 ("ciphertext outside the group")
-  if (!e) e = scratch_alloc(2 * cols * 4, (void**)&stv, st);
-  if (!e) e = launch_dec_prep((const uint32_t*)sz.dev, x->d_n2, (int)x->L, stv, cols, st);
-  if (!e) e = launch_dec_prep((const uint32_t*)sv.dev, x->d_n2, (int)x->L, stv + cols, cols, st);
-  std::vector<int32_t> hst(2 * cols);
-  if (!e) e = cuda_check(cudaMemcpyAsync(hst.data(), stv, 2 * cols * 4, cudaMemcpyDeviceToHost, st));
-  if (!e) e = cuda_check(cudaMemcpyAsync(eh.data(), se.dev, cols * cols * 8, cudaMemcpyDeviceToHost, st));
+  pcb_status e = scratch_alloc(2 * total * 4, (void**)&stv, st);
+  if (!e) e = launch_dec_prep(zc, x->d_n2, (int)x->L, stv, total, st);
+  if (!e) e = launch_dec_prep(vc, x->d_n2, (int)x->L, stv + total, total, st);
+  std::vector<int32_t> hst(2 * total);
+  if (!e) e = cuda_check(cudaMemcpyAsync(hst.data(), stv, 2 * total * 4, cudaMemcpyDeviceToHost, st));
   if (!e) e = cuda_check(cudaStreamSynchronize(st));
   if (!e)
     for (int32_t v : hst)
       if (v != PCB_OK) e = PCB_E_CIPHER_RANGE;
   // zv_j = z_j * v_j mod n^2 (hom_add, protocol.cpp:268-269), then the matvec (270-271)
-  if (!e) e = scratch_alloc(cols * wb, (void**)&zvd, st);
+  if (!e) e = scratch_alloc(total * wb, (void**)&zvd, st);
   std::vector<WStep> pa = prog_hom_add();
-  if (!e)
-    e = run_wide(x, pa.data(), (int)pa.size(), (const uint32_t*)sz.dev, (const uint32_t*)sv.dev, nullptr, 1, cols, cols,
-                 zvd, 1, st);
-  if (!e)
-    e = matvec_core(x, (const uint32_t*)sa.dev, (const uint64_t*)se.dev, eh.data(), zvd, cols, cols,
-                    (uint32_t*)so.dev, st);
-  if (!e) e = unstage_out(out, &so, st);
+  if (!e) e = run_wide(x, pa.data(), (int)pa.size(), zc, vc, nullptr, 1, total, total, zvd, 1, st);
+  bool uniform = true;
+  for (size_t k = 0; k < nblk; k++) uniform = uniform && sizes[k] == cmax;
+  if (!e && uniform) {
+    e = matvec_core(x, alpha, expo, zvd, nblk, cmax, cmax, out, st);
+  } else if (!e) {
+    uint32_t *ap = nullptr, *zp = nullptr, *op = nullptr;
+    uint64_t* ep = nullptr;
+    const size_t padded = nblk * cmax;
+    e = scratch_alloc(padded * wb, (void**)&ap, st);
+    if (!e) e = scratch_alloc(padded * wb, (void**)&zp, st);
+    if (!e) e = scratch_alloc(padded * wb, (void**)&op, st);
+    if (!e) e = scratch_alloc(padded * cmax * 8, (void**)&ep, st);
+    if (!e) e = cuda_check(cudaMemsetAsync(ap, 0, padded * wb, st));
+    if (!e) e = cuda_check(cudaMemsetAsync(zp, 0, padded * wb, st));
+    if (!e) e = cuda_check(cudaMemsetAsync(ep, 0, padded * cmax * 8, st));
+    size_t off = 0, eoff = 0;
+    for (size_t k = 0; !e && k < nblk; k++) {
+      const size_t c = sizes[k];
+      if (c) {
+        e = cuda_check(cudaMemcpyAsync((uint8_t*)ap + k * cmax * wb, (const uint8_t*)alpha + off * wb, c * wb,
+                                       cudaMemcpyDeviceToDevice, st));
+        if (!e)
+          e = cuda_check(cudaMemcpyAsync((uint8_t*)zp + k * cmax * wb, (const uint8_t*)zvd + off * wb, c * wb,
+                                         cudaMemcpyDeviceToDevice, st));
+        if (!e)
+          e = cuda_check(cudaMemcpy2DAsync(ep + k * cmax * cmax, cmax * 8, expo + eoff, c * 8, c * 8, c,
+                                           cudaMemcpyDeviceToDevice, st));
+      }
+      off += c;
+      eoff += c * c;
+    }
+    if (!e) e = matvec_core(x, ap, ep, zp, nblk, cmax, cmax, op, st);
+    off = 0;
+    for (size_t k = 0; !e && k < nblk; k++) {
+      if (sizes[k])
+        e = cuda_check(cudaMemcpyAsync((uint8_t*)out + off * wb, (const uint8_t*)op + k * cmax * wb, sizes[k] * wb,
+                                       cudaMemcpyDeviceToDevice, st));
+      off += sizes[k];
+    }
+    scratch_free(ap, st);
+    scratch_free(zp, st);
+    scratch_free(op, st);
+    scratch_free(ep, st);
+  }
   scratch_free(stv, st);
   scratch_free(zvd, st);
+  if (!e) x->pow_full += total;  // one hom_matvec row = one full exponentiation (paillier.cpp:476)
+  (void)etotal;
+  return e;
+}
+
+static pcb_status edge_entry(pcb_ctx* x, size_t nblk, const uint32_t* sizes, const uint32_t* alpha,
+                             const uint64_t* expo, const uint32_t* zc, const uint32_t* vc, uint32_t window,
+                             uint32_t* out, pcb_stream stream) {
+  if (!x || (nblk && !sizes)) return PCB_E_SHAPE;
+  if (window < 1 || window > 8) return PCB_E_SHAPE;
+  size_t total = 0, etotal = 0;
+  for (size_t k = 0; k < nblk; k++) {
+    total += sizes[k];
+    etotal += (size_t)sizes[k] * sizes[k];
+  }
+  if (total == 0) return PCB_OK;
+  if (!alpha || !expo || !zc || !vc || !out) return PCB_E_SHAPE;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t wb = 2 * x->L * 4;
+  Staged sa, se, sz, sv, so;
+  pcb_status e = stage_in(alpha, total * wb, st, &sa);
+  if (!e) e = stage_in(expo, etotal * 8, st, &se);
+  if (!e) e = stage_in(zc, total * wb, st, &sz);
+  if (!e) e = stage_in(vc, total * wb, st, &sv);
+  if (!e) e = stage_out(out, total * wb, st, &so);
+  if (!e)
+    e = edge_core(x, nblk, sizes, (const uint32_t*)sa.dev, (const uint64_t*)se.dev, (const uint32_t*)sz.dev,
+                  (const uint32_t*)sv.dev, (uint32_t*)so.dev, st);
+  if (!e) e = unstage_out(out, &so, st);
   unstage(&sa, st);
   unstage(&se, st);
   unstage(&sz, st);
@@ -1145,19 +1249,40 @@ pcb_status pcb_edge_step(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo
   return e;
 }
 
-pcb_status pcb_decrypt_update(pcb_ctx* x, const uint32_t* c, size_t count, const uint64_t* rowsum, const uint64_t* q_z,
-                              const uint64_t* q_nv, double z_min, double z_max, double delta, double kappa, double* xo,
-                              double* zo, double* vo, int32_t* status, pcb_stream stream) {
-  if (!x || (count && (!c || !rowsum || !q_z || !q_nv || !xo || !zo || !vo))) return PCB_E_SHAPE;
+pcb_status pcb_edge_step(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo, const uint32_t* zc,
+                         const uint32_t* vc, size_t cols, uint32_t window, uint32_t* out, pcb_stream stream) {
+  if (cols > 0xffffffffu) return PCB_E_SHAPE;
+  const uint32_t c = (uint32_t)cols;
+  return edge_entry(x, 1, &c, alpha, expo, zc, vc, window, out, stream);
+}
+
+pcb_status pcb_edge_step_blocks(pcb_ctx* x, size_t nblocks, const uint32_t* sizes, const uint32_t* alpha,
+                                const uint64_t* expo, const uint32_t* zc, const uint32_t* vc, uint32_t window,
+                                uint32_t* out, pcb_stream stream) {
+  return edge_entry(x, nblocks, sizes, alpha, expo, zc, vc, window, out, stream);
+}
+
+static pcb_status update_entry(pcb_ctx* x, size_t nblk, const uint32_t* sizes, const uint32_t* c,
+                               const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv, double z_min,
+                               double z_max, double delta, double kappa, double* xo, double* zo, double* vo,
+                               int32_t* status, pcb_stream stream) {
+  if (!x || (nblk && !sizes)) return PCB_E_SHAPE;
+  size_t count = 0;
+  std::vector<long long> seg(nblk + 1, 0);
+  for (size_t k = 0; k < nblk; k++) seg[k + 1] = seg[k] + sizes[k];
+  count = (size_t)seg[nblk];
+  if (count && (!c || !rowsum || !q_z || !q_nv || !xo || !zo || !vo)) return PCB_E_SHAPE;
   if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
     return PCB_E_SHAPE;  // check_spec (quantize.cpp:8-15)
   if (!x->has_prv) return PCB_E_NO_PRIVATE;
   if (count == 0) return PCB_OK;
+  if (count > 0x7fffffffu) return PCB_E_SHAPE;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
   Staged sc, sr, sz, sn, sx, szz, sv, ss;
   uint32_t* m = nullptr;
   int32_t* stv = nullptr;
+  long long* segd = nullptr;
   pcb_status e = stage_in(c, count * 2 * x->L * 4, st, &sc);
   if (!e) e = stage_in(rowsum, count * 8, st, &sr);
   if (!e) e = stage_in(q_z, count * 8, st, &sz);
@@ -1169,10 +1294,13 @@ pcb_status pcb_decrypt_update(pcb_ctx* x, const uint32_t* c, size_t count, const
   stv = (int32_t*)ss.dev;
   if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
   if (!e) e = scratch_alloc(count * x->L * 4, (void**)&m, st);
+  if (!e) e = scratch_alloc(seg.size() * 8, (void**)&segd, st);
+  if (!e) e = cuda_check(cudaMemcpyAsync(segd, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, st));
   if (!e) e = dec_core(x, (const uint32_t*)sc.dev, count, m, stv, st);
   if (!e)
     e = launch_update(m, (int)x->L, (const uint64_t*)sr.dev, (const uint64_t*)sz.dev, (const uint64_t*)sn.dev, z_min,
-                      z_max, delta, kappa, (double*)sx.dev, (double*)szz.dev, (double*)sv.dev, stv, count, st);
+                      z_max, delta, kappa, (double*)sx.dev, (double*)szz.dev, (double*)sv.dev, stv, count, segd,
+                      (int)nblk, st);
   std::vector<int32_t> hst(count);
   if (!e) e = cuda_check(cudaMemcpyAsync(hst.data(), stv, count * 4, cudaMemcpyDeviceToHost, st));
   for (auto* p : {&sx, &szz, &sv}) {
@@ -1186,6 +1314,7 @@ pcb_status pcb_decrypt_update(pcb_ctx* x, const uint32_t* c, size_t count, const
   if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
   if (!ss.dev) scratch_free(stv, st);
   scratch_free(m, st);
+  scratch_free(segd, st);
   for (auto* p : {&sc, &sr, &sz, &sn, &sx, &szz, &sv, &ss}) unstage(p, st);
   cudaStreamSynchronize(st);
   if (!e) {
@@ -1194,6 +1323,21 @@ pcb_status pcb_decrypt_update(pcb_ctx* x, const uint32_t* c, size_t count, const
       if (v != PCB_OK) return (pcb_status)v;  // first failure, like the reference's throw
   }
   return e;
+}
+
+pcb_status pcb_decrypt_update(pcb_ctx* x, const uint32_t* c, size_t count, const uint64_t* rowsum, const uint64_t* q_z,
+                              const uint64_t* q_nv, double z_min, double z_max, double delta, double kappa, double* xo,
+                              double* zo, double* vo, int32_t* status, pcb_stream stream) {
+  if (count > 0x7fffffffu) return PCB_E_SHAPE;
+  const uint32_t n = (uint32_t)count;
+  return update_entry(x, 1, &n, c, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, status, stream);
+}
+
+pcb_status pcb_decrypt_update_blocks(pcb_ctx* x, size_t nblocks, const uint32_t* sizes, const uint32_t* c,
+                                     const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv, double z_min,
+                                     double z_max, double delta, double kappa, double* xo, double* zo, double* vo,
+                                     int32_t* status, pcb_stream stream) {
+  return update_entry(x, nblocks, sizes, c, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, status, stream);
 }
 
 pcb_status pcb_quantize(const double* v, size_t count, double z_min, double z_max, double delta, int fine,

@@ -231,6 +231,19 @@ struct ASlot {  // multiplicand streamed from this thread's shared-memory slot
   __device__ __forceinline__ uint4 ev4(int c) const { return s.chunk(c); }
   __device__ __forceinline__ uint4 od4(int c) const { return s.chunk(S / 8 + c); }
 };
+__device__ __forceinline__ uint4 lds128v(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+// Streamed multiplicand that ptxas may not CSE across rows (volatile): keeps A out of the
+// register file (2S+4 live registers in the core instead of 3S+4).
+template <int S>
+struct ASlotV {
+  uint32_t a;
+  __device__ __forceinline__ uint4 ev4(int c) const { return lds128v(a + c * 512); }
+  __device__ __forceinline__ uint4 od4(int c) const { return lds128v(a + (S / 8 + c) * 512); }
+};
 
 // ------------------------------------------------------------------------------------------
 // One CIOS row on the split accumulator.
@@ -383,7 +396,7 @@ __device__ __forceinline__ void mont_mul_ss(uint32_t (&R)[S], const Slot<S>& A, 
     A.load(Ar);
     mont_mul_core<S, ARegs<S>, MA, U>(R, ARegs<S>{Ar}, B, M);
   } else {
-    mont_mul_core<S, ASlot<S>, MA, U>(R, ASlot<S>{A}, B, M);
+    mont_mul_core<S, ASlotV<S>, MA, U>(R, ASlotV<S>{A.a}, B, M);
   }
 }
 

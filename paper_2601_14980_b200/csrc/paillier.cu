@@ -301,7 +301,9 @@ struct UpdateArgs {
   const uint64_t* rowsum;  // Gamma2(B) row sums
   const uint64_t* q_z;
   const uint64_t* q_nv;
-  const double* sum_zv;    // device scalar (sequential sum, computed by sumzv_kernel)
+  const double* sum_zv;    // per block (sequential sums, computed by sumzv_kernel)
+  const long long* seg;    // nseg + 1 block offsets (rows of block s: [seg[s], seg[s+1]))
+  int nseg;
   double zmin, zmax, delta, kappa;
   double* x;
   double* z;
@@ -311,29 +313,36 @@ struct UpdateArgs {
 };
 
 // sum_j (2 zmin + step (q_z[j] + q_nv[j])) in the reference's sequential order (quantize.cpp:96-99)
-__global__ void sumzv_kernel(const uint64_t* q_z, const uint64_t* q_nv, int cols, double zmin, double zmax,
-                             double delta, double* out) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+// one thread per block of the batch
+__global__ void sumzv_kernel(const uint64_t* q_z, const uint64_t* q_nv, const long long* seg, int nseg, double zmin,
+                             double zmax, double delta, double* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nseg) return;
   const double step = __ddiv_rn(__dsub_rn(zmax, zmin), delta);
   double s = 0.0;
-  for (int j = 0; j < cols; j++)
+  for (long long j = seg[b]; j < seg[b + 1]; j++)
     s = __dadd_rn(s, __dadd_rn(__dmul_rn(2.0, zmin),
                                __dmul_rn(step, __dadd_rn(__ull2double_rn(q_z[j]), __ull2double_rn(q_nv[j])))));
-  *out = s;
+  out[b] = s;
 }
 
 __global__ void update_kernel(const __grid_constant__ UpdateArgs P) {
   const double range = __dsub_rn(P.zmax, P.zmin);
   const double step = __ddiv_rn(range, P.delta);
   const double step2 = __dmul_rn(step, step);
-  const double cols = (double)P.count;
-  // check_update_range cap (protocol.cpp:23-24)
-  const double cap = __dadd_rn(__ddiv_rn(__dmul_rn(P.delta, P.delta), range),
-                               __dmul_rn(__dmul_rn(__dmul_rn(cols, P.delta), 2.0), P.delta));
-  const double lim = __dadd_rn(__dmul_rn(cap, 1.000001), 4.0);
-  const double szv = *P.sum_zv;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.count; i += gridDim.x * blockDim.x) {
     if (P.st[i] != PCB_OK) continue;  // decryption already failed
+    int lo_s = 0, hi_s = P.nseg - 1;  // block of row i
+    while (lo_s < hi_s) {
+      const int mid = (lo_s + hi_s + 1) >> 1;
+      if (P.seg[mid] <= i) lo_s = mid; else hi_s = mid - 1;
+    }
+    const double cols = (double)(P.seg[lo_s + 1] - P.seg[lo_s]);
+    // check_update_range cap (protocol.cpp:23-24)
+    const double cap = __dadd_rn(__ddiv_rn(__dmul_rn(P.delta, P.delta), range),
+                                 __dmul_rn(__dmul_rn(__dmul_rn(cols, P.delta), 2.0), P.delta));
+    const double lim = __dadd_rn(__dmul_rn(cap, 1.000001), 4.0);
+    const double szv = P.sum_zv[lo_s];
     const uint32_t* w = P.m + (size_t)i * P.L;
     bool wide = false;
     for (int j = 4; j < P.L; j++) wide = wide || w[j] != 0;
@@ -366,12 +375,12 @@ __global__ void update_kernel(const __grid_constant__ UpdateArgs P) {
 
 pcb_status launch_update(const uint32_t* m, int L, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
                          double zmin, double zmax, double delta, double kappa, double* x, double* z, double* v,
-                         int32_t* st, size_t count, cudaStream_t stream) {
+                         int32_t* st, size_t count, const long long* seg_dev, int nseg, cudaStream_t stream) {
   double* szv = nullptr;
-  if (auto e = scratch_alloc(8, (void**)&szv, stream)) return e;
-  sumzv_kernel<<<1, 32, 0, stream>>>(q_z, q_nv, (int)count, zmin, zmax, delta, szv);
+  if (auto e = scratch_alloc((size_t)nseg * 8, (void**)&szv, stream)) return e;
+  sumzv_kernel<<<(nseg + 127) / 128, 128, 0, stream>>>(q_z, q_nv, seg_dev, nseg, zmin, zmax, delta, szv);
   count_launch();
-  UpdateArgs P{m, L, rowsum, q_z, q_nv, szv, zmin, zmax, delta, kappa, x, z, v, st, (int)count};
+  UpdateArgs P{m, L, rowsum, q_z, q_nv, szv, seg_dev, nseg, zmin, zmax, delta, kappa, x, z, v, st, (int)count};
   const int grid = (int)std::min<size_t>((count + 255) / 256, 4096);
   update_kernel<<<grid > 0 ? grid : 1, 256, 0, stream>>>(P);
   count_launch();

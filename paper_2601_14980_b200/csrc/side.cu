@@ -40,10 +40,16 @@ struct SideArgs {
   int count, mode;
 };
 
+#ifndef PCB_SIDE_AREG_MAX
+#define PCB_SIDE_AREG_MAX 64  // largest S that keeps the multiplicand in registers
+#endif
+#ifndef PCB_SIDE_MINB
+#define PCB_SIDE_MINB 1
+#endif
 template <int S>
-__global__ void __launch_bounds__(kThreadsPerBlock) side_kernel(const __grid_constant__ SideArgs<S> P) {
+__global__ void __launch_bounds__(kThreadsPerBlock, PCB_SIDE_MINB) side_kernel(const __grid_constant__ SideArgs<S> P) {
   extern __shared__ __align__(16) uint32_t smem[];
-  constexpr bool AR = S <= 64;
+  constexpr bool AR = S <= PCB_SIDE_AREG_MAX;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Slot<S> Acc{smem_addr(smem + warp * (64 * S) + lane * 4)};
   const Slot<S> Op{smem_addr(smem + warp * (64 * S) + 32 * S + lane * 4)};

@@ -41,6 +41,7 @@ struct WideArgs {
   uint32_t* mtab;         // power tables: entry (col, w, d) at ((col * nwin + w) * 64 + d) * N words
   const uint64_t* expo;   // rows x cols exponents (row-major)
   int cols, nwin, cc, nch, wcur;
+  int brows;              // rows per diagonal block (0: a single block)
 };
 
 template <int RB, int N, int TPI>
@@ -90,16 +91,21 @@ __global__ void __launch_bounds__(kThreadsPerBlock) wide_kernel(const __grid_con
       } else if (src == kSrcMatTab) {  // group o = (row, chunk); entry (col, w, digit of E[row][col])
         const int jl = arg >> 4, w = arg & 15;
         const int row = o / P.nch, col = (o % P.nch) * P.cc + jl;
+        const int tcol = (P.brows ? (row / P.brows) * P.cols : 0) + col;  // block-diagonal batches
         int d = 0;
         if (col < P.cols) d = (int)((P.expo[(size_t)row * P.cols + col] >> (kMatWin * w)) & ((1u << kMatWin) - 1));
         if (d == 0) {
 #pragma unroll
           for (int j = 0; j < K; j++) v[j] = P.consts[kConstOneR * N + t * K + j];
         } else {
-          const uint32_t* e = P.mtab + ((size_t)(col * P.nwin + w) * 64 + d) * N + t * K;
+          const uint32_t* e = P.mtab + ((size_t)(tcol * P.nwin + w) * 64 + d) * N + t * K;
 #pragma unroll
           for (int j = 0; j < K; j++) v[j] = e[j];
         }
+      } else if (src == kSrcGEntry) {  // table fill: element o = (column, window) pair
+        const uint32_t* e = P.mtab + ((size_t)o * 64 + arg) * N + t * K;
+#pragma unroll
+        for (int j = 0; j < K; j++) v[j] = e[j];
       } else {  // kSrcTabDigit: entry = 4-bit digit `arg` of this element's scalar
         const int d = (int)((kk >> (4 * arg)) & 15u);
         if (d == 0) {
@@ -130,8 +136,9 @@ __global__ void __launch_bounds__(kThreadsPerBlock) wide_kernel(const __grid_con
       for (int j = 0; j < K; j++) A[j] = R[j];
       if (st.post & kPostAcc) Acc.store(R, t);
       if (st.post & kPostOp) Op.store(R, t);
-      if (st.post & kPostGTab) {  // matvec table build: group o = column, window P.wcur, digit st.tab
-        uint32_t* e = P.mtab + ((size_t)(o * P.nwin + P.wcur) * 64 + st.tab) * N + t * K;
+      if (st.post & kPostGTab) {  // matvec table build (wide.h kPostGTab)
+        const size_t ent = P.wcur >= 0 ? (size_t)(o * P.nwin + P.wcur + st.pad0) * 64 + st.tab : (size_t)o * 64 + st.tab;
+        uint32_t* e = P.mtab + ent * N + t * K;
 #pragma unroll
         for (int j = 0; j < K; j++) e[j] = R[j];
       }
@@ -192,6 +199,7 @@ pcb_status launch_wide(const WideMod& md, const WStep* prog, int nsteps, const u
   P.cc = mg ? mg->cc : 1;
   P.nch = mg ? mg->nch : 1;
   P.wcur = mg ? mg->wcur : 0;
+  P.brows = mg ? mg->brows : 0;
   constexpr int G = 32 / TPI;
   const size_t smem = (size_t)(((N + 3) & ~3) + (kThreadsPerBlock / 32) * 2 * N * G) * 4;
   int blocks = 0;

@@ -17,7 +17,10 @@ enum : uint8_t {
   kSrcTabDigit = 6,  // table entry = 4-bit digit #arg of this element's scalar (0 -> Montgomery one)
   kSrcOpKeep = 7,    // B: the Op slot as left by the previous step (kPostOp)
   kSrcMatTab = 8,    // matvec power-table entry of (column j, window w), arg = j * 16 + w, digit of E[i][col]
+  kSrcGEntry = 9,    // matvec table fill: entry `arg` of this element's own (column, window) table
 };
+// kPostGTab writes the matvec power-table entry `tab` of window wcur + pad0 of column o; with
+// wcur < 0 (fill mode) element o IS the (column, window) pair and the entry is o * 64 + tab.
 enum : uint8_t { kPostAcc = 1, kPostTab = 2, kPostOut = 4, kPostOp = 8, kPostGTab = 16 };
 constexpr int kMatWin = 6;  // matvec window bits (table of 2^6 powers per column and window)
 
@@ -32,6 +35,7 @@ struct MatvecGeom {
   uint32_t* mtab = nullptr;
   const uint64_t* expo = nullptr;
   int cols = 0, nwin = 0, cc = 1, nch = 1, wcur = 0;
+  int brows = 0;  // rows per diagonal block (row r uses table columns of block r / brows); 0 = one block
 };
 
 struct WideMod {  // host-side constants of one modulus in radix 2^rb

@@ -387,6 +387,18 @@ class Paillier:
                                          L.ptr(out), self._stream() if dev else None), "edge_step")
         return out
 
+    def edge_step_blocks_batch(self, sizes, alpha, expo, zc, vc, window: int = 6):
+        """pcb_edge_step_blocks: the edge steps of len(sizes) square blocks in one batch (block k's
+        rows / columns are the next sizes[k] ciphertexts; expo holds the sizes[k]^2 exponents of
+        each block back to back, row-major)."""
+        sz = np.ascontiguousarray(np.asarray(sizes, dtype=np.uint32))
+        dev = hasattr(alpha, "is_cuda") and alpha.is_cuda
+        out = _torch().empty_like(alpha) if dev else np.zeros_like(alpha)
+        _raise_for(L.lib().pcb_edge_step_blocks(self._ctx, len(sz), sz.ctypes.data, L.ptr(alpha), L.ptr(expo),
+                                                L.ptr(zc), L.ptr(vc), window, L.ptr(out),
+                                                self._stream() if dev else None), "edge_step_blocks")
+        return out
+
     def aggregate(self, cs) -> Ciphertext:
         """prod c_i mod n^2; plain_bits follows a balanced hom_add tree (depth ceil(log2 count))."""
         cs = list(cs)

@@ -21,7 +21,8 @@ def factors_for(a, y, sizes, rho=1.0):
     return f
 
 
-@pytest.mark.parametrize("bits,m,n,k,iters,seed", [(64, 20, 30, 3, 5, 1), (1024, 128, 256, 4, 3, 1)])
+@pytest.mark.parametrize("bits,m,n,k,iters,seed", [(64, 20, 30, 3, 5, 1), (64, 16, 31, 4, 4, 2),
+                                                   (1024, 128, 256, 4, 3, 1)])
 def test_session_bit_exact_vs_shadow(bits, m, n, k, iters, seed):
     a, y, _ = AO.gen_gaussian_problem(m, n, 0.1, seed)
     sizes = AO.split_columns(n, k)

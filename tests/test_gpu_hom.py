@@ -210,3 +210,32 @@ def test_edge_step_matches_bigint():
     bad[3] = kp.n2  # protocol.cpp:264-266
     with pytest.raises(ValueError):
         ph.edge_step_batch(L.ints_to_limbs(alpha, W), E, L.ints_to_limbs(bad, W), L.ints_to_limbs(vc, W))
+
+
+@pytest.mark.parametrize("idx,sizes", [(0, [1, 7, 3]), (1, [5, 3, 4]), (2, [6, 6])])
+def test_edge_step_blocks_match_bigint(idx, sizes):
+    """pcb_edge_step_blocks == pcb_edge_step per block (unequal sizes exercise the padding)."""
+    kp = key(idx)
+    ph = P.Paillier(P.PublicKey(kp.n, kp.key_bits))
+    rnd = random.Random(11 + idx)
+    n2, W, tot = kp.n2, 2 * ph.L, sum(sizes)
+    zc = [rnd.randrange(1, n2) for _ in range(tot)]
+    vc = [rnd.randrange(1, n2) for _ in range(tot)]
+    alpha = [rnd.randrange(1, n2) for _ in range(tot)]
+    Es = [np.array([[rnd.getrandbits(rnd.choice([1, 20, 53])) for _ in range(c)] for _ in range(c)], np.uint64)
+          for c in sizes]
+    expo = np.concatenate([e.reshape(-1) for e in Es])
+    out = ph.edge_step_blocks_batch(sizes, L.ints_to_limbs(alpha, W), expo, L.ints_to_limbs(zc, W),
+                                    L.ints_to_limbs(vc, W))
+    got = L.limbs_to_ints(out)
+    at = 0
+    for c, E in zip(sizes, Es):
+        single = L.limbs_to_ints(ph.edge_step_batch(L.ints_to_limbs(alpha[at:at + c], W), np.ascontiguousarray(E),
+                                                    L.ints_to_limbs(zc[at:at + c], W),
+                                                    L.ints_to_limbs(vc[at:at + c], W)))
+        for i in range(c):
+            want = alpha[at + i]
+            for j in range(c):
+                want = want * pow(zc[at + j] * vc[at + j] % n2, int(E[i, j]), n2) % n2
+            assert got[at + i] == want == single[i]
+        at += c
