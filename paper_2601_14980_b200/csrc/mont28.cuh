@@ -22,6 +22,12 @@
 #pragma once
 #include <cstdint>
 
+// Row unroll of mm(): -1 = K rows (one register rotation, default), 0 = all N rows, r > 0 = r
+// rows where r divides N (else K).
+#ifndef PCB_R28_ROWS
+#define PCB_R28_ROWS -1
+#endif
+
 namespace pcb {
 namespace r28 {
 
@@ -82,8 +88,16 @@ __device__ __forceinline__ void mm(uint32_t (&R)[N / TPI], const uint32_t (&A)[N
   uint64_t T[K];
 #pragma unroll
   for (int j = 0; j < K; j++) T[j] = 0;
+  // Rows are unrolled K at a time: the one-slot shift per row rotates the accumulator's register
+  // names with period K, so a K-row body needs no moves, while the code stays 1/TPI of a full
+  // unroll (a fully unrolled 152-row product is ~460 KB of SASS and stalls on instruction fetch).
+  constexpr int RU = PCB_R28_ROWS == 0 ? N : ((PCB_R28_ROWS > 0 && N % PCB_R28_ROWS == 0) ? PCB_R28_ROWS : K);
+  static_assert(N % RU == 0, "row unroll must divide N");
+#pragma unroll 1
+  for (int i0 = 0; i0 < N; i0 += RU) {
 #pragma unroll
-  for (int i = 0; i < N; i++) {
+  for (int ii = 0; ii < RU; ii++) {
+    const int i = i0 + ii;
     const uint32_t b = B.digit(i);
 #pragma unroll
     for (int j = 0; j < K; j++) madw(T[j], A[j], b);
@@ -112,6 +126,7 @@ __device__ __forceinline__ void mm(uint32_t (&R)[N / TPI], const uint32_t (&A)[N
       T[K - 1] = in;
       T[0] += c0;
     }
+  }
   }
   // normalise to r-bit limbs (ALU pipe); carries across lanes in TPI-1 rounds
   uint64_t c = 0;
