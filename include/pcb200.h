@@ -95,6 +95,15 @@ pcb_status pcb_sample_r(pcb_ctx* ctx, uint64_t* rng_state, size_t count, uint32_
 pcb_status pcb_encrypt(pcb_ctx* ctx, const uint32_t* m, uint32_t m_limbs, const uint32_t* r,
                        size_t count, uint32_t* c, int use_crt, int32_t* status, pcb_stream stream);
 
+/* Offline/online split of encryption.  Offline: rn_i = r_i^n mod n^2, which is pcb_encrypt with
+ * m = 0 (the randomness stream does not depend on the data, so it can run ahead, e.g. during
+ * the previous ADMM iteration's edge step).  Online: c_i = (1 + m_i n) rn_i mod n^2 — bit-equal
+ * to crt_encrypt_with_r / encrypt_with_r (paillier.cpp:320-344) with the same r.  Per element:
+ * PCB_E_PLAINTEXT_RANGE if m >= n, PCB_E_RANDOMNESS_RANGE if rn is 0 or >= n^2 (c = 0).  Works on
+ * public-key contexts.  m: count x m_limbs u32, rn / c: count x 2L. */
+pcb_status pcb_encrypt_rn(pcb_ctx* ctx, const uint32_t* m, uint32_t m_limbs, const uint32_t* rn,
+                          size_t count, uint32_t* c, int32_t* status, pcb_stream stream);
+
 /* m_i = L(c_i^eps mod n^2) mu mod n.
  *   use_crt = 1: Paillier::crt_decrypt (paillier.cpp:354-361);  use_crt = 0: decrypt (346-352).
  * Both compute the same residue (c^(p-1) mod p^2 / L_p / h_p form + CRT on the device).

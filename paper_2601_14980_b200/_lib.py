@@ -62,6 +62,7 @@ SIGNATURES = {
     "pcb_ctx_reset_counters": (None, [_vp]),
     "pcb_sample_r": (C.c_int, [_vp, _u64p, C.c_size_t, _vp, _vp]),
     "pcb_encrypt": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_size_t, _vp, C.c_int, _vp, _vp]),
+    "pcb_encrypt_rn": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp, _vp]),
     "pcb_decrypt": (C.c_int, [_vp, _vp, C.c_size_t, _vp, C.c_int, _vp, _vp]),
     "pcb_hom_add": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
     "pcb_hom_scalar_mul": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),

@@ -12,9 +12,12 @@ resident in HBM:
       Dec, range gate, inverse quantization, soft threshold
 
 Blocks are independent inside an iteration (block k reads only its own z_k, v_k), so one
-iteration is three batched calls over all blocks a rank owns — pcb_quantize_encrypt([z ; -v]),
-pcb_edge_step_blocks, pcb_decrypt_update_blocks — with the master r stream drawn once in
-reference order and permuted into batch order.  Ciphertexts and the x/z/v trajectory are
+iteration is a few batched calls over all blocks a rank owns — pcb_quantize + pcb_encrypt_rn
+on [z ; -v], pcb_edge_step_blocks, pcb_decrypt_update_blocks — with the master r stream drawn
+once per iteration in reference order and permuted into batch order.  Encryption is split
+offline/online: rn = r^n mod n^2 for iteration t+1 (the expensive modexps; the r stream does not
+depend on the data) is computed on a side stream while iteration t's edge step runs, and the
+online part is c = (1 + m n) rn mod n^2.  Ciphertexts and the x/z/v trajectory are
 bit-identical to the block-at-a-time reference loop.
 
 Setup per edge (protocol.cpp:186-220): node factors (FP64 on the GPU via torch.linalg.solve —
@@ -229,6 +232,9 @@ class EncryptedSession(ShardedDriver):
         super().__init__(cfg, rank, world, group, device=f"cuda:{device}")
         self.device = device
         self.master = Paillier(keys, device=device)
+        # offline randomness rn = r^n mod n^2 runs on its own stream and context (the master's
+        # private key; separate internal side streams, so it never queues behind the master's Dec)
+        self.pre = Paillier(keys, device=device)
         self.edge = Paillier(PublicKey(keys.n, keys.key_bits), device=device)
         self.L = self.master.L
         self.lib = L.lib()
@@ -311,38 +317,68 @@ class EncryptedSession(ShardedDriver):
             perm_v.extend(range(2 * o + c, 2 * o + 2 * c))
         self.rperm = torch.tensor(perm_z + perm_v, dtype=torch.int64, device=self.dev)
         self.rall = torch.empty((2 * sum(self.sizes), self.L), dtype=torch.int32, device=self.dev)
+        self.rn = [torch.empty((2 * n_own, 2 * self.L), dtype=torch.int32, device=self.dev) for _ in range(2)]
+        self.m0 = torch.zeros((2 * n_own, 1), dtype=torch.int32, device=self.dev)
+        self.pstream = torch.cuda.Stream(device=self.device)
+        self.rn_ready = [torch.cuda.Event() for _ in range(2)]
+        self.enc_done = torch.cuda.Event()
         return cl_b + cla[0] + cla[1]
 
+
+    def _precompute(self, slot: int) -> None:
+        """Offline half of the next iteration's encryptions on the side stream: draw the master r
+        stream for ALL blocks (reference order), keep this rank's draws in batch order, and
+        rn = r^n mod n^2 = Enc(0; r)."""
+        import torch
+
+        ps = self.pstream
+        ps.wait_event(self.enc_done)  # the slot was last read by an earlier online encryption
+        with torch.cuda.stream(ps):
+            st = C.c_void_p(ps.cuda_stream)
+            s_ = C.c_uint64(self.rng_r.state)
+            _raise_for(self.lib.pcb_sample_r(self.pre._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
+                       "sample_r")
+            self.rng_r.state = s_.value
+            if self.n_own:
+                r_in = self.rall.index_select(0, self.rperm).contiguous()
+                _raise_for(self.lib.pcb_encrypt(self.pre._ctx, L.ptr(self.m0), 1, L.ptr(r_in), r_in.shape[0],
+                                                L.ptr(self.rn[slot]), 1, None, st), "offline encryption")
+            self.rn_ready[slot].record(ps)
+
     def step_all(self, t: int) -> int:
-        """One iteration, all owned blocks batched: one r draw for the whole master stream, one
-        fused quantize+CRT-Enc of [z ; -v], one edge step over the blocks, one Dec+update."""
+        """One iteration, all owned blocks batched: quantize [z ; -v] and encrypt online with the
+        precomputed rn, launch the offline half of iteration t+1 on the side stream, then one edge
+        step over the blocks and one Dec+update — all bit-equal to the block-at-a-time loop."""
         import torch
 
         cfg, spec, st = self.cfg, self.spec, self._stream()
-        s_ = C.c_uint64(self.rng_r.state)
-        _raise_for(self.lib.pcb_sample_r(self.master._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
-                   "sample_r")
-        self.rng_r.state = s_.value
+        slot = t % 2
+        if t == 0:
+            self._precompute(slot)
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_event(self.rn_ready[slot])
         n = self.n_own
-        if n == 0:
-            return 0
-        lo = self.own_lo
-        r_in = self.rall.index_select(0, self.rperm).contiguous()
-        vin = torch.cat([self.z[lo:lo + n], -self.v[lo:lo + n]]).contiguous()
-        W = 2 * self.L
-        ct = torch.empty((2 * n, W), dtype=torch.int32, device=self.dev)
-        q = torch.empty(2 * n, dtype=torch.int64, device=self.dev)
-        cl = (C.c_uint64 * 2)()
-        _raise_for(self.lib.pcb_quantize_encrypt(self.master._ctx, L.ptr(vin), 2 * n, spec[0], spec[1], spec[2], 0,
-                                                 L.ptr(r_in), 1, L.ptr(ct), L.ptr(q), cl, st), "Enc z, -v")
-        upd = torch.empty((n, W), dtype=torch.int32, device=self.dev)
-        sz = self.own_sizes
-        _raise_for(self.lib.pcb_edge_step_blocks(self.edge._ctx, len(sz), sz.ctypes.data, L.ptr(self.alpha_hat),
-                                                 L.ptr(self.expo), L.ptr(ct[:n]), L.ptr(ct[n:]), cfg.window,
-                                                 L.ptr(upd), st), "edge step")
-        _raise_for(self.lib.pcb_decrypt_update_blocks(self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd),
-                                                      L.ptr(self.rowsum), L.ptr(q[:n]), L.ptr(q[n:]), spec[0],
-                                                      spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
-                                                      L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None, st),
-                   "master update")
-        return cl[0] + cl[1]
+        clamps = 0
+        if n:
+            lo = self.own_lo
+            W = 2 * self.L
+            vin = torch.cat([self.z[lo:lo + n], -self.v[lo:lo + n]]).contiguous()
+            q, clamps = self._quantize(vin, spec, fine=False)
+            ct = torch.empty((2 * n, W), dtype=torch.int32, device=self.dev)
+            _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(self.rn[slot]), 2 * n, L.ptr(ct),
+                                               None, st), "Enc z, -v")
+        self.enc_done.record(cur)
+        if t + 1 < cfg.iters:
+            self._precompute(1 - slot)
+        if n:
+            upd = torch.empty((n, W), dtype=torch.int32, device=self.dev)
+            sz = self.own_sizes
+            _raise_for(self.lib.pcb_edge_step_blocks(self.edge._ctx, len(sz), sz.ctypes.data, L.ptr(self.alpha_hat),
+                                                     L.ptr(self.expo), L.ptr(ct[:n]), L.ptr(ct[n:]), cfg.window,
+                                                     L.ptr(upd), st), "edge step")
+            _raise_for(self.lib.pcb_decrypt_update_blocks(self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd),
+                                                          L.ptr(self.rowsum), L.ptr(q[:n]), L.ptr(q[n:]), spec[0],
+                                                          spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
+                                                          L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None,
+                                                          st), "master update")
+        return clamps

@@ -257,6 +257,8 @@ pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, doub
                            int fine, uint32_t* m_out, int m_out_limbs, uint64_t* q_out, unsigned long long* clamps,
                            const uint32_t* r, const uint32_t* n_dev, int L, int32_t* st, size_t count,
                            cudaStream_t stream);
+pcb_status launch_onepmn(const uint32_t* m, int ml, const uint32_t* rn, const uint32_t* n_dev, const uint32_t* n2_dev,
+                         int L, uint32_t* out, int32_t* st, size_t count, cudaStream_t stream);
 pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int32_t* st, size_t count,
                            cudaStream_t stream);
 pcb_status launch_update(const uint32_t* m, int L, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
@@ -904,6 +906,44 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
     else
       x->pow_full += (uint64_t)count;      // encrypt_with_r: r^n mod n^2 (paillier.cpp:325)
   }
+  return e;
+}
+
+// Online encryption with precomputed randomness: c = (1 + m n) rn mod n^2, rn = r^n mod n^2
+// (= pcb_encrypt(m = 0, r)); the value equals crt_encrypt_with_r(m, r) / encrypt_with_r(m, r).
+pcb_status pcb_encrypt_rn(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* rn, size_t count,
+                          uint32_t* c, int32_t* status, pcb_stream stream) {
+  if (!x || (count && (!m || !rn || !c))) return PCB_E_SHAPE;
+  if (m_limbs == 0 || m_limbs > x->L) return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t wb = 2 * x->L * 4;
+  Staged sm, sr, sc, ss;
+  uint32_t* b = nullptr;
+  pcb_status e = stage_in(m, count * m_limbs * 4, st, &sm);
+  if (!e) e = stage_in(rn, count * wb, st, &sr);
+  if (!e) e = stage_out(c, count * wb, st, &sc);
+  if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+  int32_t* stv = (int32_t*)ss.dev;
+  if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = scratch_alloc(count * wb, (void**)&b, st);
+  if (!e)
+    e = launch_onepmn((const uint32_t*)sm.dev, (int)m_limbs, (const uint32_t*)sr.dev, x->d_n, x->d_n2, (int)x->L, b,
+                      stv, count, st);
+  std::vector<WStep> p = prog_hom_add();  // (1 + m n) * rn mod n^2; failed rows have b = 0 -> c = 0
+  if (!e) e = run_wide(x, p.data(), (int)p.size(), (const uint32_t*)sr.dev, b, nullptr, 1, count, count,
+                       (uint32_t*)sc.dev, 1, st);
+  if (!e) e = unstage_out(c, &sc, st);
+  if (!e) e = unstage_out(status, &ss, st);
+  scratch_free(b, st);
+  if (!ss.dev) scratch_free(stv, st);
+  const bool any_host = sm.host || sr.host || sc.host || ss.host;
+  unstage(&sm, st);
+  unstage(&sr, st);
+  unstage(&sc, st);
+  unstage(&ss, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
   return e;
 }
 

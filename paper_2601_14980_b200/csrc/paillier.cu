@@ -406,6 +406,72 @@ pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, doub
   return cuda_check(cudaGetLastError());
 }
 
+// Online half of an offline/online encryption (pcb_encrypt_rn): out = 1 + m n  (2L words, < n^2
+// when m < n), with the checks of crt_encrypt_with_r (paillier.cpp:330-336) applied to m and the
+// precomputed rn = r^n mod n^2 (0 < rn < n^2).  Failed elements get out = 0.
+struct OnePmnArgs {
+  const uint32_t* m;   // count x ml
+  int ml;
+  const uint32_t* rn;  // count x 2L
+  const uint32_t* n;   // L limbs (device)
+  const uint32_t* n2;  // 2L limbs (device)
+  int L;
+  uint32_t* out;       // count x 2L
+  int32_t* st;
+  int count;
+};
+
+__global__ void onepmn_kernel(const __grid_constant__ OnePmnArgs P) {
+  const int W = 2 * P.L;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.count; i += gridDim.x * blockDim.x) {
+    const uint32_t* mi = P.m + (size_t)i * P.ml;
+    const uint32_t* ri = P.rn + (size_t)i * W;
+    uint32_t* o = P.out + (size_t)i * W;
+    int cmp = 0;  // m vs n
+    for (int j = max(P.ml, P.L) - 1; j >= 0 && cmp == 0; j--) {
+      const uint32_t a = j < P.ml ? mi[j] : 0u, b = j < P.L ? P.n[j] : 0u;
+      cmp = a < b ? -1 : (a > b ? 1 : 0);
+    }
+    int rc = 0;  // rn vs n^2
+    bool nz = false;
+    for (int j = W - 1; j >= 0; j--) {
+      const uint32_t a = ri[j], b = P.n2[j];
+      nz = nz || a != 0;
+      if (rc == 0) rc = a < b ? -1 : (a > b ? 1 : 0);
+    }
+    const int32_t s = cmp >= 0 ? PCB_E_PLAINTEXT_RANGE : ((rc >= 0 || !nz) ? PCB_E_RANDOMNESS_RANGE : PCB_OK);
+    P.st[i] = s;
+    for (int k = 0; k < W; k++) o[k] = 0;
+    if (s != PCB_OK) continue;
+    int mt = P.ml < P.L ? P.ml : P.L;
+    while (mt > 0 && mi[mt - 1] == 0) mt--;
+    for (int a = 0; a < mt; a++) {
+      uint64_t carry = 0;
+      for (int b = 0; b < P.L; b++) {
+        const uint64_t t = (uint64_t)mi[a] * P.n[b] + o[a + b] + carry;
+        o[a + b] = (uint32_t)t;
+        carry = t >> 32;
+      }
+      o[a + P.L] = (uint32_t)carry;
+    }
+    uint64_t c = 1;
+    for (int k = 0; k < W && c; k++) {
+      const uint64_t t = (uint64_t)o[k] + c;
+      o[k] = (uint32_t)t;
+      c = t >> 32;
+    }
+  }
+}
+
+pcb_status launch_onepmn(const uint32_t* m, int ml, const uint32_t* rn, const uint32_t* n_dev, const uint32_t* n2_dev,
+                         int L, uint32_t* out, int32_t* st, size_t count, cudaStream_t stream) {
+  OnePmnArgs P{m, ml, rn, n_dev, n2_dev, L, out, st, (int)count};
+  const int grid = (int)std::min<size_t>((count + 127) / 128, 4096);
+  onepmn_kernel<<<grid > 0 ? grid : 1, 128, 0, stream>>>(P);
+  count_launch();
+  return cuda_check(cudaGetLastError());
+}
+
 pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int32_t* st, size_t count,
                            cudaStream_t stream) {
   DecPrepArgs P{c, n2_dev, L, st, (int)count};

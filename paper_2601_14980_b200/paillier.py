@@ -196,6 +196,18 @@ class Paillier:
         _raise_for(rc, "encrypt")
         return c
 
+    def encrypt_rn_batch(self, m, rn, status=None):
+        """Online encryption with precomputed randomness rn = r^n mod n^2 (= encrypt_batch(0, r)):
+        c = (1 + m n) rn mod n^2, equal to encrypt_batch(m, r)."""
+        torch = _torch()
+        count, ml = m.shape
+        dev = m.is_cuda if hasattr(m, "is_cuda") else False
+        c = torch.empty((count, 2 * self.L), dtype=torch.int32, device=m.device) if dev else \
+            np.zeros((count, 2 * self.L), np.uint32)
+        _raise_for(L.lib().pcb_encrypt_rn(self._ctx, L.ptr(m), ml, L.ptr(rn), count, L.ptr(c), L.ptr(status),
+                                          self._stream() if dev else None), "encrypt_rn")
+        return c
+
     def decrypt_batch(self, c, use_crt: bool = True, status=None):
         torch = _torch()
         self._need_prv()

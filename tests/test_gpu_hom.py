@@ -239,3 +239,24 @@ def test_edge_step_blocks_match_bigint(idx, sizes):
                 want = want * pow(zc[at + j] * vc[at + j] % n2, int(E[i, j]), n2) % n2
             assert got[at + i] == want == single[i]
         at += c
+
+
+def test_encrypt_rn_equals_encrypt(kk):
+    """Offline/online split: pcb_encrypt_rn(m, pcb_encrypt(0, r)) == pcb_encrypt(m, r) (== the
+    reference's crt_encrypt_with_r golden ciphertexts), on private and public contexts."""
+    idx, kp, ph, pub = kk
+    e = golden("encrypt.json")[idx]
+    ms, rs, cs = [H(v) for v in e["m"]], [H(v) for v in e["r"]], [H(v) for v in e["c"]]
+    R = L.ints_to_limbs(rs, ph.L)
+    rn = ph.encrypt_batch(L.ints_to_limbs([0] * len(rs), 1), R, use_crt=True)
+    assert L.limbs_to_ints(rn) == [pow(r, kp.n, kp.n2) for r in rs]
+    for ctx in (ph, pub):
+        st = np.zeros(len(ms), np.int32)
+        c = ctx.encrypt_rn_batch(L.ints_to_limbs(ms, ctx.L), rn, status=st)
+        assert (st == 0).all() and L.limbs_to_ints(c) == cs
+    bad_m = [kp.n, kp.n + 5, 3, 4]
+    bad_rn = [5, 5, 0, kp.n2]
+    st = np.zeros(4, np.int32)
+    c = pub.encrypt_rn_batch(L.ints_to_limbs(bad_m, pub.L), L.ints_to_limbs(bad_rn, 2 * pub.L), status=st)
+    assert st.tolist() == [1, 1, 2, 2]  # PLAINTEXT_RANGE, RANDOMNESS_RANGE
+    assert not L.limbs_to_ints(c)[0] and not L.limbs_to_ints(c)[3]
