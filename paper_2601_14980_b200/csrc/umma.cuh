@@ -1,0 +1,96 @@
+// umma.cuh — minimal tcgen05 (5th-gen tensor core) helpers for sm_100a: int8 MMA with int32
+// accumulation in TMEM, shared-memory matrix descriptors for the no-swizzle K-major layout,
+// TMEM allocation / loads, and the mbarrier completion handshake.
+//
+// Shared-memory layout of an R x K (bytes) operand, K-major, no swizzle: the matrix is cut into
+// "core matrices" of 8 rows x 16 bytes (128 contiguous bytes, row r%8 at 16*(r%8)); core
+// matrices are stored chunk-major — all R/8 row groups of K-chunk c, then chunk c+1:
+//   off(r, k) = (k/16) * (R*16) + (r/8) * 128 + (r%8) * 16 + k%16.
+// For the descriptor this is SBO = 128 B (next 8-row group) and LBO = R*16 B (next 16-byte K
+// chunk); one MMA consumes K = 32 bytes = two chunks, so K-step s starts at base + 2*s*R*16.
+#pragma once
+#include <cstdint>
+
+namespace pcb {
+namespace umma {
+
+__host__ __device__ constexpr uint32_t kmajor_off(int r, int k, int R) {
+  return (uint32_t)((k >> 4) * (R * 16) + (r >> 3) * 128 + (r & 7) * 16 + (k & 15));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// shared-memory matrix descriptor (tcgen05 format, version 1, SWIZZLE_NONE)
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr, int R) {
+  const uint64_t lbo = (uint64_t)(R * 16) >> 4, sbo = 128 >> 4;
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((lbo & 0x3FFF) << 16) | ((sbo & 0x3FFF) << 32) | (1ull << 46);
+}
+
+// instruction descriptor, kind::i8: D s32, A/B unsigned 8-bit, both K-major, shape M x N
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, bool accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"((uint32_t)accumulate));
+}
+
+// arrive on the mbarrier once all previously issued MMAs of this thread have completed
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+      "r"(parity)
+      : "memory");
+}
+
+// generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <int COLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // one full warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(COLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int COLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t base) {  // the allocating warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(COLS) : "memory");
+}
+
+// 32 lanes x 16 consecutive 32-bit columns: thread l of the warp gets lane (taddr.lane + l)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+}  // namespace umma
+}  // namespace pcb
