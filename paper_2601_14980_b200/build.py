@@ -38,6 +38,7 @@ SOURCES = [
     "wide.cu",
     "rstream.cu",
     "imad_peak.cu",
+    "rns.cu",
     "host/hbn.cpp",
 ]
 

@@ -16,6 +16,7 @@
 #include "paillier_params.cuh"
 #include "pcb_internal.h"
 #include "wide.h"
+#include "rns.h"
 
 namespace pcb {
 
@@ -234,6 +235,8 @@ struct pcb_ctx {
   std::mutex mu;                 // serialises use of the side streams
   WideMod wide;                  // n^2 constants for the radix-2^r kernels (public-key ops)
   R28Mod rp2, rq2;               // p^2, q^2 for the radix CRT halves (3072-bit keys)
+  RnsModulus rns_p, rns_q;       // p^2, q^2 for the RNS / tensor-core CRT halves (2048-bit keys)
+  bool use_rns = false;
   std::vector<uint32_t> rp2_nR, rq2_nR, rp2_R3, rq2_R3;
   std::vector<uint32_t> wide_r2, wide_nR;
   uint32_t* d_wconst = nullptr;  // [R^2, R, 1, R^C (aggregate)] radix limbs
@@ -454,7 +457,14 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
       if (x->S == 0) return PCB_E_SHAPE;
       switch (x->S) {
         case 32: build_enc<32>(x.get()); build_dec<32>(x.get()); break;
-        case 64: build_enc<64>(x.get()); build_dec<64>(x.get()); break;
+        case 64: {
+          build_enc<64>(x.get());
+          build_dec<64>(x.get());
+          const char* ev = getenv("PCB_RNS");  // RNS core for the CRT halves (opt-in while measured)
+          if (ev && atoi(ev) != 0)
+            x->use_rns = rns_build(p2, x->n, 64, &x->rns_p) && rns_build(q2, x->n, 64, &x->rns_q);
+          break;
+        }
         case 96: {
           build_enc<96>(x.get());
           build_dec<96>(x.get());
@@ -556,6 +566,8 @@ void pcb_ctx_destroy(pcb_ctx* x) {
     if (x->ev_join[k]) cudaEventDestroy(x->ev_join[k]);
   }
   if (x->ev_fork) cudaEventDestroy(x->ev_fork);
+  rns_free(&x->rns_p);
+  rns_free(&x->rns_q);
   delete x;
 }
 
@@ -627,10 +639,24 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
                         stv, count, st);
   const uint32_t* mm = v ? mq : m;
   const uint32_t* mmv = mm;
+  const uint32_t* mm_ = mm;
   const int ml = v ? mql : (int)m_limbs;
   const uint8_t* opp = x->d_sched + x->off_enc_p;
   const uint8_t* opq = x->d_sched + x->off_enc_q;
-  if (!e) {
+  if (!e && x->use_rns) {
+    const auto& k = *reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data());
+    const double mm = 2.0 * 64 * 64 + 64, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm + 2 * mm;
+    e = fork_join(
+        x, st,
+        [&](cudaStream_t s2) {
+          return launch_rns(x->rns_p, kRnsEnc, opp, x->len_enc_p, kTab, r, (int)x->L, mm_, ml, count, yp, s2, alg);
+        },
+        [&](cudaStream_t s2) {
+          return launch_rns(x->rns_q, kRnsEnc, opq, x->len_enc_q, kTab, r, (int)x->L, mm_, ml, count, yq, s2, alg);
+        },
+        count);
+    if (!e) e = launch_garner<64>(k, yp, yq, stv, c, (int)x->L, count, st);
+  } else if (!e) {
     switch (S) {
 #define PCB_CASE(SS)                                                                                                  \
   case SS: {                                                                                                          \
@@ -690,7 +716,23 @@ static pcb_status dec_core(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t
   if (!e) e = launch_dec_prep(c, x->d_n2, (int)x->L, stv, count, st);
   const uint8_t* opp = x->d_sched + x->off_dec_p;
   const uint8_t* opq = x->d_sched + x->off_dec_q;
-  if (!e) {
+  if (!e && x->use_rns) {
+    const auto& k = *reinterpret_cast<const CrtDecConsts<64>*>(x->dec_blob.data());
+    const double mm = 2.0 * 64 * 64 + 64,
+                 alg = ((double)(x->nbits / 2) + (double)((x->nbits / 2 + 3) / 4)) * mm + 2 * mm;
+    e = fork_join(
+        x, st,
+        [&](cudaStream_t s2) {
+          return launch_rns(x->rns_p, kRnsDec, opp, x->len_dec_p, kTab, c, 2 * (int)x->L, nullptr, 0, count, yp, s2,
+                            alg);
+        },
+        [&](cudaStream_t s2) {
+          return launch_rns(x->rns_q, kRnsDec, opq, x->len_dec_q, kTab, c, 2 * (int)x->L, nullptr, 0, count, yq, s2,
+                            alg);
+        },
+        count);
+    if (!e) e = launch_dec_finish<64>(k, yp, yq, stv, m, (int)x->L, count, st);
+  } else if (!e) {
     switch (S) {
 #define PCB_CASE(SS)                                                                                                \
   case SS: {                                                                                                        \

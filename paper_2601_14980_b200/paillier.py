@@ -145,8 +145,8 @@ class Paillier:
 
     def __del__(self):
         ctx = getattr(self, "_ctx", None)
-        if ctx:
-            L.lib().pcb_ctx_destroy(ctx)
+        if ctx and L is not None and L._lib is not None:  # module globals are gone at interpreter exit
+            L._lib.pcb_ctx_destroy(ctx)
             self._ctx = None
 
     # ---- introspection ------------------------------------------------------------------
