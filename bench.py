@@ -285,10 +285,21 @@ def main() -> None:
     ms_per_step = t_ms / args.steps
     value = world * N / (ms_per_step / 1e3)
 
-    # ---- roofline of the dominant kernel (side_kernel), live CUDA-event per-launch times -----
+    # ---- roofline of the dominant kernel, live CUDA-event per-launch times --------------------
     peak = max(lib.pcb_imad_peak(0, 2000, None), lib.pcb_imad_peak(1, 2000, None))
     achieved = alg.value / (ms.value / 1e3)
     side_share = ms.value / t_ms
+    engine = lib.pcb_ctx_engine(ph._ctx)
+    if engine == 1:
+        kname = "pcb::rns_pow_kernel (RNS Montgomery, tcgen05 kind::i8 base extensions)"
+        dtype = "u32 RNS residues (IMAD) + u8 byte planes on tcgen05 kind::i8 (s32 accumulate); FP64 quantizer"
+        rnote = ("canonical CIOS MAC32 of the reference algorithm per Enc/Dec (BASELINE.md 2.1) per second; the RNS "
+                 "core issues ~4x fewer CUDA-core instructions per product and runs the base extensions on the "
+                 "int8 tensor cores, so it can exceed the carry-chain ceiling (9.27 TMAC32/s)")
+    else:
+        kname = "pcb::side_kernel<64>"
+        dtype = "u32-limb integer (IMAD.WIDE.U32); FP64 quantizer"
+        rnote = "canonical CIOS MAC32 per second (BASELINE.md 2.1)"
 
     # ---- e2e through the C ABI with pinned HOST buffers (copies inside the timed region) ------
     hv = torch.from_numpy(vals_np).pin_memory()
@@ -334,7 +345,7 @@ def main() -> None:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32-limb integer (IMAD.WIDE.U32); FP64 quantizer", "data": "synthetic",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {"workload": "cfg2: Paillier-2048 fused Gamma2-quantize+CRT-Enc then CRT-Dec of 2^20 values",
                        "values_per_gpu": N, "key_bits": 2048, "parallelism": f"dp{world} (independent batches)",
                        "l2": "inputs+outputs 0.8 GB/step > 126 MB L2 (no flush needed)",
@@ -342,7 +353,7 @@ def main() -> None:
             "parity_check": ok,
             "enc_dec_mac32_per_s": value * (ENC_MAC + DEC_MAC),
             "roofline": {"bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TMAC32/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "pcb::side_kernel<64>",
+                         "frac": achieved / peak, "traffic": None, "kernel": kname, "note": rnote,
                          "launches": int(nl.value), "kernel_ms": ms.value, "share_of_step": side_share,
                          "peak_source": "pcb_imad_peak (IMAD.WIDE.U32 chains on all SMs), measured in this run"},
             "cpu_baseline": cpu,

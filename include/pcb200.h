@@ -70,6 +70,10 @@ void pcb_ctx_destroy(pcb_ctx* ctx);
 uint32_t pcb_ctx_n_limbs(const pcb_ctx* ctx);   /* L: limb width of plaintexts and r       */
 uint32_t pcb_ctx_n_bits(const pcb_ctx* ctx);    /* bit length of n (plain_bits guard bound) */
 int pcb_ctx_has_private(const pcb_ctx* ctx);
+/* Core that runs the CRT halves of Enc/Dec: 0 = 32-bit carry-chain Montgomery (side_kernel),
+ * 1 = RNS Montgomery with tensor-core base extensions (rns_pow_kernel; 2048-bit keys, default;
+ * PCB_RNS=0 in the environment at context creation selects 0), 2 = radix-2^28 (3072-bit). */
+int pcb_ctx_engine(const pcb_ctx* ctx);
 /* Copies n (L limbs) / n^2 (2L limbs) out of the context. */
 pcb_status pcb_ctx_get_n(const pcb_ctx* ctx, uint32_t* n, uint32_t* n2);
 /* Exponentiation ledger, pcadmm::OpCount (paillier.hpp:84-87): same counting rules as the

@@ -460,8 +460,10 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
         case 64: {
           build_enc<64>(x.get());
           build_dec<64>(x.get());
-          const char* ev = getenv("PCB_RNS");  // RNS core for the CRT halves (opt-in while measured)
-          if (ev && atoi(ev) != 0)
+          // RNS / tensor-core core for the CRT halves (default; PCB_RNS=0 selects the carry-chain
+          // core).  Falls back to the carry core if the bases cannot be built for this key.
+          const char* ev = getenv("PCB_RNS");
+          if (!ev || atoi(ev) != 0)
             x->use_rns = rns_build(p2, x->n, 64, &x->rns_p) && rns_build(q2, x->n, 64, &x->rns_q);
           break;
         }
@@ -574,6 +576,7 @@ void pcb_ctx_destroy(pcb_ctx* x) {
 uint32_t pcb_ctx_n_limbs(const pcb_ctx* x) { return x ? x->L : 0; }
 uint32_t pcb_ctx_n_bits(const pcb_ctx* x) { return x ? x->nbits : 0; }
 int pcb_ctx_has_private(const pcb_ctx* x) { return x && x->has_prv ? 1 : 0; }
+int pcb_ctx_engine(const pcb_ctx* x) { return !x || !x->has_prv ? 0 : (x->use_rns ? 1 : (x->S == 96 ? 2 : 0)); }
 
 pcb_status pcb_ctx_get_n(const pcb_ctx* x, uint32_t* n, uint32_t* n2) {
   if (!x) return PCB_E_SHAPE;
