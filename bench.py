@@ -290,7 +290,25 @@ def main() -> None:
     achieved = alg.value / (ms.value / 1e3)
     side_share = ms.value / t_ms
     engine = lib.pcb_ctx_engine(ph._ctx)
-    if engine == 1:
+    int8_macs = lib.pcb_profile_int8_macs()
+    tensor = None
+    if engine == 3:
+        kname = "pcb::rnsx_kernel<72> (streaming RNS Montgomery, tcgen05 kind::i8 base extensions)"
+        dtype = "u32 RNS residues (IMAD) + u8 byte planes on tcgen05 kind::i8 (s32 accumulate); FP64 quantizer"
+        rnote = ("canonical CIOS MAC32 of the reference algorithm per Enc/Dec (BASELINE.md 2.1) per second; the RNS "
+                 "core replaces the quadratic limb products by O(K) per-prime REDC work on the CUDA cores plus two "
+                 "fixed-matrix base extensions on the int8 tensor cores, so it exceeds the carry-chain ceiling "
+                 "(9.27 TMAC32/s); 'tensor_int8' below is the same kernel against the tensor-core roofline")
+        # int8 dense peak: 2 x the measured bf16 dense peak (same tcgen05 datapath, byte operands)
+        mp = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json"))) \
+            if os.path.exists(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) else {}
+        i8_peak = float(mp.get("bf16_tflops", 2250.0))  # int8 T MAC/s = 2 x (bf16 TFLOP/s / 2)
+        i8_ach = int8_macs / (ms.value / 1e3) / 1e12
+        tensor = {"bound": "tensor", "achieved": i8_ach, "peak": i8_peak, "unit": "T int8 MAC/s", "frac": i8_ach / i8_peak,
+                  "int8_macs": int8_macs,
+                  "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops / 2 (int8 dense = 2x bf16 on tcgen05)"
+                  if mp else "nominal 4.5 POPS dense int8 (MEASURED_PEAKS.json absent)"}
+    elif engine == 1:
         kname = "pcb::rns_pow_kernel (RNS Montgomery, tcgen05 kind::i8 base extensions)"
         dtype = "u32 RNS residues (IMAD) + u8 byte planes on tcgen05 kind::i8 (s32 accumulate); FP64 quantizer"
         rnote = ("canonical CIOS MAC32 of the reference algorithm per Enc/Dec (BASELINE.md 2.1) per second; the RNS "
@@ -355,7 +373,8 @@ def main() -> None:
             "roofline": {"bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TMAC32/s",
                          "frac": achieved / peak, "traffic": None, "kernel": kname, "note": rnote,
                          "launches": int(nl.value), "kernel_ms": ms.value, "share_of_step": side_share,
-                         "peak_source": "pcb_imad_peak (IMAD.WIDE.U32 chains on all SMs), measured in this run"},
+                         "peak_source": "pcb_imad_peak (IMAD.WIDE.U32 chains on all SMs), measured in this run",
+                         "tensor_int8": tensor},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(gpu_launches),

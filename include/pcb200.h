@@ -209,6 +209,8 @@ uint64_t pcb_launch_count(void);
  * synchronises, sums the per-launch event durations and disables recording. */
 void pcb_profile_begin(void);
 pcb_status pcb_profile_end(double* side_ms_total, uint64_t* side_launches, double* side_alg_mac32);
+/* int8 tensor-core MACs issued by the RNS kernels (base extensions) in the last profile window. */
+double pcb_profile_int8_macs(void);
 
 const char* pcb_status_str(pcb_status s);
 

@@ -83,6 +83,7 @@ SIGNATURES = {
     "pcb_launch_count": (C.c_uint64, []),
     "pcb_profile_begin": (None, []),
     "pcb_profile_end": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_double)]),
+    "pcb_profile_int8_macs": (C.c_double, []),
     "pcb_status_str": (C.c_char_p, [C.c_int]),
 }
 

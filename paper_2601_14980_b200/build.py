@@ -39,6 +39,7 @@ SOURCES = [
     "rstream.cu",
     "imad_peak.cu",
     "rns.cu",
+    "rnsx.cu",
     "host/hbn.cpp",
 ]
 

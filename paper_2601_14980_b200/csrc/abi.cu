@@ -17,6 +17,7 @@
 #include "pcb_internal.h"
 #include "wide.h"
 #include "rns.h"
+#include "rnsx.h"
 
 namespace pcb {
 
@@ -30,6 +31,7 @@ namespace {
 struct ProfState {
   std::mutex mu;
   bool on = false;
+  double int8 = 0.0, last_int8 = 0.0;  // tensor-core int8 MACs issued by the RNS kernels
   std::vector<std::pair<ProfMark, double>> marks;
 };
 ProfState& prof() {
@@ -46,6 +48,11 @@ ProfMark prof_start(cudaStream_t st) {
   cudaEventCreate(&m.b);
   cudaEventRecord(m.a, st);
   return m;
+}
+
+void prof_add_int8(double macs) {
+  std::lock_guard<std::mutex> lk(prof().mu);
+  if (prof().on) prof().int8 += macs;
 }
 
 void prof_stop(ProfMark m, cudaStream_t st, double alg) {
@@ -237,6 +244,10 @@ struct pcb_ctx {
   R28Mod rp2, rq2;               // p^2, q^2 for the radix CRT halves (3072-bit keys)
   RnsModulus rns_p, rns_q;       // p^2, q^2 for the RNS / tensor-core CRT halves (2048-bit keys)
   bool use_rns = false;
+  RnsXModulus rx_p, rx_q;        // p^2, q^2 for the streaming RNS core (rnsx.cu)
+  bool use_rnsx = false;
+  RnsXModulus rx_n2;             // n^2 on the streaming RNS core (matvec, public-key ops)
+  bool use_rx_n2 = false;
   std::vector<uint32_t> rp2_nR, rq2_nR, rp2_R3, rq2_R3;
   std::vector<uint32_t> wide_r2, wide_nR;
   uint32_t* d_wconst = nullptr;  // [R^2, R, 1, R^C (aggregate)] radix limbs
@@ -376,12 +387,19 @@ uint64_t pcb_launch_count(void) { return launch_counter().load(); }
 void pcb_profile_begin(void) {
   std::lock_guard<std::mutex> lk(prof().mu);
   prof().marks.clear();
+  prof().int8 = 0.0;
   prof().on = true;
+}
+
+double pcb_profile_int8_macs(void) {
+  std::lock_guard<std::mutex> lk(prof().mu);
+  return prof().last_int8;
 }
 
 pcb_status pcb_profile_end(double* side_ms_total, uint64_t* side_launches, double* side_alg_mac32) {
   std::lock_guard<std::mutex> lk(prof().mu);
   prof().on = false;
+  prof().last_int8 = prof().int8;
   double ms = 0, alg = 0;
   pcb_status e = PCB_OK;
   for (auto& [m, a] : prof().marks) {
@@ -455,6 +473,13 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
       const uint32_t l2 = (uint32_t)((std::max(p2.bit_length(), q2.bit_length()) + 31) / 32);
       x->S = kernel_width(std::max(l2, x->L));
       if (x->S == 0) return PCB_E_SHAPE;
+      {
+        // streaming RNS core for the CRT halves (default; PCB_RNSX=0 selects the older cores)
+        const char* ev = getenv("PCB_RNSX");
+        int K = 0;
+        if ((!ev || atoi(ev) != 0) && (x->S == 64 || x->S == 96) && rnsx_shape((int)(32 * x->S), &K))
+          x->use_rnsx = rnsx_build(p2, x->n, x->S, K, &x->rx_p) && rnsx_build(q2, x->n, x->S, K, &x->rx_q);
+      }
       switch (x->S) {
         case 32: build_enc<32>(x.get()); build_dec<32>(x.get()); break;
         case 64: {
@@ -544,6 +569,12 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
           return PCB_E_CUDA;
       }
     }
+    {  // n^2 on the streaming RNS core (2048-bit keys: 4096-bit n^2, K = 144)
+      const char* ev = getenv("PCB_RNSX_N2");
+      int K = 0;
+      if ((!ev || atoi(ev) != 0) && x->n2.bit_length() > 2048 && rnsx_shape((int)x->n2.bit_length(), &K))
+        x->use_rx_n2 = rnsx_build(x->n2, x->n, 2 * (int)x->L, K, &x->rx_n2);
+    }
     if (cudaMalloc(&x->d_sched, all.size()) != cudaSuccess) return PCB_E_CUDA;
     if (cudaMemcpy(x->d_sched, all.data(), all.size(), cudaMemcpyHostToDevice) != cudaSuccess)
       return PCB_E_CUDA;
@@ -570,13 +601,18 @@ void pcb_ctx_destroy(pcb_ctx* x) {
   if (x->ev_fork) cudaEventDestroy(x->ev_fork);
   rns_free(&x->rns_p);
   rns_free(&x->rns_q);
+  rnsx_free(&x->rx_p);
+  rnsx_free(&x->rx_q);
+  rnsx_free(&x->rx_n2);
   delete x;
 }
 
 uint32_t pcb_ctx_n_limbs(const pcb_ctx* x) { return x ? x->L : 0; }
 uint32_t pcb_ctx_n_bits(const pcb_ctx* x) { return x ? x->nbits : 0; }
 int pcb_ctx_has_private(const pcb_ctx* x) { return x && x->has_prv ? 1 : 0; }
-int pcb_ctx_engine(const pcb_ctx* x) { return !x || !x->has_prv ? 0 : (x->use_rns ? 1 : (x->S == 96 ? 2 : 0)); }
+int pcb_ctx_engine(const pcb_ctx* x) {
+  return !x || !x->has_prv ? 0 : (x->use_rnsx ? 3 : (x->use_rns ? 1 : (x->S == 96 ? 2 : 0)));
+}
 
 pcb_status pcb_ctx_get_n(const pcb_ctx* x, uint32_t* n, uint32_t* n2) {
   if (!x) return PCB_E_SHAPE;
@@ -646,7 +682,20 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
   const int ml = v ? mql : (int)m_limbs;
   const uint8_t* opp = x->d_sched + x->off_enc_p;
   const uint8_t* opq = x->d_sched + x->off_enc_q;
-  if (!e && x->use_rns) {
+  if (!e && x->use_rnsx) {
+    const double mm = 2.0 * S * S + S, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm + 2 * mm;
+    e = fork_join(
+        x, st,
+        [&](cudaStream_t s2) {
+          return launch_rnsx(x->rx_p, kRxEnc, opp, x->len_enc_p, kTab, r, (int)x->L, mm_, ml, count, yp, s2, alg);
+        },
+        [&](cudaStream_t s2) {
+          return launch_rnsx(x->rx_q, kRxEnc, opq, x->len_enc_q, kTab, r, (int)x->L, mm_, ml, count, yq, s2, alg);
+        },
+        count);
+    if (!e && S == 64) e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
+    if (!e && S == 96) e = launch_garner<96>(*reinterpret_cast<const CrtEncConsts<96>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
+  } else if (!e && x->use_rns) {
     const auto& k = *reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data());
     const double mm = 2.0 * 64 * 64 + 64, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm + 2 * mm;
     e = fork_join(
@@ -719,7 +768,21 @@ static pcb_status dec_core(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t
   if (!e) e = launch_dec_prep(c, x->d_n2, (int)x->L, stv, count, st);
   const uint8_t* opp = x->d_sched + x->off_dec_p;
   const uint8_t* opq = x->d_sched + x->off_dec_q;
-  if (!e && x->use_rns) {
+  if (!e && x->use_rnsx) {
+    const double mm = 2.0 * S * S + S,
+                 alg = ((double)(x->nbits / 2) + (double)((x->nbits / 2 + 3) / 4)) * mm + 2 * mm;
+    e = fork_join(
+        x, st,
+        [&](cudaStream_t s2) {
+          return launch_rnsx(x->rx_p, kRxDec, opp, x->len_dec_p, kTab, c, 2 * (int)x->L, nullptr, 0, count, yp, s2, alg);
+        },
+        [&](cudaStream_t s2) {
+          return launch_rnsx(x->rx_q, kRxDec, opq, x->len_dec_q, kTab, c, 2 * (int)x->L, nullptr, 0, count, yq, s2, alg);
+        },
+        count);
+    if (!e && S == 64) e = launch_dec_finish<64>(*reinterpret_cast<const CrtDecConsts<64>*>(x->dec_blob.data()), yp, yq, stv, m, (int)x->L, count, st);
+    if (!e && S == 96) e = launch_dec_finish<96>(*reinterpret_cast<const CrtDecConsts<96>*>(x->dec_blob.data()), yp, yq, stv, m, (int)x->L, count, st);
+  } else if (!e && x->use_rns) {
     const auto& k = *reinterpret_cast<const CrtDecConsts<64>*>(x->dec_blob.data());
     const double mm = 2.0 * 64 * 64 + 64,
                  alg = ((double)(x->nbits / 2) + (double)((x->nbits / 2 + 3) / 4)) * mm + 2 * mm;
@@ -808,6 +871,8 @@ static pcb_status run_pub_enc(pcb_ctx* x, const uint32_t* r, const uint32_t* m, 
   const uint8_t* ops = x->d_sched + x->off_pub;
   const double S2 = 2.0 * x->L, mm = 2 * S2 * S2 + S2;
   const double alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm + mm;  // EXP(2|n|,|n|) + MM(2|n|)
+  if (x->use_rx_n2)  // streaming RNS core at n^2 (rnsx.cu); rows with argument errors stay 0
+    return launch_rnsx(x->rx_n2, kRxEnc, ops, x->len_pub, kTab, r, (int)x->L, m, m_words, count, c, st, alg, stv);
 #define PCB_W(RB, NN, TT)                                                                                           \
   if (w.rb == RB && w.n == NN && w.tpi == TT)                                                                        \
     return launch_side28<RB, NN, TT>(w.mlimb.data(), w.mword.data(), w.mwords, x->wide_r2.data(), x->wide_nR.data(), \
@@ -1140,6 +1205,100 @@ static pcb_status expo_max_bits(const uint64_t* expo_dev, size_t n, cudaStream_t
 //   out[b][i] = alpha[b][i] * prod_j zv[b][j]^expo[b][i][j] mod n^2.
 // A1: window bases per column (squaring chains), A2: the 63-entry tables per (column, window),
 // B: table products per (row, chunk of cc columns), C: alpha_i times the chunk partials.
+// hom_matvec on the streaming RNS core: the same table method (paillier.cpp:441-493) with every
+// table entry and partial product kept as an RNS record (2K residues) in HBM.
+//   A1 (one element per column):  window bases zv^(64^w), 6 squarings per window
+//   A2 (one per (column, window)): entries 0..63 (entry 0 = the Montgomery one)
+//   B  (one per (row, chunk of cc columns)): product of the cc x nwin selected entries
+//   C  (one per row): alpha_i x the chunk partials, converted back to binary mod n^2
+static pcb_status matvec_rnsx(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo_dev, const uint32_t* zv,
+                              size_t nblk, size_t rows_b, size_t cols_b, int nwin, uint32_t* out, cudaStream_t st) {
+  const RnsXModulus& md = x->rx_n2;
+  const size_t rows = nblk * rows_b, cols = nblk * cols_b;
+  const int cc = std::max(1, std::min(16, (kRxMaxSteps - 1) / nwin));
+  const int nch = (int)((cols_b + cc - 1) / cc);
+  const size_t REC = (size_t)rnsx_rec_words(md);
+  const double mm = 2.0 * (2 * x->L) * (2 * x->L) + 2 * x->L;  // canonical MM(2|n|) MAC32
+  RxProg g;
+  g.expo = expo_dev;
+  g.cols = (int)cols_b;
+  g.nwin = nwin;
+  g.cc = cc;
+  g.nch = nch;
+  g.brows = (int)rows_b;
+  g.nparts = nch;
+  pcb_status e = scratch_alloc(cols * (size_t)nwin * 64 * REC * 4, (void**)&g.mtab, st);
+  if (!e) e = scratch_alloc(rows * (size_t)nch * REC * 4, (void**)&g.part, st);
+  auto S = [](uint8_t xs, uint8_t xa, uint8_t ys, uint8_t ya, uint8_t post, uint8_t pa, uint8_t flags = 0) {
+    return XStep{xs, xa, ys, ya, post, pa, flags, 0};
+  };
+  if (!e && getenv("PCB_RNSX_MVDBG") && atoi(getenv("PCB_RNSX_MVDBG")) >= 2) {  // debug: A1 (+A2) then out
+    const int dbg = atoi(getenv("PCB_RNSX_MVDBG"));
+    g.nsteps = 0;
+    g.st[g.nsteps++] = S(kRsConv, 0, kRsCvec, kRxR2N, kRpChain, 0);
+    e = launch_rnsx_prog(md, g, zv, 2 * (int)x->L, cols, nullptr, st, 0);
+    if (dbg == 3) {  // A2 (entries 2.. of every (column, window)); out = entry 2 of element el = zv^2 for el < cols
+      g.nwin = 1;
+      g.nsteps = 0;
+      g.st[g.nsteps++] = S(kRsSelf, 1, kRsSelf, 1, kRpSelf, 2, 1);
+      for (int d = 3; d < 64; d++) g.st[g.nsteps++] = S(kRsKeep, 0, kRsSelf, 1, kRpSelf, (uint8_t)d);
+      if (!e) e = launch_rnsx_prog(md, g, nullptr, 0, cols, nullptr, st, 0);
+    }
+    g.nsteps = 0;
+    g.st[g.nsteps++] = S(kRsSelf, dbg == 3 ? 2 : 1, kRsCvec, kRxOne, kRpOut, 0);
+    if (!e) e = launch_rnsx_prog(md, g, nullptr, 0, rows, out, st, 0);
+    scratch_free(g.mtab, st);
+    scratch_free(g.part, st);
+    return e;
+  }
+  if (!e && getenv("PCB_RNSX_MVDBG")) {  // debug: out = alpha through conv -> x R2N -> x 1 -> out
+    g.nsteps = 0;
+    g.st[g.nsteps++] = S(kRsConv, 0, kRsCvec, kRxR2N, kRpNone, 0);
+    g.st[g.nsteps++] = S(kRsKeep, 0, kRsCvec, kRxOne, kRpOut, 0);
+    e = launch_rnsx_prog(md, g, alpha, 2 * (int)x->L, rows, out, st, 0);
+    scratch_free(g.mtab, st);
+    scratch_free(g.part, st);
+    return e;
+  }
+  if (!e) {  // A1
+    g.nsteps = 0;
+    g.st[g.nsteps++] = S(kRsConv, 0, kRsCvec, kRxR2N, kRpChain, 0);
+    for (int w = 1; w < nwin; w++)
+      for (int q = 1; q <= kMatWin; q++) g.st[g.nsteps++] = S(kRsKeep, 0, kRsSq, 0, q == kMatWin ? kRpChain : kRpNone, (uint8_t)w);
+    e = launch_rnsx_prog(md, g, zv, 2 * (int)x->L, cols, nullptr, st, mm * g.nsteps);
+  }
+  if (!e) {  // A2
+    g.nsteps = 0;
+    g.st[g.nsteps++] = S(kRsSelf, 1, kRsSelf, 1, kRpSelf, 2, 1);
+    for (int d = 3; d < 64; d++) g.st[g.nsteps++] = S(kRsKeep, 0, kRsSelf, 1, kRpSelf, (uint8_t)d);
+    e = launch_rnsx_prog(md, g, nullptr, 0, cols * nwin, nullptr, st, mm * g.nsteps);
+  }
+  if (!e) {  // B
+    std::vector<uint8_t> ids;
+    for (int j = 0; j < cc; j++)
+      for (int w = 0; w < nwin; w++) ids.push_back((uint8_t)(j * 16 + w));
+    g.nsteps = 0;
+    if (ids.size() == 1) {
+      g.st[g.nsteps++] = S(kRsMat, ids[0], kRsCvec, kRxOneM, kRpRec, 0);
+    } else {
+      g.st[g.nsteps++] = S(kRsMat, ids[0], kRsMat, ids[1], kRpNone, 0);
+      for (size_t q = 2; q < ids.size(); q++) g.st[g.nsteps++] = S(kRsKeep, 0, kRsMat, ids[q], kRpNone, 0);
+      g.st[g.nsteps - 1].post = kRpRec;
+    }
+    e = launch_rnsx_prog(md, g, nullptr, 0, rows * nch, nullptr, st, mm * g.nsteps);
+  }
+  if (!e) {  // C
+    g.nsteps = 0;
+    g.st[g.nsteps++] = S(kRsConv, 0, kRsCvec, kRxR2N, kRpNone, 0);
+    for (int c = 0; c < nch; c++) g.st[g.nsteps++] = S(kRsKeep, 0, kRsPart, (uint8_t)c, kRpNone, 0);
+    g.st[g.nsteps++] = S(kRsKeep, 0, kRsCvec, kRxOne, kRpOut, 0);
+    e = launch_rnsx_prog(md, g, alpha, 2 * (int)x->L, rows, out, st, mm * g.nsteps);
+  }
+  scratch_free(g.mtab, st);
+  scratch_free(g.part, st);
+  return e;
+}
+
 static pcb_status matvec_core(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo_dev, const uint32_t* zv,
                               size_t nblk, size_t rows_b, size_t cols_b, uint32_t* out, cudaStream_t st) {
   const size_t wb = 2 * x->L * 4;
@@ -1149,6 +1308,8 @@ static pcb_status matvec_core(pcb_ctx* x, const uint32_t* alpha, const uint64_t*
   int maxbits = 0;
   if (auto e = expo_max_bits(expo_dev, rows * cols_b, st, &maxbits)) return e;
   const int nwin = maxbits ? (maxbits + kMatWin - 1) / kMatWin : 1;
+  if (x->use_rx_n2 && nwin <= 15 && nblk * cols_b <= (1u << 20))
+    return matvec_rnsx(x, alpha, expo_dev, zv, nblk, rows_b, cols_b, nwin, out, st);
   const int cc = std::max(1, std::min(16, (kWideMaxSteps - 1) / nwin));
   const int nch = (int)((cols_b + cc - 1) / cc);
   const int N = x->wide.n;

@@ -52,6 +52,7 @@ struct ProfMark {
 bool prof_enabled();
 ProfMark prof_start(cudaStream_t st);
 void prof_stop(ProfMark m, cudaStream_t st, double alg_mac32);
+void prof_add_int8(double macs);  // int8 tensor-core MACs issued (RNS base extensions)
 
 // Stream-ordered device scratch (cudaMallocAsync on the caller's stream; freed on the same
 // stream once the kernels using it are enqueued).

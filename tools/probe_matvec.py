@@ -19,6 +19,10 @@ r = ph.sample_r_batch(P.Rng(3), 2 * c_)
 alpha = ph.encrypt_batch(m, r[:c_], True)
 zc = ph.encrypt_batch(m, r[c_:], True)
 torch.cuda.synchronize()
+import time
 out = edge.hom_matvec_batch(alpha, q_b, zc, 6)
 torch.cuda.synchronize()
-print("done", out.shape)
+t0 = time.perf_counter()
+out = edge.hom_matvec_batch(alpha, q_b, zc, 6)
+torch.cuda.synchronize()
+print("matvec", c_, "x", c_, "s:", round(time.perf_counter() - t0, 4), out.shape)
