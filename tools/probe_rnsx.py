@@ -27,7 +27,7 @@ def key(bits):
 bits = int(sys.argv[1])
 sizes = [int(a) for a in sys.argv[2:]] or [1024]
 kp = key(bits)
-os.environ.pop("PCB_RNSX", None)
+os.environ["PCB_RNSX"] = "0"  # baseline: the previous default core for this key size
 base = P.Paillier(kp)
 os.environ["PCB_RNSX"] = "1"
 rx = P.Paillier(kp)
