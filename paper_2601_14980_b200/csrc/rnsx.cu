@@ -48,11 +48,11 @@ namespace {
 // 4 PTc columns the primes sit in quads of <= 4 primes x 4 bytes ([quad][byte][prime]), so one
 // tcgen05.ld x16 returns four complete primes.
 // slices per stream stage: bigger bulk copies where the ring has room (8+ stages either way)
-__host__ __device__ constexpr int sps_for(int K) { return K <= 80 ? 2 : 1; }
+__host__ __device__ constexpr int sps_for(int) { return 1; }  // one <= 8 KB slice per stage
 
-template <int K_>
+template <int K_, int NT_ = 1>
 struct Cfg {
-  static constexpr int K = K_, G = 4;
+  static constexpr int K = K_, G = 4, NT = NT_;  // NT: tiles in flight per CTA (1 or 2)
   static constexpr int CP = 64, TPC = CP / G;  // primes per full chunk (256 TMEM columns), per thread
   static constexpr int NC = (K + CP - 1) / CP, PL = K - CP * (NC - 1), PTL = PL / 4;
   static constexpr int RPT = TPC * (NC - 1) + PTL;  // residues per thread per base
@@ -65,8 +65,9 @@ struct Cfg {
   static constexpr int SLOT = 8192 * SPS;          // ring slot: SPS slices of <= 256 x 32 bytes
   static constexpr int NB = 2, BUFC = 256, TMC = 512;  // TMEM ring: 2 buffers of 256 columns
   static constexpr int TILE = 128, NCW = 16, NCT = 32 * NCW, NTHR = NCT + 128;  // + role warpgroup
-  static constexpr uint32_t OFF_A1 = 0, OFF_A2 = OFF_A1 + TILE * K1, OFF_CONS = OFF_A2 + TILE * K2;
-  static constexpr uint32_t OFF_S = OFF_CONS + K * 48, OFF_SLT = OFF_S + G * TILE * 8;
+  static constexpr uint32_t ABLK = TILE * (K1 + K2);  // A1 + A2 of one tile
+  static constexpr uint32_t OFF_A1 = 0, OFF_A2 = OFF_A1 + TILE * K1, OFF_CONS = NT * ABLK;
+  static constexpr uint32_t OFF_S = OFF_CONS + K * 48, OFF_SLT = OFF_S + NT * G * TILE * 8;
   static constexpr uint32_t OFF_BAR = OFF_SLT + NSLICE * 16 + NSTG * 8;
   static constexpr uint32_t OFF_RING = (OFF_BAR + 512 + 1023) & ~1023u;
   static constexpr int NSTAGE_FIT = (int)((227u * 1024u - OFF_RING) / SLOT);
@@ -76,7 +77,8 @@ struct Cfg {
   __host__ __device__ static constexpr int ncol(int c) { return 16 * ptc(c); }
   static_assert(PL % 8 == 0 && (PTL == 2 || PTL % 4 == 0), "ragged chunk: 8 or a multiple of 16 primes");
   static_assert(NSTAGE >= 4, "stream ring");
-  static_assert((2 * NSTAGE + 2 * NB + 2) * 8 + 4 <= 512, "barriers");
+  static_assert((2 * NSTAGE + 2 * NB + 2 * NT) * 8 + 4 <= 512, "barriers");
+  static_assert(NT == 1 || NT == 2, "tiles in flight");
 };
 
 struct XArgs {
@@ -188,15 +190,15 @@ __device__ __forceinline__ void d_quad(Thr<C>& T, int ptc, int j, bool first, bo
   }
 }
 
-// One RNS Montgomery product for the tile: X <- MM(X, Y), Y = X (sq) or the 4-word vectors at
-// ybase + v * yvs (v < NQ: base-B quad v; v >= NQ: base-B' quad v - NQ).
+// One RNS Montgomery product for a tile in three phases (so two tiles can be interleaved):
+//   rx_s1: t = x y (both bases), xi = t C1 -> A1, t' parked in XQ; hands A1 to the MMA warp
+//   rx_e1: GEMM-1 epilogue: qh', r' (new B'), xi' -> A2, beta; hands A2 to the MMA warp
+//   rx_e2: GEMM-2 epilogue: new B residues
+// Y = X (sq) or the 4-word vectors at ybase + v * yvs (v < NQ: base-B quad v; v >= NQ: B').
 template <class C>
-__device__ __forceinline__ void rx_mm(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::RPT], bool sq, const uint32_t* ybase,
-                                      int yvs, Thr<C>& T) {
+__device__ __forceinline__ void rx_s1(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::RPT], bool sq, const uint32_t* ybase,
+                                      int yvs, Thr<C>& T, uint8_t* A1, uint64_t* a1) {
   constexpr int NC = C::NC;
-  uint8_t* A1 = T.sm + C::OFF_A1;
-  uint8_t* A2 = T.sm + C::OFF_A2;
-  double* sS = reinterpret_cast<double*>(T.sm + C::OFF_S);
   // ---- 1. t = x y: xi = t C1 (B) -> A1; t' parked in XQ ------------------------------------------
 #pragma unroll
   for (int c = 0; c < NC; c++) {
@@ -231,7 +233,12 @@ __device__ __forceinline__ void rx_mm(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
   }
   umma::fence_async_smem();
   __syncwarp();
-  if (T.lane == 0) umma::mbar_arrive(T.a1);
+  if (T.lane == 0) umma::mbar_arrive(a1);
+}
+
+template <class C>
+__device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t* A2, double* sS, uint64_t* a2) {
+  constexpr int NC = C::NC;
   // ---- 2. GEMM-1 epilogue per chunk: qh', r' (new B'), xi' -> A2, partial beta ------------------
   double sp = 0.0;
 #pragma unroll
@@ -269,7 +276,12 @@ __device__ __forceinline__ void rx_mm(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
     umma::fence_async_smem();
   }
   __syncwarp();
-  if (T.lane == 0) umma::mbar_arrive(T.a2);
+  if (T.lane == 0) umma::mbar_arrive(a2);
+}
+
+template <class C>
+__device__ __forceinline__ void rx_e2(uint32_t (&XB)[C::RPT], Thr<C>& T) {
+  constexpr int NC = C::NC;
   // ---- 3. GEMM-2 epilogue per chunk: r (new B residues) -------------------------------------------
 #pragma unroll
   for (int c = 0; c < NC; c++) {
@@ -289,6 +301,14 @@ __device__ __forceinline__ void rx_mm(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
       }
     }
   }
+}
+
+template <class C>
+__device__ __forceinline__ void rx_mm(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::RPT], bool sq, const uint32_t* ybase,
+                                      int yvs, Thr<C>& T) {
+  rx_s1<C>(XB, XQ, sq, ybase, yvs, T, T.sm + C::OFF_A1, T.a1);
+  rx_e1<C>(XQ, T, T.sm + C::OFF_A2, reinterpret_cast<double*>(T.sm + C::OFF_S), T.a2);
+  rx_e2<C>(XB, T);
 }
 
 template <class C>
@@ -404,6 +424,126 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int nste
     }
     return;
   }
+  // ---- exponentiation programs (Enc / Dec / Pow): per-step operand selection and epilogue ------
+  // `tt` selects the per-thread window table of tile slot tt (two tiles in flight when C::NT == 2)
+  auto tabp = [&](int ent, int tt) { return tab_ptr(ent * C::NT + tt); };
+  auto prep = [&](int s, uint32_t (&XB)[RPT], uint32_t (&XQ)[RPT], int tt, int el, bool live, bool& sq,
+                  const uint32_t*& yb, int& yvs) {
+    sq = false;
+    yb = nullptr;
+    yvs = 4;
+    if (s < npre) {
+      const bool first = npre == 2 && s == 0;
+      const uint32_t* src = &zero;
+      int nw = 1;
+      int cst = kRxR2N;
+      if (P.mode == kRxEnc && first) {  // m n
+        if (live) { src = P.m + (size_t)el * P.m_words; nw = P.m_words; }
+        cst = kRxNM;
+      } else if (P.mode == kRxDec && first) {  // c_hi 2^(32 S) M
+        if (live) { src = P.x + (size_t)el * P.x_words + P.S; nw = P.x_words - P.S; }
+        cst = kRxCR2N;
+      } else {  // r M / c_lo M / x M
+        if (live) { src = P.x + (size_t)el * P.x_words; nw = P.mode == kRxDec ? P.S : P.x_words; }
+      }
+      conv_in<C>(XB, XQ, src, nw, T);
+      yb = cv_ptr(cst);
+    } else if (s == s_x2) {
+      sq = true;
+    } else if (s < s_main) {
+      yb = tabp(park_x2, tt);
+      yvs = tab_vs;
+    } else if (s < s_fin) {
+      const uint8_t op = P.ops[s - s_main + 1];
+      if (op == kOpSquare) {
+        sq = true;
+      } else {
+        yb = tabp(op, tt);
+        yvs = tab_vs;
+      }
+    } else if (P.mode == kRxEnc) {
+      yb = tabp(park, tt);
+      yvs = tab_vs;
+    } else {
+      yb = cv_ptr(kRxOne);
+    }
+  };
+  auto post = [&](int s, uint32_t (&XB)[RPT], uint32_t (&XQ)[RPT], int tt, int el, bool live) {
+    if (s < npre) {
+      const bool first = npre == 2 && s == 0;
+      if (first) {
+        if (P.mode == kRxEnc) vec_op(cv_ptr(kRxOne), 4, XB, XQ, 1);  // 1 + m n (plain)
+        vec_op(tabp(park, tt), tab_vs, XB, XQ, 2);
+      } else {
+        if (P.mode == kRxDec) vec_op(tabp(park, tt), tab_vs, XB, XQ, 1);  // c M = c_lo M + c_hi 2^(32S) M
+        vec_op(tabp(0, tt), tab_vs, XB, XQ, 2);
+      }
+    } else if (s == s_x2) {
+      vec_op(tabp(park_x2, tt), tab_vs, XB, XQ, 2);
+      vec_op(tabp(0, tt), tab_vs, XB, XQ, 0);
+    } else if (s < s_main) {
+      vec_op(tabp(s - s_tab + 1, tt), tab_vs, XB, XQ, 2);
+      if (s == s_main - 1) vec_op(tabp(P.ops[0], tt), tab_vs, XB, XQ, 0);
+    } else if (s == s_fin) {
+      if (live) {
+        uint32_t* o = P.out + (size_t)el * C::K;
+#pragma unroll
+        for (int c = 0; c < C::NC; c++) {
+          const int ptc = C::ptc(c);
+#pragma unroll
+          for (int j = 0; j < (ptc + 3) / 4; j++) {
+            const int QT = ptc < 4 ? ptc : 4, w0 = C::TPC * c + 4 * j;
+            uint32_t* d = o + C::CP * c + T.g * ptc + 4 * j;
+            if (QT == 4) stq<4>(d, &XQ[w0]); else stq<2>(d, &XQ[w0]);
+          }
+        }
+      }
+    }
+    if (P.ntab == 1 && s == s_x2) vec_op(tabp(P.ops[0], tt), tab_vs, XB, XQ, 0);
+  };
+  if constexpr (C::NT == 2) {
+    // Two tiles in flight: compute order A.s1, B.s1, A.e1, B.e1, then (next step) A.e2 + A.s1, ...
+    // while the tensor core runs A.G1, B.G1, A.G2, B.G2: each GEMM overlaps the other tile's
+    // CUDA-core phase.
+    uint8_t* A1a = T.sm + C::OFF_A1;
+    uint8_t* A2a = T.sm + C::OFF_A2;
+    uint8_t* A1b = A1a + C::ABLK;
+    uint8_t* A2b = A2a + C::ABLK;
+    double* sSa = reinterpret_cast<double*>(T.sm + C::OFF_S);
+    double* sSb = sSa + C::G * C::TILE;
+    const int npairs = (ntiles + 1) / 2;
+#pragma unroll 1
+    for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+      const int ela = (2 * pr) * C::TILE + T.e, elb = (2 * pr + 1) * C::TILE + T.e;
+      const bool la = ela < P.count, lb = elb < P.count;
+      uint32_t XBa[RPT], XQa[RPT], XBb[RPT], XQb[RPT];
+      bool sq;
+      const uint32_t* yb;
+      int yvs;
+#pragma unroll 1
+      for (int s = 0; s < nsteps; s++) {
+        if (s > 0) {
+          rx_e2<C>(XBa, T);
+          post(s - 1, XBa, XQa, 0, ela, la);
+        }
+        prep(s, XBa, XQa, 0, ela, la, sq, yb, yvs);
+        rx_s1<C>(XBa, XQa, sq, yb, yvs, T, A1a, T.a1);
+        if (s > 0) {
+          rx_e2<C>(XBb, T);
+          post(s - 1, XBb, XQb, 1, elb, lb);
+        }
+        prep(s, XBb, XQb, 1, elb, lb, sq, yb, yvs);
+        rx_s1<C>(XBb, XQb, sq, yb, yvs, T, A1b, T.a1 + 2);
+        rx_e1<C>(XQa, T, A2a, sSa, T.a2);
+        rx_e1<C>(XQb, T, A2b, sSb, T.a2 + 2);
+      }
+      rx_e2<C>(XBa, T);
+      post(nsteps - 1, XBa, XQa, 0, ela, la);
+      rx_e2<C>(XBb, T);
+      post(nsteps - 1, XBb, XQb, 1, elb, lb);
+    }
+    return;
+  }
 #pragma unroll 1
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int el = tile * C::TILE + T.e;
@@ -411,76 +551,12 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int nste
     uint32_t XB[RPT], XQ[RPT];
 #pragma unroll 1
     for (int s = 0; s < nsteps; s++) {
-      bool sq = false;
-      const uint32_t* yb = nullptr;
-      int yvs = 4;
-      if (s < npre) {
-        const bool first = npre == 2 && s == 0;
-        const uint32_t* src = &zero;
-        int nw = 1;
-        int cst = kRxR2N;
-        if (P.mode == kRxEnc && first) {  // m n
-          if (live) { src = P.m + (size_t)el * P.m_words; nw = P.m_words; }
-          cst = kRxNM;
-        } else if (P.mode == kRxDec && first) {  // c_hi 2^(32 S) M
-          if (live) { src = P.x + (size_t)el * P.x_words + P.S; nw = P.x_words - P.S; }
-          cst = kRxCR2N;
-        } else {  // r M / c_lo M / x M
-          if (live) { src = P.x + (size_t)el * P.x_words; nw = P.mode == kRxDec ? P.S : P.x_words; }
-        }
-        conv_in<C>(XB, XQ, src, nw, T);
-        yb = cv_ptr(cst);
-      } else if (s == s_x2) {
-        sq = true;
-      } else if (s < s_main) {
-        yb = tab_ptr(park_x2);
-        yvs = tab_vs;
-      } else if (s < s_fin) {
-        const uint8_t op = P.ops[s - s_main + 1];
-        if (op == kOpSquare) {
-          sq = true;
-        } else {
-          yb = tab_ptr(op);
-          yvs = tab_vs;
-        }
-      } else if (P.mode == kRxEnc) {
-        yb = tab_ptr(park);
-        yvs = tab_vs;
-      } else {
-        yb = cv_ptr(kRxOne);
-      }
+      bool sq;
+      const uint32_t* yb;
+      int yvs;
+      prep(s, XB, XQ, 0, el, live, sq, yb, yvs);
       rx_mm<C>(XB, XQ, sq, yb, yvs, T);
-      if (s < npre) {
-        const bool first = npre == 2 && s == 0;
-        if (first) {
-          if (P.mode == kRxEnc) vec_op(cv_ptr(kRxOne), 4, XB, XQ, 1);  // 1 + m n (plain)
-          vec_op(tab_ptr(park), tab_vs, XB, XQ, 2);
-        } else {
-          if (P.mode == kRxDec) vec_op(tab_ptr(park), tab_vs, XB, XQ, 1);  // c M = c_lo M + c_hi 2^(32S) M
-          vec_op(tab_ptr(0), tab_vs, XB, XQ, 2);
-        }
-      } else if (s == s_x2) {
-        vec_op(tab_ptr(park_x2), tab_vs, XB, XQ, 2);
-        vec_op(tab_ptr(0), tab_vs, XB, XQ, 0);
-      } else if (s < s_main) {
-        vec_op(tab_ptr(s - s_tab + 1), tab_vs, XB, XQ, 2);
-        if (s == s_main - 1) vec_op(tab_ptr(P.ops[0]), tab_vs, XB, XQ, 0);
-      } else if (s == s_fin) {
-        if (live) {
-          uint32_t* o = P.out + (size_t)el * C::K;
-#pragma unroll
-          for (int c = 0; c < C::NC; c++) {
-            const int ptc = C::ptc(c);
-#pragma unroll
-            for (int j = 0; j < (ptc + 3) / 4; j++) {
-              const int QT = ptc < 4 ? ptc : 4, w0 = C::TPC * c + 4 * j;
-              uint32_t* d = o + C::CP * c + T.g * ptc + 4 * j;
-              if (QT == 4) stq<4>(d, &XQ[w0]); else stq<2>(d, &XQ[w0]);
-            }
-          }
-        }
-      }
-      if (P.ntab == 1 && s == s_x2) vec_op(tab_ptr(P.ops[0]), tab_vs, XB, XQ, 0);
+      post(s, XB, XQ, 0, el, live);
     }
   }
 }
@@ -523,19 +599,27 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
   const uint2* stg = reinterpret_cast<const uint2*>(sm + C::OFF_SLT + C::NSLICE * 16);
   // every SM streams the same matrices: spread the reads over kRxReplicas copies (L2 slices)
   const uint8_t* wimg = wimg0 + (size_t)(blockIdx.x % kRxReplicas) * wstride;
-  const uint32_t total = nprod * (uint32_t)C::NSTG;
-  uint32_t pslot = 0, pph = 0, pi = 0;
+  static_assert(C::SPS == 1, "one slice per stage: stages never straddle a GEMM");
+  constexpr int NG1 = C::NC * C::KS1;
+  uint32_t issued = 0, pslot = 0, pph = 0;
 #pragma unroll 1
-  for (uint32_t issued = 0; issued < total; issued++) {
-    if (issued >= (uint32_t)C::NSTAGE) umma::mbar_wait(empty + pslot, pph ^ 1);
-    const uint2 d = stg[pi];
-    if (lane == 0) {
-      umma::mbar_arrive_expect_tx(full + pslot, d.y);
-      umma::bulk_g2s(ring + pslot * C::SLOT, wimg + (size_t)d.x * 16, d.y, full + pslot);
+  for (uint32_t pr = 0; pr < nprod; pr++) {
+#pragma unroll 1
+    for (int seg = 0; seg < 2 * C::NT; seg++) {  // G1 per tile, then G2 per tile (MMA issue order)
+      const int gm = C::NT == 2 ? seg >> 1 : seg;
+      const int i0 = gm ? NG1 : 0, i1 = gm ? C::NSLICE : NG1;
+#pragma unroll 1
+      for (int i = i0; i < i1; i++, issued++) {
+        if (issued >= (uint32_t)C::NSTAGE) umma::mbar_wait(empty + pslot, pph ^ 1);
+        const uint2 d = stg[i];
+        if (lane == 0) {
+          umma::mbar_arrive_expect_tx(full + pslot, d.y);
+          umma::bulk_g2s(ring + pslot * C::SLOT, wimg + (size_t)d.x * 16, d.y, full + pslot);
+        }
+        __syncwarp();
+        if (++pslot == (uint32_t)C::NSTAGE) { pslot = 0; pph ^= 1; }
+      }
     }
-    __syncwarp();
-    if (++pi == (uint32_t)C::NSTG) pi = 0;
-    if (++pslot == (uint32_t)C::NSTAGE) { pslot = 0; pph ^= 1; }
   }
 }
 
@@ -556,16 +640,23 @@ __device__ __noinline__ void mma_role(uint8_t* sm, uint32_t tm, uint64_t* bars, 
   const uint32_t a2lo = (uint32_t)umma::desc_kmajor(umma::smem_u32(sm + C::OFF_A2), C::TILE);
   const uint32_t ring16 = umma::smem_u32(sm + C::OFF_RING) >> 4;
   uint4 e = slt[0];
+  constexpr int NG1 = C::NC * C::KS1;
+  constexpr uint32_t ABLK16 = C::ABLK / 16;
 #pragma unroll 1
   for (uint32_t pr = 0; pr < nprod; pr++) {
 #pragma unroll 1
-    for (int i = 0; i < C::NSLICE; i++) {
+    for (int seg = 0; seg < 2 * C::NT; seg++) {  // G1 per tile, then G2 per tile
+    const int gm = C::NT == 2 ? seg >> 1 : seg, tt = C::NT == 2 ? (seg & 1) : 0;
+    const int i0 = gm ? NG1 : 0, i1 = gm ? C::NSLICE : NG1;
+    e = slt[i0];
+#pragma unroll 1
+    for (int i = i0; i < i1; i++) {
       const uint4 cur = e;
-      e = slt[i + 1 < C::NSLICE ? i + 1 : 0];  // prefetch the next entry
+      e = slt[i + 1 < i1 ? i + 1 : i0];  // prefetch the next entry
       const uint32_t f = cur.w;
       if (f & (kFGemm | kFChunk)) {
         if (kWaitCompute && (f & kFGemm)) {
-          umma::mbar_wait(f & kFG2 ? a2 : a1, pr & 1);
+          umma::mbar_wait((f & kFG2 ? a2 : a1) + 2 * tt, pr & 1);
           umma::tmem_fence_after();
         }
         if (kWaitCompute && (f & kFChunk) && dcnt >= (uint32_t)C::NB) {
@@ -575,7 +666,7 @@ __device__ __noinline__ void mma_role(uint8_t* sm, uint32_t tm, uint64_t* bars, 
       }
       if (kRing && (f & kFStage)) umma::mbar_wait(full + cslot, cph);
       if (kMma) {
-        const uint64_t ad = ((uint64_t)hi << 32) | (uint64_t)((f & kFG2 ? a2lo : a1lo) + cur.x);
+        const uint64_t ad = ((uint64_t)hi << 32) | (uint64_t)((f & kFG2 ? a2lo : a1lo) + tt * ABLK16 + cur.x);
         const uint64_t bd =
             ((uint64_t)hi << 32) | (uint64_t)(((ring16 + cslot * (C::SLOT / 16) + (cur.y & 0xFFFFu)) & 0x3FFFu) | (cur.y & 0xFFFF0000u));
         mma_elect(tm + dbi * C::BUFC, ad, bd, cur.z, f & kFAcc);
@@ -597,6 +688,7 @@ __device__ __noinline__ void mma_role(uint8_t* sm, uint32_t tm, uint64_t* bars, 
         }
       }
     }
+    }
   }
   if (!kWaitCompute && nprod) umma::mbar_wait(dfull + (dbi + C::NB - 1) % C::NB, (dbi == 0) ? dph ^ 1 : dph);
 }
@@ -606,8 +698,8 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
   extern __shared__ __align__(1024) uint8_t sm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
-  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 2 * C::NSTAGE + 2 * C::NB + 2);
-  for (uint32_t o = tid * 16; o < (uint32_t)(C::TILE * (C::K1 + C::K2)); o += C::NTHR * 16)
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 2 * C::NSTAGE + 2 * C::NB + 2 * C::NT);
+  for (uint32_t o = tid * 16; o < (uint32_t)(C::NT * C::ABLK); o += C::NTHR * 16)
     *reinterpret_cast<uint4*>(sm + C::OFF_A1 + o) = make_uint4(0, 0, 0, 0);
   for (int o = tid; o < C::K * 3; o += C::NTHR) reinterpret_cast<uint4*>(sm + C::OFF_CONS)[o] = P.cons[o];
   for (int o = tid; o < 4 * C::NSLICE + 2 * C::NSTG; o += C::NTHR)
@@ -615,7 +707,7 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
   if (warp == C::NCW) umma::tmem_alloc<C::TMC>(tbase);
   if (tid == 0) {
     for (int i = 0; i < 2 * C::NSTAGE + C::NB; i++) umma::mbar_init(bars + i, 1);
-    for (int i = 0; i < C::NB + 2; i++) umma::mbar_init(bars + 2 * C::NSTAGE + C::NB + i, C::NCW);
+    for (int i = 0; i < C::NB + 2 * C::NT; i++) umma::mbar_init(bars + 2 * C::NSTAGE + C::NB + i, C::NCW);
   }
   umma::fence_async_smem();
   umma::tmem_fence_before();
@@ -628,9 +720,10 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
   const int nsteps = P.mode == kRxProg ? P.prog.nsteps : s_fin + 1;
   const int ntiles = (P.count + C::TILE - 1) / C::TILE;
   if (warp >= C::NCW) {
-    // role warpgroup hands registers to the compute warps (CTA pool: 4 x 32 x 32 = 16 x 8 x 32)
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
-    const int mine = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    // role warpgroup hands registers to the compute warps (CTA pool: 4 x 64 x 32 = 16 x 16 x 32)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
+    const int units = P.mode == kRxProg ? ntiles : (ntiles + C::NT - 1) / C::NT;  // tiles or tile pairs
+    const int mine = blockIdx.x < units ? (units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const uint32_t np = (uint32_t)(mine * nsteps);
     if (warp == C::NCW) {
       if (P.dbg == 0) mma_role<C, 0>(sm, tm, bars, np);
@@ -641,7 +734,7 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     if (warp == C::NCW + 1 && P.dbg != 2 && P.dbg != 4) producer_role<C>(P.wimg, P.wimg_stride, sm, bars, np, lane);
     __syncwarp();
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
     Thr<C> T;
     T.sm = sm;
     const int qd = warp & 3;
@@ -792,11 +885,12 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int ntiles = (int)((count + C::TILE - 1) / C::TILE);
-  const int blocks = ntiles < nsm ? ntiles : nsm;
+  const int units = mode == kRxProg ? ntiles : (ntiles + C::NT - 1) / C::NT;
+  const int blocks = units < nsm ? units : nsm;
   const size_t nthr = (size_t)blocks * C::NCT;
   pcb_status e = PCB_OK;
   P.tab = nullptr;
-  if (mode != kRxProg) e = scratch_alloc(nthr * (size_t)(ntab + 2) * C::NV * 4 * 4, (void**)&P.tab, st);
+  if (mode != kRxProg) e = scratch_alloc(nthr * (size_t)(ntab + 2) * C::NT * C::NV * 4 * 4, (void**)&P.tab, st);
   uint32_t* res = nullptr;
   if (!e && y) e = scratch_alloc(count * C::K * 4, (void**)&res, st);
   P.out = res;
@@ -810,7 +904,7 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
       double mps = 0;  // int8 MACs per tile-product: every slice is an M = 128 x N = ncol x K = 32 MMA
       for (int c = 0; c < C::NC; c++) mps += (double)C::TILE * C::ncol(c) * 32 * (C::KS1 + C::KS2);
       const int nsteps = mode == kRxProg ? prog->nsteps : (mode == kRxPow ? 1 : 2) + ntab + nops;
-      prof_add_int8(mps * nsteps * (double)ntiles);
+      prof_add_int8(mps * nsteps * (double)(units * C::NT));
     }
     const cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) fprintf(stderr, "rnsx_kernel<K=%d>: %s\n", C::K, cudaGetErrorString(ce));
@@ -1143,6 +1237,15 @@ pcb_status launch_rnsx(const RnsXModulus& md, int mode, const uint8_t* ops, int 
   if (!md.ok) return PCB_E_UNSUPPORTED;
 #define PCB_RX(KK)                                                                                                 \
   if (md.K == KK) return launch_cfg<Cfg<KK>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
+  if (md.K == 72) {  // two tiles in flight per CTA (the K = 72 register budget allows it)
+    const char* ppv = getenv("PCB_RNSX_PP");
+    const bool pp = !ppv || atoi(ppv) != 0;  // default on; PCB_RNSX_PP=0 runs one tile per CTA
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (pp && count >= (size_t)nsm * 2 * 128)  // pairs only pay once every SM has two tiles
+      return launch_cfg<Cfg<72, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
+  }
   PCB_RX(72)
   PCB_RX(112)
   PCB_RX(144)
