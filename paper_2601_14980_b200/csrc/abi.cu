@@ -543,6 +543,7 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
       if (b2 + 4 <= 28 * 38) { rb = 28; nl = 38; tpi = 1; }
       else if (b2 + 4 <= 28 * 76) { rb = 28; nl = 76; tpi = 2; }
       else if (b2 + 4 <= 27 * 152) { rb = 27; nl = 152; tpi = 4; }
+      else if (b2 + 4 <= 27 * 240) { rb = 27; nl = 240; tpi = 8; }
       if (rb) {
         R28Mod c = r28_mod(x->n2, rb, nl);
         x->wide.rb = rb;
@@ -859,6 +860,7 @@ static pcb_status run_wide(pcb_ctx* x, const WStep* prog, int nsteps, const uint
   PCB_W(28, 38, 1)
   PCB_W(28, 76, 2)
   PCB_W(27, 152, 4)
+  PCB_W(27, 240, 8)
 #undef PCB_W
   return PCB_E_UNSUPPORTED;
 }
@@ -881,6 +883,7 @@ static pcb_status run_pub_enc(pcb_ctx* x, const uint32_t* r, const uint32_t* m, 
   PCB_W(28, 38, 1)
   PCB_W(28, 76, 2)
   PCB_W(27, 152, 4)
+  PCB_W(27, 240, 8)
 #undef PCB_W
   return PCB_E_UNSUPPORTED;
 }

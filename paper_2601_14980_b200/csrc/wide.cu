@@ -219,5 +219,6 @@ pcb_status launch_wide(const WideMod& md, const WStep* prog, int nsteps, const u
 PCB_WIDE(28, 38, 1)   // n^2 <= 1060 bits (toy / 64-bit keys)
 PCB_WIDE(28, 76, 2)   // n^2 <= 2124 bits (1024-bit keys)
 PCB_WIDE(27, 152, 4)  // n^2 <= 4100 bits (2048-bit keys)
+PCB_WIDE(27, 240, 8)  // n^2 <= 6476 bits (3072-bit keys)
 
 }  // namespace pcb

@@ -232,11 +232,15 @@ def test_3072_bit_crt_encrypt_decrypt_vs_oracle():
         assert cs[i] == O.crt_encrypt_with_r(okp, ms[i], rs[i])
     m = ph.decrypt_batch(c)
     assert L.limbs_to_ints(m.cpu().numpy().view(np.uint32)) == ms
-    # public-key path at 6144-bit n^2 is not instantiated in this build
+    # public-key path at 6144-bit n^2 (radix-2^27 core, 240 limbs): bit-identical to CRT Enc
     pub = P.Paillier(P.PublicKey(kp.n, 3072))
-    with pytest.raises(L.PcbError):
-        pub.encrypt_batch(M.cpu().numpy().view(np.uint32)[:2].copy(), R.cpu().numpy().view(np.uint32)[:2].copy(),
-                          use_crt=False)
+    c_pub = pub.encrypt_batch(M.cpu().numpy().view(np.uint32)[:8].copy(), R.cpu().numpy().view(np.uint32)[:8].copy(),
+                              use_crt=False)
+    assert (c_pub == c.cpu().numpy().view(np.uint32)[:8]).all()
+    # homomorphic aggregation at 6144 bits decrypts to the plaintext sum (cfg4)
+    agg = ph.aggregate_batch(c[:50])
+    s = ph.decrypt_batch(agg.reshape(1, -1))
+    assert L.limbs_to_ints(s.cpu().numpy().view(np.uint32))[0] == sum(ms[:50]) % kp.n
 
 
 def test_3072_bit_matches_compiled_reference():
