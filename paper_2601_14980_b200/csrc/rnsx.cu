@@ -97,6 +97,7 @@ struct XArgs {
   uint32_t* out;  // count x K: B' residues (lazy Montgomery) of the result
   int count, mode, S;
   int dbg;  // timing experiments: 1 = tensor/stream only, 2 = CUDA cores only
+  int cl;   // CTAs per cluster sharing the W stream (1 or 2)
   RxProg prog;  // kRxProg
 };
 
@@ -312,8 +313,8 @@ __device__ __forceinline__ void rx_mm(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
 }
 
 template <class C>
-__device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int nsteps, int npre, int s_x2, int s_tab,
-                                             int s_main, int s_fin) {
+__device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine, int nsteps, int npre, int s_x2,
+                                             int s_tab, int s_main, int s_fin) {
   constexpr int NQ = C::NQ, NV = C::NV, RPT = C::RPT;
   const int ntiles = (P.count + C::TILE - 1) / C::TILE;
   const int park = P.ntab, park_x2 = P.ntab + 1;
@@ -377,7 +378,8 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int nste
       return rec(G.mtab, ((size_t)tcol * G.nwin + w) * 64 + d);
     };
 #pragma unroll 1
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int k = 0; k < mine; k++) {
+      const int tile = blockIdx.x + k * gridDim.x;
       const int el0 = tile * C::TILE + T.e;
       const bool live = el0 < P.count;
       const int el = live ? el0 : P.count - 1;  // padding lanes recompute the last element (not stored)
@@ -512,8 +514,10 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int nste
     double* sSa = reinterpret_cast<double*>(T.sm + C::OFF_S);
     double* sSb = sSa + C::G * C::TILE;
     const int npairs = (ntiles + 1) / 2;
+    (void)npairs;
 #pragma unroll 1
-    for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+    for (int k = 0; k < mine; k++) {
+      const int pr = blockIdx.x + k * gridDim.x;
       const int ela = (2 * pr) * C::TILE + T.e, elb = (2 * pr + 1) * C::TILE + T.e;
       const bool la = ela < P.count, lb = elb < P.count;
       uint32_t XBa[RPT], XQa[RPT], XBb[RPT], XQb[RPT];
@@ -545,7 +549,8 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int nste
     return;
   }
 #pragma unroll 1
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int k = 0; k < mine; k++) {
+    const int tile = blockIdx.x + k * gridDim.x;
     const int el = tile * C::TILE + T.e;
     const bool live = el < P.count;
     uint32_t XB[RPT], XQ[RPT];
@@ -590,9 +595,21 @@ enum : uint32_t { kFGemm = 1, kFG2 = 2, kFChunk = 4, kFChunkEnd = 8, kFStage = 1
 // {A offset, B offset | LBO, idesc, flags}; elect.sync issue), warp 1 streams the W stages into
 // the ring (one bulk copy per stage, full/empty mbarrier handshake).  Scalars come by value: a
 // noinline callee would otherwise re-read the kernel parameters through generic loads.
+__device__ __forceinline__ void commit_elect_mc(uint64_t* mbar, uint16_t mask) {  // arrive in every CTA of mask
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          umma::smem_u32(mbar)),
+      "h"(mask)
+      : "memory");
+}
+
 template <class C>
 __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride, uint8_t* sm, uint64_t* bars,
-                                           uint32_t nprod, int lane) {
+                                           uint32_t nprod, int lane, int cl, uint32_t rank) {
+  // cl == 2: the CTA pair of a cluster shares the stream; each CTA fetches half of every stage
+  // and multicasts it into both CTAs' rings (half the L2 traffic per SM)
   uint64_t* full = bars;
   uint64_t* empty = bars + C::NSTAGE;
   uint8_t* ring = sm + C::OFF_RING;
@@ -614,7 +631,13 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
         const uint2 d = stg[i];
         if (lane == 0) {
           umma::mbar_arrive_expect_tx(full + pslot, d.y);
-          umma::bulk_g2s(ring + pslot * C::SLOT, wimg + (size_t)d.x * 16, d.y, full + pslot);
+          if (cl == 2) {
+            const uint32_t half = d.y >> 1;
+            umma::bulk_g2s_mc(ring + pslot * C::SLOT + rank * half, wimg + (size_t)d.x * 16 + rank * half, half,
+                              full + pslot, 0x3);
+          } else {
+            umma::bulk_g2s(ring + pslot * C::SLOT, wimg + (size_t)d.x * 16, d.y, full + pslot);
+          }
         }
         __syncwarp();
         if (++pslot == (uint32_t)C::NSTAGE) { pslot = 0; pph ^= 1; }
@@ -625,7 +648,7 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
 
 // DBG: 0 normal, 1 no compute handshakes (tensor + stream only), 3 stream only, 4 MMAs only
 template <class C, int DBG>
-__device__ __noinline__ void mma_role(uint8_t* sm, uint32_t tm, uint64_t* bars, uint32_t nprod) {
+__device__ __noinline__ void mma_role(uint8_t* sm, uint32_t tm, uint64_t* bars, uint32_t nprod, int cl) {
   uint64_t* full = bars;
   uint64_t* empty = bars + C::NSTAGE;
   uint64_t* dfull = bars + 2 * C::NSTAGE;
@@ -677,7 +700,8 @@ __device__ __noinline__ void mma_role(uint8_t* sm, uint32_t tm, uint64_t* bars, 
             if ((threadIdx.x & 31) == 0) umma::mbar_arrive(empty + cslot);
             __syncwarp();
           } else if (kRing) {
-            commit_elect(empty + cslot);
+            if (cl == 2) commit_elect_mc(empty + cslot, 0x3);  // the slot is shared by the CTA pair
+            else commit_elect(empty + cslot);
           }
           if (++cslot == (uint32_t)C::NSTAGE) { cslot = 0; cph ^= 1; }
         }
@@ -706,12 +730,15 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     reinterpret_cast<uint32_t*>(sm + C::OFF_SLT)[o] = P.slt[o];
   if (warp == C::NCW) umma::tmem_alloc<C::TMC>(tbase);
   if (tid == 0) {
-    for (int i = 0; i < 2 * C::NSTAGE + C::NB; i++) umma::mbar_init(bars + i, 1);
+    for (int i = 0; i < C::NSTAGE; i++) umma::mbar_init(bars + i, 1);                  // full
+    for (int i = 0; i < C::NSTAGE; i++) umma::mbar_init(bars + C::NSTAGE + i, P.cl);   // empty: every CTA of the pair
+    for (int i = 0; i < C::NB; i++) umma::mbar_init(bars + 2 * C::NSTAGE + i, 1);      // dfull
     for (int i = 0; i < C::NB + 2 * C::NT; i++) umma::mbar_init(bars + 2 * C::NSTAGE + C::NB + i, C::NCW);
   }
   umma::fence_async_smem();
   umma::tmem_fence_before();
   __syncthreads();
+  if (P.cl == 2) umma::cluster_sync();  // the peer's barriers exist before any multicast lands
   umma::tmem_fence_after();
   const uint32_t tm = *tbase;
   // uniform step plan: [pre0] pre1 | x^2 | table (ntab-1) | main (nops-1) | final
@@ -719,19 +746,23 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
   const int s_x2 = npre, s_tab = s_x2 + 1, s_main = s_tab + (P.ntab - 1), s_fin = s_main + (P.nops - 1);
   const int nsteps = P.mode == kRxProg ? P.prog.nsteps : s_fin + 1;
   const int ntiles = (P.count + C::TILE - 1) / C::TILE;
+  // units (tiles, or tile pairs when NT == 2) of this CTA: u = blockIdx.x + k gridDim.x; within a
+  // cluster every CTA runs the count of its rank-0 CTA (the other one runs dead tiles at the tail)
+  const int units = P.mode == kRxProg ? ntiles : (ntiles + C::NT - 1) / C::NT;
+  const int b0 = P.cl == 2 ? (int)(blockIdx.x & ~1u) : (int)blockIdx.x;
+  const int mine = b0 < units ? (units - 1 - b0) / (int)gridDim.x + 1 : 0;
   if (warp >= C::NCW) {
     // role warpgroup hands registers to the compute warps (CTA pool: 4 x 64 x 32 = 16 x 16 x 32)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
-    const int units = P.mode == kRxProg ? ntiles : (ntiles + C::NT - 1) / C::NT;  // tiles or tile pairs
-    const int mine = blockIdx.x < units ? (units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const uint32_t np = (uint32_t)(mine * nsteps);
     if (warp == C::NCW) {
-      if (P.dbg == 0) mma_role<C, 0>(sm, tm, bars, np);
-      else if (P.dbg == 1) mma_role<C, 1>(sm, tm, bars, np);
-      else if (P.dbg == 3) mma_role<C, 3>(sm, tm, bars, np);
-      else if (P.dbg == 4) mma_role<C, 4>(sm, tm, bars, np);
+      if (P.dbg == 0) mma_role<C, 0>(sm, tm, bars, np, P.cl);
+      else if (P.dbg == 1) mma_role<C, 1>(sm, tm, bars, np, P.cl);
+      else if (P.dbg == 3) mma_role<C, 3>(sm, tm, bars, np, P.cl);
+      else if (P.dbg == 4) mma_role<C, 4>(sm, tm, bars, np, P.cl);
     }
-    if (warp == C::NCW + 1 && P.dbg != 2 && P.dbg != 4) producer_role<C>(P.wimg, P.wimg_stride, sm, bars, np, lane);
+    if (warp == C::NCW + 1 && P.dbg != 2 && P.dbg != 4)
+      producer_role<C>(P.wimg, P.wimg_stride, sm, bars, np, lane, P.cl, P.cl == 2 ? umma::cluster_ctarank() : 0);
     __syncwarp();
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
@@ -752,10 +783,11 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     T.dfree = T.dfull + C::NB;
     T.a1 = T.dfree + C::NB;
     T.a2 = T.a1 + 1;
-    if (P.dbg == 0 || P.dbg == 2) compute_role<C>(P, T, nsteps, npre, s_x2, s_tab, s_main, s_fin);
+    if (P.dbg == 0 || P.dbg == 2) compute_role<C>(P, T, mine, nsteps, npre, s_x2, s_tab, s_main, s_fin);
   }
   umma::tmem_fence_before();
   __syncthreads();
+  if (P.cl == 2) umma::cluster_sync();  // no CTA leaves while its peer may still multicast into it
   if (warp == C::NCW) umma::tmem_dealloc<C::TMC>(tm);
 }
 
@@ -886,7 +918,16 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int ntiles = (int)((count + C::TILE - 1) / C::TILE);
   const int units = mode == kRxProg ? ntiles : (ntiles + C::NT - 1) / C::NT;
-  const int blocks = units < nsm ? units : nsm;
+  // PCB_RNSX_CL=2: CTA pairs share the W stream (cluster multicast, each CTA fetches half of
+  // every stage).  Measured slower on B200 (K = 144 public Enc 277 K/s vs 305 K/s): with clusters
+  // of 2 the multicast does not cut the L2 -> SM traffic each SM receives, which is the bound; kept
+  // opt-in for the record (profiles/r01_rnsx_cluster_multicast.txt).
+  const char* clv = getenv("PCB_RNSX_CL");
+  int cl = clv ? atoi(clv) : 1;
+  if (cl != 2 || units < 2 || P.dbg != 0) cl = 1;
+  P.cl = cl;
+  int blocks = units < nsm ? units : nsm;
+  if (cl == 2) blocks = std::min((units + 1) & ~1, nsm & ~1);
   const size_t nthr = (size_t)blocks * C::NCT;
   pcb_status e = PCB_OK;
   P.tab = nullptr;
@@ -897,7 +938,23 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
   if (!e) {
     ProfMark pm;
     if (prof_enabled()) pm = prof_start(st);
-    rnsx_kernel<C><<<blocks, C::NTHR, C::SMEM, st>>>(P);
+    if (cl == 2) {
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(blocks);
+      lc.blockDim = dim3(C::NTHR);
+      lc.dynamicSmemBytes = C::SMEM;
+      lc.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      cudaLaunchKernelEx(&lc, rnsx_kernel<C>, P);
+    } else {
+      rnsx_kernel<C><<<blocks, C::NTHR, C::SMEM, st>>>(P);
+    }
     count_launch();
     if (prof_enabled()) {
       prof_stop(pm, st, alg_mac32 * (double)count);
