@@ -647,6 +647,61 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
 }
 
 // DBG: 0 normal, 1 no compute handshakes (tensor + stream only), 3 stream only, 4 MMAs only
+// Production MMA issue loop: the product's structure (GEMM -> chunk -> k-step) is the loop
+// structure, so the per-MMA work is one full-barrier wait, the descriptor adds, the MMA and the
+// slot release (one 8 KB slice per ring stage).
+template <class C>
+__device__ __noinline__ void mma_fast(uint8_t* sm, uint32_t tm, uint64_t* bars, uint32_t nprod, int cl) {
+  static_assert(C::SPS == 1, "one slice per stage");
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::NSTAGE;
+  uint64_t* dfull = bars + 2 * C::NSTAGE;
+  uint64_t* dfree = dfull + C::NB;
+  uint64_t* abar = dfree + C::NB;  // per tile: a1, a2
+  const uint64_t hi = umma::desc_kmajor(0, 128) & 0xFFFFFFFF00000000ull;
+  const uint32_t a1lo = (uint32_t)umma::desc_kmajor(umma::smem_u32(sm + C::OFF_A1), C::TILE);
+  const uint32_t a2lo = (uint32_t)umma::desc_kmajor(umma::smem_u32(sm + C::OFF_A2), C::TILE);
+  const uint32_t ring16 = umma::smem_u32(sm + C::OFF_RING) >> 4;
+  constexpr uint32_t SLOT16 = C::SLOT / 16, ABLK16 = C::ABLK / 16;
+  uint32_t cslot = 0, cph = 0, dbi = 0, dph = 0, dcnt = 0;
+  uint32_t bslot = ring16;  // address field of the current ring slot
+#pragma unroll 1
+  for (uint32_t pr = 0; pr < nprod; pr++) {
+#pragma unroll 1
+    for (int seg = 0; seg < 2 * C::NT; seg++) {
+      const int gm = C::NT == 2 ? seg >> 1 : seg, tt = C::NT == 2 ? (seg & 1) : 0;
+      umma::mbar_wait(abar + 2 * tt + gm, pr & 1);
+      umma::tmem_fence_after();
+      const uint32_t alo = (gm ? a2lo : a1lo) + tt * ABLK16;
+      const int ks = gm ? C::KS2 : C::KS1;
+#pragma unroll
+      for (int c = 0; c < C::NC; c++) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const uint32_t ncol = (uint32_t)C::ncol(c);
+        const uint32_t idesc = umma::idesc_i8(C::TILE, (int)ncol);
+        if (dcnt >= (uint32_t)C::NB) {
+          umma::mbar_wait(dfree + dbi, dph ^ 1);
+          umma::tmem_fence_after();
+        }
+        const uint32_t dt = tm + dbi * C::BUFC;
+#pragma unroll 1
+        for (int k = 0; k < ks; k++) {
+          umma::mbar_wait(full + cslot, cph);
+          mma_elect(dt, hi | (uint64_t)(alo + (uint32_t)k * (2 * C::TILE * 16 / 16)),
+                    hi | (uint64_t)((bslot & 0x3FFFu) | (ncol << 16)), idesc, (uint32_t)k);
+          if (cl == 2) commit_elect_mc(empty + cslot, 0x3); else commit_elect(empty + cslot);
+          bslot += SLOT16;
+          if (++cslot == (uint32_t)C::NSTAGE) { cslot = 0; cph ^= 1; bslot = ring16; }
+        }
+        commit_elect(dfull + dbi);
+        dcnt++;
+        if (++dbi == (uint32_t)C::NB) { dbi = 0; dph ^= 1; }
+      }
+    }
+  }
+}
+
 template <class C, int DBG>
 __device__ __noinline__ void mma_role(uint8_t* sm, uint32_t tm, uint64_t* bars, uint32_t nprod, int cl) {
   uint64_t* full = bars;
@@ -756,7 +811,7 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
     const uint32_t np = (uint32_t)(mine * nsteps);
     if (warp == C::NCW) {
-      if (P.dbg == 0) mma_role<C, 0>(sm, tm, bars, np, P.cl);
+      if (P.dbg == 0) mma_fast<C>(sm, tm, bars, np, P.cl);
       else if (P.dbg == 1) mma_role<C, 1>(sm, tm, bars, np, P.cl);
       else if (P.dbg == 3) mma_role<C, 3>(sm, tm, bars, np, P.cl);
       else if (P.dbg == 4) mma_role<C, 4>(sm, tm, bars, np, P.cl);
