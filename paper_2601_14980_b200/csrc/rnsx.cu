@@ -261,7 +261,7 @@ __device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t
         if (r >= 2 * rq.x) r -= 2 * rq.x;
         XQ[w] = r;
         xp[t] = mulr(r, rr.x, rq.x, rq.y);
-        sp += (double)xp[t] * __hiloint2double((int)rr.z, (int)rr.y);
+        sp = __fma_rn((double)xp[t], __hiloint2double((int)rr.z, (int)rr.y), sp);  // beta needs 2^-20 only
       }
       uint8_t* dst = A2 + umma::kmajor_off(T.e, 4 * (C::CP * c + T.g * ptc + 4 * j), C::TILE);
       if (QT == 4) stq<4>(dst, xp); else stq<2>(dst, xp);
