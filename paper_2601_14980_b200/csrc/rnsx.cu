@@ -392,6 +392,14 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
         } else if (stp.xs != kRsKeep) {
           vec_op(src_ptr(stp.xs, stp.xa, el), 4, XB, XQ, 0);
         }
+        if (s + 1 < G.nsteps) {  // warm L2 with the next step's gathered multiplier record (no registers)
+          const XStep nx = G.st[s + 1];
+          if (nx.ys == kRsMat || nx.ys == kRsSelf || nx.ys == kRsPart) {
+            const char* pn = reinterpret_cast<const char*>(src_ptr(nx.ys, nx.ya, el));
+#pragma unroll
+            for (int o = 0; o < NV * 16; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pn + o));
+          }
+        }
         if (stp.ys == kRsSq)
           rx_mm<C>(XB, XQ, true, nullptr, 4, T);
         else
