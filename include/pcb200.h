@@ -73,6 +73,9 @@ int pcb_ctx_has_private(const pcb_ctx* ctx);
 /* Core that runs the CRT halves of Enc/Dec: 0 = 32-bit carry-chain Montgomery (side_kernel),
  * 1 = RNS Montgomery with tensor-core base extensions (rns_pow_kernel; 2048-bit keys, default;
  * PCB_RNS=0 in the environment at context creation selects 0), 2 = radix-2^28 (3072-bit). */
+/* Stream priority of the context's internal CRT-half side streams (used for batches below one
+ * full wave): high != 0 -> the device's greatest priority, 0 -> least (e.g. offline precompute). */
+pcb_status pcb_ctx_set_priority(pcb_ctx* ctx, int high);
 int pcb_ctx_engine(const pcb_ctx* ctx);
 /* Copies n (L limbs) / n^2 (2L limbs) out of the context. */
 pcb_status pcb_ctx_get_n(const pcb_ctx* ctx, uint32_t* n, uint32_t* n2);

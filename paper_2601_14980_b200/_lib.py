@@ -58,6 +58,7 @@ SIGNATURES = {
     "pcb_ctx_n_bits": (C.c_uint32, [_vp]),
     "pcb_ctx_has_private": (C.c_int, [_vp]),
     "pcb_ctx_engine": (C.c_int, [_vp]),
+    "pcb_ctx_set_priority": (C.c_int, [_vp, C.c_int]),
     "pcb_ctx_get_n": (C.c_int, [_vp, _u32p, _u32p]),
     "pcb_ctx_counters": (None, [_vp, _u64p, _u64p]),
     "pcb_ctx_reset_counters": (None, [_vp]),

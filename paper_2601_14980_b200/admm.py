@@ -238,6 +238,11 @@ class EncryptedSession(ShardedDriver):
         self.edge = Paillier(PublicKey(keys.n, keys.key_bits), device=device)
         self.L = self.master.L
         self.lib = L.lib()
+        # the iteration's critical path (online Enc -> edge step -> Dec + update) runs at high
+        # stream priority; the offline r^n precompute of the next iteration only fills idle SMs
+        _raise_for(self.lib.pcb_ctx_set_priority(self.master._ctx, 1), "priority")
+        _raise_for(self.lib.pcb_ctx_set_priority(self.edge._ctx, 1), "priority")
+        _raise_for(self.lib.pcb_ctx_set_priority(self.pre._ctx, 0), "priority")
 
     def _stream(self):
         import torch
@@ -319,7 +324,8 @@ class EncryptedSession(ShardedDriver):
         self.rall = torch.empty((2 * sum(self.sizes), self.L), dtype=torch.int32, device=self.dev)
         self.rn = [torch.empty((2 * n_own, 2 * self.L), dtype=torch.int32, device=self.dev) for _ in range(2)]
         self.m0 = torch.zeros((2 * n_own, 1), dtype=torch.int32, device=self.dev)
-        self.pstream = torch.cuda.Stream(device=self.device)
+        self.pstream = torch.cuda.Stream(device=self.device, priority=0)  # least priority (offline work)
+        self.mstream = torch.cuda.Stream(device=self.device, priority=-1)  # critical path
         self.rn_ready = [torch.cuda.Event() for _ in range(2)]
         self.enc_done = torch.cuda.Event()
         return cl_b + cla[0] + cla[1]
@@ -346,6 +352,17 @@ class EncryptedSession(ShardedDriver):
             self.rn_ready[slot].record(ps)
 
     def step_all(self, t: int) -> int:
+        """The iteration on the high-priority session stream, joined back to the caller's stream."""
+        import torch
+
+        cur = torch.cuda.current_stream(self.device)
+        self.mstream.wait_stream(cur)
+        with torch.cuda.stream(self.mstream):
+            clamps = self._step_all(t)
+        cur.wait_stream(self.mstream)
+        return clamps
+
+    def _step_all(self, t: int) -> int:
         """One iteration, all owned blocks batched: quantize [z ; -v] and encrypt online with the
         precomputed rn, launch the offline half of iteration t+1 on the side stream, then one edge
         step over the blocks and one Dec+update — all bit-equal to the block-at-a-time loop."""

@@ -611,6 +611,24 @@ void pcb_ctx_destroy(pcb_ctx* x) {
 uint32_t pcb_ctx_n_limbs(const pcb_ctx* x) { return x ? x->L : 0; }
 uint32_t pcb_ctx_n_bits(const pcb_ctx* x) { return x ? x->nbits : 0; }
 int pcb_ctx_has_private(const pcb_ctx* x) { return x && x->has_prv ? 1 : 0; }
+pcb_status pcb_ctx_set_priority(pcb_ctx* x, int high) {
+  if (!x) return PCB_E_SHAPE;
+  if (auto e = set_device(x)) return e;
+  int least = 0, greatest = 0;
+  if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return PCB_E_CUDA;
+  std::lock_guard<std::mutex> lk(x->mu);
+  for (int k = 0; k < 2; k++) {
+    if (x->side_st[k]) {
+      cudaStreamSynchronize(x->side_st[k]);
+      cudaStreamDestroy(x->side_st[k]);
+      x->side_st[k] = nullptr;
+    }
+    if (cudaStreamCreateWithPriority(&x->side_st[k], cudaStreamNonBlocking, high ? greatest : least) != cudaSuccess)
+      return PCB_E_CUDA;
+  }
+  return PCB_OK;
+}
+
 int pcb_ctx_engine(const pcb_ctx* x) {
   return !x || !x->has_prv ? 0 : (x->use_rnsx ? 3 : (x->use_rns ? 1 : (x->S == 96 ? 2 : 0)));
 }
