@@ -50,9 +50,12 @@ namespace {
 // slices per stream stage: bigger bulk copies where the ring has room (8+ stages either way)
 __host__ __device__ constexpr int sps_for(int) { return 1; }  // one <= 8 KB slice per stage
 
-template <int K_, int NT_ = 1>
+template <int K_, int NT_ = 1, int CG_ = 1>
 struct Cfg {
   static constexpr int K = K_, G = 4, NT = NT_;  // NT: tiles in flight per CTA (1 or 2)
+  // CG = 2: the CTA pair of a cluster runs every MMA as one cta_group::2 MMA (M = 256, the leader
+  // issues); each CTA holds half of every W slice (N / 2 rows), so each SM streams half the bytes
+  static constexpr int CG = CG_;
   static constexpr int CP = 64, TPC = CP / G;  // primes per full chunk (256 TMEM columns), per thread
   static constexpr int NC = (K + CP - 1) / CP, PL = K - CP * (NC - 1), PTL = PL / 4;
   static constexpr int RPT = TPC * (NC - 1) + PTL;  // residues per thread per base
@@ -62,7 +65,7 @@ struct Cfg {
   static constexpr int NSLICE = NC * (KS1 + KS2);  // MMAs (and streamed slices) per product
   static constexpr int SPS = sps_for(K);           // slices per stream stage (one bulk copy)
   static constexpr int NSTG = (NSLICE + SPS - 1) / SPS;  // stages per product
-  static constexpr int SLOT = 8192 * SPS;          // ring slot: SPS slices of <= 256 x 32 bytes
+  static constexpr int SLOT = 8192 * SPS / CG;     // ring slot: SPS slices of <= 256 x 32 bytes (CG = 2: halves)
   static constexpr int NB = 2, BUFC = 256, TMC = 512;  // TMEM ring: 2 buffers of 256 columns
   static constexpr int TILE = 128, NCW = 16, NCT = 32 * NCW, NTHR = NCT + 128;  // + role warpgroup
   static constexpr uint32_t ABLK = TILE * (K1 + K2);  // A1 + A2 of one tile
@@ -77,12 +80,14 @@ struct Cfg {
   __host__ __device__ static constexpr int ncol(int c) { return 16 * ptc(c); }
   static_assert(PL % 8 == 0 && (PTL == 2 || PTL % 4 == 0), "ragged chunk: 8 or a multiple of 16 primes");
   static_assert(NSTAGE >= 4, "stream ring");
-  static_assert((2 * NSTAGE + 2 * NB + 2 * NT) * 8 + 4 <= 512, "barriers");
+  static_assert((3 * NSTAGE + 2 * NB + 2 * NT) * 8 + 4 <= 512, "barriers");
+  static_assert(CG == 1 || (CG == 2 && NT == 1), "pair MMA only with one tile per CTA");
   static_assert(NT == 1 || NT == 2, "tiles in flight");
 };
 
 struct XArgs {
   const uint8_t* wimg;
+  const uint8_t* wimg2;  // split-halves stream image (cta_group::2)
   size_t wimg_stride;  // bytes between the replicas of the stream image
   const uint4* cons;
   const uint32_t* cvec;
@@ -147,8 +152,19 @@ struct Thr {
   int e, g, lane, gt, NT;
   uint32_t dbi, dph;
   bool nowait;
+  uint32_t rank;  // CTA rank in the pair (cta_group::2): rank 1 signals the leader's barriers
   uint64_t *dfull, *dfree, *a1, *a2;
 };
+
+// hand-off arrive (A tile ready / TMEM buffer drained): the MMA issuer's barrier is local, or the
+// leader CTA's for the peer of a cta_group::2 pair
+template <class C>
+__device__ __forceinline__ void arrive_issuer(const Thr<C>& T, uint64_t* bar) {
+  if (C::CG == 2 && T.rank == 1)
+    umma::mbar_arrive_remote(bar, 0);
+  else
+    umma::mbar_arrive(bar);
+}
 
 // x (nw words, LE) -> lazy Montgomery residues of this thread's primes (both bases)
 template <class C>
@@ -186,7 +202,7 @@ __device__ __forceinline__ void d_quad(Thr<C>& T, int ptc, int j, bool first, bo
   if (last) {
     umma::tmem_fence_before();
     __syncwarp();
-    if (T.lane == 0 && !T.nowait) umma::mbar_arrive(T.dfree + T.dbi);
+    if (T.lane == 0 && !T.nowait) arrive_issuer<C>(T, T.dfree + T.dbi);
     if (++T.dbi == (uint32_t)C::NB) { T.dbi = 0; T.dph ^= 1; }
   }
 }
@@ -234,7 +250,7 @@ __device__ __forceinline__ void rx_s1(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
   }
   umma::fence_async_smem();
   __syncwarp();
-  if (T.lane == 0) umma::mbar_arrive(a1);
+  if (T.lane == 0) arrive_issuer<C>(T, a1);
 }
 
 template <class C>
@@ -277,7 +293,7 @@ __device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t
     umma::fence_async_smem();
   }
   __syncwarp();
-  if (T.lane == 0) umma::mbar_arrive(a2);
+  if (T.lane == 0) arrive_issuer<C>(T, a2);
 }
 
 template <class C>
@@ -613,6 +629,91 @@ __device__ __forceinline__ void commit_elect_mc(uint64_t* mbar, uint16_t mask) {
       : "memory");
 }
 
+__device__ __forceinline__ void mma_elect_cg2(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit_elect_cg2(uint64_t* mbar) {  // arrive in both CTAs of the pair
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          umma::smem_u32(mbar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+// cta_group::2 leader (rank 0): one M = 256 MMA per slice for both CTAs' tiles; waits for both
+// halves of the slice (own full barrier + the peer's, relayed) and both CTAs' A tiles / drains.
+template <class C>
+__device__ __noinline__ void mma_pair(uint8_t* sm, uint32_t tm, uint64_t* bars, uint32_t nprod) {
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::NSTAGE;
+  uint64_t* dfull = bars + 2 * C::NSTAGE;
+  uint64_t* dfree = dfull + C::NB;
+  uint64_t* abar = dfree + C::NB;
+  uint64_t* pfull = abar + 2 * C::NT;
+  const uint64_t hi = umma::desc_kmajor(0, 128) & 0xFFFFFFFF00000000ull;
+  const uint32_t a1lo = (uint32_t)umma::desc_kmajor(umma::smem_u32(sm + C::OFF_A1), C::TILE);
+  const uint32_t a2lo = (uint32_t)umma::desc_kmajor(umma::smem_u32(sm + C::OFF_A2), C::TILE);
+  const uint32_t ring16 = umma::smem_u32(sm + C::OFF_RING) >> 4;
+  constexpr uint32_t SLOT16 = C::SLOT / 16;
+  uint32_t cslot = 0, cph = 0, dbi = 0, dph = 0, dcnt = 0, bslot = ring16;
+#pragma unroll 1
+  for (uint32_t pr = 0; pr < nprod; pr++) {
+#pragma unroll 1
+    for (int gm = 0; gm < 2; gm++) {
+      umma::mbar_wait_cluster(abar + gm, pr & 1);
+      umma::tmem_fence_after();
+      const uint32_t alo = gm ? a2lo : a1lo;
+      const int ks = gm ? C::KS2 : C::KS1;
+#pragma unroll
+      for (int c = 0; c < C::NC; c++) {
+        const uint32_t ncol = (uint32_t)C::ncol(c);
+        const uint32_t idesc = umma::idesc_i8(2 * C::TILE, (int)ncol);
+        if (dcnt >= (uint32_t)C::NB) {
+          umma::mbar_wait_cluster(dfree + dbi, dph ^ 1);
+          umma::tmem_fence_after();
+        }
+        const uint32_t dt = tm + dbi * C::BUFC;
+#pragma unroll 1
+        for (int k = 0; k < ks; k++) {
+          umma::mbar_wait(full + cslot, cph);
+          umma::mbar_wait_cluster(pfull + cslot, cph);
+          mma_elect_cg2(dt, hi | (uint64_t)(alo + (uint32_t)k * (2 * C::TILE * 16 / 16)),
+                        hi | (uint64_t)((bslot & 0x3FFFu) | ((ncol / 2) << 16)), idesc, (uint32_t)k);
+          commit_elect_cg2(empty + cslot);
+          bslot += SLOT16;
+          if (++cslot == (uint32_t)C::NSTAGE) { cslot = 0; cph ^= 1; bslot = ring16; }
+        }
+        commit_elect_cg2(dfull + dbi);
+        dcnt++;
+        if (++dbi == (uint32_t)C::NB) { dbi = 0; dph ^= 1; }
+      }
+    }
+  }
+}
+
+// cta_group::2 peer (rank 1): relay "my half of slice i has landed" to the leader, in order
+template <class C>
+__device__ __noinline__ void relay_pair(uint64_t* bars, uint32_t nprod, int lane) {
+  uint64_t* full = bars;
+  uint64_t* pfull = bars + 2 * C::NSTAGE + 2 * C::NB + 2 * C::NT;
+  const uint32_t total = nprod * (uint32_t)C::NSLICE;
+  uint32_t slot = 0, ph = 0;
+#pragma unroll 1
+  for (uint32_t i = 0; i < total; i++) {
+    umma::mbar_wait(full + slot, ph);
+    if (lane == 0) umma::mbar_arrive_remote(pfull + slot, 0);
+    __syncwarp();
+    if (++slot == (uint32_t)C::NSTAGE) { slot = 0; ph ^= 1; }
+  }
+}
+
 template <class C>
 __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride, uint8_t* sm, uint64_t* bars,
                                            uint32_t nprod, int lane, int cl, uint32_t rank) {
@@ -638,8 +739,12 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
         if (issued >= (uint32_t)C::NSTAGE) umma::mbar_wait(empty + pslot, pph ^ 1);
         const uint2 d = stg[i];
         if (lane == 0) {
-          umma::mbar_arrive_expect_tx(full + pslot, d.y);
-          if (cl == 2) {
+          umma::mbar_arrive_expect_tx(full + pslot, C::CG == 2 ? d.y >> 1 : d.y);
+          if (C::CG == 2) {  // wimg is the split-halves image: this CTA's half of the slice
+            const uint32_t half = d.y >> 1;
+            umma::bulk_g2s(ring + pslot * C::SLOT, wimg + (size_t)d.x * 16 + rank * half, half, full + pslot);
+            (void)cl;
+          } else if (cl == 2) {
             const uint32_t half = d.y >> 1;
             umma::bulk_g2s_mc(ring + pslot * C::SLOT + rank * half, wimg + (size_t)d.x * 16 + rank * half, half,
                               full + pslot, 0x3);
@@ -785,18 +890,24 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
   extern __shared__ __align__(1024) uint8_t sm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
-  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 2 * C::NSTAGE + 2 * C::NB + 2 * C::NT);
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(bars + 3 * C::NSTAGE + 2 * C::NB + 2 * C::NT);
   for (uint32_t o = tid * 16; o < (uint32_t)(C::NT * C::ABLK); o += C::NTHR * 16)
     *reinterpret_cast<uint4*>(sm + C::OFF_A1 + o) = make_uint4(0, 0, 0, 0);
   for (int o = tid; o < C::K * 3; o += C::NTHR) reinterpret_cast<uint4*>(sm + C::OFF_CONS)[o] = P.cons[o];
   for (int o = tid; o < 4 * C::NSLICE + 2 * C::NSTG; o += C::NTHR)
     reinterpret_cast<uint32_t*>(sm + C::OFF_SLT)[o] = P.slt[o];
-  if (warp == C::NCW) umma::tmem_alloc<C::TMC>(tbase);
+  if (warp == C::NCW) {
+    if (C::CG == 2) umma::tmem_alloc_cg2<C::TMC>(tbase);
+    else umma::tmem_alloc<C::TMC>(tbase);
+  }
   if (tid == 0) {
+    const int cn = C::CG == 2 ? 1 : P.cl;  // empty: multicast commits (one per CTA for cluster multicast)
     for (int i = 0; i < C::NSTAGE; i++) umma::mbar_init(bars + i, 1);                  // full
-    for (int i = 0; i < C::NSTAGE; i++) umma::mbar_init(bars + C::NSTAGE + i, P.cl);   // empty: every CTA of the pair
+    for (int i = 0; i < C::NSTAGE; i++) umma::mbar_init(bars + C::NSTAGE + i, cn);     // empty
     for (int i = 0; i < C::NB; i++) umma::mbar_init(bars + 2 * C::NSTAGE + i, 1);      // dfull
-    for (int i = 0; i < C::NB + 2 * C::NT; i++) umma::mbar_init(bars + 2 * C::NSTAGE + C::NB + i, C::NCW);
+    // dfree / A-tile hand-offs: every compute warp of the CTA (of both CTAs at the pair leader)
+    for (int i = 0; i < C::NB + 2 * C::NT; i++) umma::mbar_init(bars + 2 * C::NSTAGE + C::NB + i, C::NCW * C::CG);
+    for (int i = 0; i < C::NSTAGE; i++) umma::mbar_init(bars + 2 * C::NSTAGE + 2 * C::NB + 2 * C::NT + i, 1);  // pfull
   }
   umma::fence_async_smem();
   umma::tmem_fence_before();
@@ -818,14 +929,20 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     // role warpgroup hands registers to the compute warps (CTA pool: 4 x 64 x 32 = 16 x 16 x 32)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 32;");
     const uint32_t np = (uint32_t)(mine * nsteps);
-    if (warp == C::NCW) {
+    const uint32_t rank = P.cl == 2 ? umma::cluster_ctarank() : 0;
+    if (C::CG == 2) {
+      if (warp == C::NCW) {
+        if (rank == 0) mma_pair<C>(sm, tm, bars, np);
+        else relay_pair<C>(bars, np, lane);
+      }
+    } else if (warp == C::NCW) {
       if (P.dbg == 0) mma_fast<C>(sm, tm, bars, np, P.cl);
       else if (P.dbg == 1) mma_role<C, 1>(sm, tm, bars, np, P.cl);
       else if (P.dbg == 3) mma_role<C, 3>(sm, tm, bars, np, P.cl);
       else if (P.dbg == 4) mma_role<C, 4>(sm, tm, bars, np, P.cl);
     }
     if (warp == C::NCW + 1 && P.dbg != 2 && P.dbg != 4)
-      producer_role<C>(P.wimg, P.wimg_stride, sm, bars, np, lane, P.cl, P.cl == 2 ? umma::cluster_ctarank() : 0);
+      producer_role<C>(C::CG == 2 ? P.wimg2 : P.wimg, P.wimg_stride, sm, bars, np, lane, P.cl, rank);
     __syncwarp();
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
@@ -842,6 +959,8 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     T.dbi = 0;
     T.dph = 0;
     T.nowait = P.dbg == 2;
+    if constexpr (C::CG == 2) T.rank = umma::cluster_ctarank();
+    else T.rank = 0;
     T.dfull = bars + 2 * C::NSTAGE;
     T.dfree = T.dfull + C::NB;
     T.a1 = T.dfree + C::NB;
@@ -851,7 +970,10 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
   umma::tmem_fence_before();
   __syncthreads();
   if (P.cl == 2) umma::cluster_sync();  // no CTA leaves while its peer may still multicast into it
-  if (warp == C::NCW) umma::tmem_dealloc<C::TMC>(tm);
+  if (warp == C::NCW) {
+    if (C::CG == 2) umma::tmem_dealloc_cg2<C::TMC>(tm);
+    else umma::tmem_dealloc<C::TMC>(tm);
+  }
 }
 
 // Exact conversion of the B' residues to the binary residue mod N (one thread per element):
@@ -952,6 +1074,7 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
   XArgs P;
   if (prog) P.prog = *prog;
   P.wimg = md.d_wimg;
+  P.wimg2 = md.d_wimg2;
   P.wimg_stride = md.wimg_stride;
   P.cons = md.d_cons;
   P.cvec = reinterpret_cast<const uint32_t*>(md.d_cvec);
@@ -988,6 +1111,7 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
   const char* clv = getenv("PCB_RNSX_CL");
   int cl = clv ? atoi(clv) : 1;
   if (cl != 2 || units < 2 || P.dbg != 0) cl = 1;
+  if (C::CG == 2) cl = 2;  // a CTA pair always (a single tile runs with a dead peer)
   P.cl = cl;
   int blocks = units < nsm ? units : nsm;
   if (cl == 2) blocks = std::min((units + 1) & ~1, nsm & ~1);
@@ -1214,7 +1338,7 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
     for (int j = 0; j < K; j++) W2[(size_t)i * (K + 1) + j] = (uint32_t)((uint64_t)mprod_mod(Bp, j, m) * q64[i] % m);
     W2[(size_t)i * (K + 1) + K] = (uint32_t)((m - (uint64_t)big_mod(Mp, m) * q64[i] % m) % m);
   }
-  std::vector<uint8_t> img;
+  std::vector<uint8_t> img, img2;  // img2: every slice as two halves (rows [0, N/2), [N/2, N)), R = N/2 each
   std::vector<uint32_t> slt, soff;  // slice offsets in the image (16-byte units)
   for (int gm = 0; gm < 2; gm++) {
     const int ks = gm ? KS2 : KS1;
@@ -1223,6 +1347,7 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
       for (int s = 0; s < ks; s++) {
         const size_t off = img.size();
         img.resize(off + (size_t)ncol * 32, 0);
+        img2.resize(off + (size_t)ncol * 32, 0);
         soff.push_back((uint32_t)(off / 16));
         uint8_t* dst = img.data() + off;
         for (int nl = 0; nl < ncol; nl++) {
@@ -1239,6 +1364,8 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
               base = src <= K ? W2[(size_t)o * (K + 1) + src] : 0;
             const uint32_t v = (uint32_t)((base << (8 * a)) % m);
             dst[slice_off(nl, kk2, ncol)] = (uint8_t)(v >> (8 * b));
+            const int hn = ncol / 2, hh = nl / hn;
+            img2[off + (size_t)hh * hn * 32 + slice_off(nl - hh * hn, kk2, hn)] = (uint8_t)(v >> (8 * b));
           }
         }
       }
@@ -1299,12 +1426,14 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
   md.ntop = nt;
   md.wimg_stride = (img.size() + 4095) & ~(size_t)4095;
   bool ok = cudaMalloc(&md.d_wimg, md.wimg_stride * kRxReplicas) == cudaSuccess;
+  ok = ok && cudaMalloc(&md.d_wimg2, md.wimg_stride * kRxReplicas) == cudaSuccess;
   ok = ok && cudaMalloc(&md.d_cons, cons.size() * 4) == cudaSuccess;
   ok = ok && cudaMalloc(&md.d_cvec, cvec.size() * 4) == cudaSuccess;
   ok = ok && cudaMalloc(&md.d_out, otab.size() * 4) == cudaSuccess;
   ok = ok && cudaMalloc(&md.d_slt, slt.size() * 4) == cudaSuccess;
   for (int r = 0; r < kRxReplicas; r++)
-    ok = ok && cudaMemcpy(md.d_wimg + r * md.wimg_stride, img.data(), img.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(md.d_wimg + r * md.wimg_stride, img.data(), img.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(md.d_wimg2 + r * md.wimg_stride, img2.data(), img2.size(), cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(md.d_cons, cons.data(), cons.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(md.d_cvec, cvec.data(), cvec.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(md.d_out, otab.data(), otab.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -1320,6 +1449,8 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
 
 void rnsx_free(RnsXModulus* md) {
   if (md->d_wimg) cudaFree(md->d_wimg);
+  if (md->d_wimg2) cudaFree(md->d_wimg2);
+  md->d_wimg2 = nullptr;
   if (md->d_cons) cudaFree(md->d_cons);
   if (md->d_cvec) cudaFree(md->d_cvec);
   if (md->d_out) cudaFree(md->d_out);
@@ -1341,6 +1472,13 @@ pcb_status launch_rnsx_prog(const RnsXModulus& md, const RxProg& prog, const uin
                             uint32_t* y, cudaStream_t st, double alg_mac32) {
   if (count == 0) return PCB_OK;
   if (!md.ok || prog.nsteps < 1 || prog.nsteps > kRxMaxSteps) return PCB_E_UNSUPPORTED;
+  {
+    const char* cgv = getenv("PCB_RNSX_CG2");
+    if (cgv && atoi(cgv) != 0) {
+      if (md.K == 144) return launch_cfg<Cfg<144, 1, 2>>(md, kRxProg, nullptr, 0, 0, x, x_words, nullptr, 0, count, y, st, alg_mac32, &prog);
+      if (md.K == 112) return launch_cfg<Cfg<112, 1, 2>>(md, kRxProg, nullptr, 0, 0, x, x_words, nullptr, 0, count, y, st, alg_mac32, &prog);
+    }
+  }
 #define PCB_RX(KK)                                                                                                 \
   if (md.K == KK) return launch_cfg<Cfg<KK>>(md, kRxProg, nullptr, 0, 0, x, x_words, nullptr, 0, count, y, st, alg_mac32, &prog);
   PCB_RX(72)
@@ -1357,6 +1495,13 @@ pcb_status launch_rnsx(const RnsXModulus& md, int mode, const uint8_t* ops, int 
   if (!md.ok) return PCB_E_UNSUPPORTED;
 #define PCB_RX(KK)                                                                                                 \
   if (md.K == KK) return launch_cfg<Cfg<KK>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
+  {
+    const char* cgv = getenv("PCB_RNSX_CG2");
+    if (cgv && atoi(cgv) != 0) {
+      if (md.K == 144) return launch_cfg<Cfg<144, 1, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
+      if (md.K == 112) return launch_cfg<Cfg<112, 1, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
+    }
+  }
   if (md.K == 72) {  // two tiles in flight per CTA (the K = 72 register budget allows it)
     const char* ppv = getenv("PCB_RNSX_PP");
     const bool pp = !ppv || atoi(ppv) != 0;  // default on; PCB_RNSX_PP=0 runs one tile per CTA

@@ -55,6 +55,7 @@ struct RnsXModulus {
   int K = 0, S = 0;           // primes per base, words of N
   int mpw = 0;                // words of M' (output conversion)
   uint8_t* d_wimg = nullptr;  // base-extension stream: one slice (<= 128 x 32 bytes) per MMA, x kRxReplicas
+  uint8_t* d_wimg2 = nullptr; // the same stream with every slice split in two row halves (cta_group::2)
   size_t wimg_stride = 0;
   uint4* d_cons = nullptr;    // per (g, w): {m, minv, c1, q64}, {m', minv', c2, c3}, {c4, invp, q64'}
   uint4* d_cvec = nullptr;    // constant operands in thread order: [id][g][NV][4]
