@@ -60,9 +60,9 @@ int main() {
   cudaMalloc(&cyc, 8 * 256);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   unsigned long long h[256];
-  for (int grid : {1, 148})
-    for (int ce : {0, 1})
-      for (int N : {64, 128, 256}) {
+  for (int grid : {148})
+    for (int ce : {1})
+      for (int N : {64, 96, 128, 144, 160, 192, 224, 256}) {
         const int n = 4096;
         k<<<grid, 128, 160 * 1024>>>(N, n, ce, cyc);
         cudaError_t e = cudaDeviceSynchronize();
