@@ -118,6 +118,20 @@ pcb_status pcb_encrypt_rn(pcb_ctx* ctx, const uint32_t* m, uint32_t m_limbs, con
 pcb_status pcb_decrypt(pcb_ctx* ctx, const uint32_t* c, size_t count, uint32_t* m, int use_crt,
                        int32_t* status, pcb_stream stream);
 
+/* ---- collaborative variant (paper Alg. 3): the p^2 side delegated to an edge ------------------- */
+
+/* m_i = L(x_i) mu mod n, x_i = CRT(p2_power_i mod p^2, c_i^(eps mod phi(q^2)) mod q^2) —
+ * Paillier::decrypt_with_half (paillier.cpp:363-369).  p2_power: count x pw_limbs (pw_limbs <= 2L),
+ * e.g. an edge's delegated_power (protocol.cpp:15-18).  Statuses as pcb_decrypt.  2048/3072-bit keys. */
+pcb_status pcb_decrypt_with_half(pcb_ctx* ctx, const uint32_t* c, const uint32_t* p2_power, uint32_t pw_limbs,
+                                 size_t count, uint32_t* m, int32_t* status, pcb_stream stream);
+
+/* c_i = CRT((p2_g_power_i mod p^2) r_i^(n mod phi(p^2)) mod p^2, (1 + m_i n) r_i^(n mod phi(q^2)) mod q^2)
+ * — Paillier::finish_split_encrypt (paillier.cpp:402-414).  Statuses as pcb_encrypt. */
+pcb_status pcb_finish_split_encrypt(pcb_ctx* ctx, const uint32_t* m, uint32_t m_limbs, const uint32_t* p2_g_power,
+                                    uint32_t pg_limbs, const uint32_t* r, size_t count, uint32_t* c,
+                                    int32_t* status, pcb_stream stream);
+
 /* ---- homomorphic operations (public key suffices) ----------------------------------------- */
 
 /* out_i = a_i * b_i mod n^2 — Paillier::hom_add (paillier.cpp:428-432).  plain_bits tracking

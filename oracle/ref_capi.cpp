@@ -221,6 +221,42 @@ void pcref_decrypt(void* h, int mode, const uint32_t* c, uint32_t c_limbs, size_
   }
 }
 
+// ---- collaborative variant: decrypt_with_half (paillier.cpp:363-369), finish_split_encrypt
+// (paillier.cpp:402-414).  Element i: c / p2 values of c_limbs / p_limbs words.
+void pcref_decrypt_with_half(void* h, const uint32_t* c, uint32_t c_limbs, const uint32_t* p2, uint32_t p_limbs,
+                             size_t count, uint32_t* m, uint32_t m_limbs, int32_t* st) {
+  RefKey* k = (RefKey*)h;
+  for (size_t i = 0; i < count; i++) {
+    try {
+      Ciphertext ct{from_limbs32(c + i * c_limbs, c_limbs), 0};
+      BigNat mi = k->ph->decrypt_with_half(ct, from_limbs32(p2 + i * p_limbs, p_limbs));
+      to_limbs32(mi, m + i * m_limbs, m_limbs);
+      if (st) st[i] = ST_OK;
+    } catch (const std::exception& e) {
+      std::memset(m + i * m_limbs, 0, m_limbs * 4);
+      if (st) st[i] = classify(e);
+    }
+  }
+}
+
+void pcref_finish_split_encrypt(void* h, const uint32_t* m, uint32_t m_limbs, const uint32_t* g, uint32_t g_limbs,
+                                const uint32_t* r, uint32_t r_limbs, size_t count, uint32_t* c, uint32_t c_limbs,
+                                int32_t* st) {
+  RefKey* k = (RefKey*)h;
+  for (size_t i = 0; i < count; i++) {
+    try {
+      Ciphertext ct = k->ph->finish_split_encrypt(from_limbs32(m + i * m_limbs, m_limbs),
+                                                  from_limbs32(g + i * g_limbs, g_limbs),
+                                                  from_limbs32(r + i * r_limbs, r_limbs));
+      to_limbs32(ct.value, c + i * c_limbs, c_limbs);
+      if (st) st[i] = ST_OK;
+    } catch (const std::exception& e) {
+      std::memset(c + i * c_limbs, 0, c_limbs * 4);
+      if (st) st[i] = classify(e);
+    }
+  }
+}
+
 // ---- homomorphic operations ------------------------------------------------------------------
 // hom_add (paillier.cpp:428-432) with plain_bits in/out; status ST_OVERFLOW when the guard trips.
 void pcref_hom_add(void* h, const uint32_t* a, const uint32_t* b, const uint32_t* a_bits,

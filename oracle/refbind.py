@@ -26,6 +26,10 @@ _SIGS = {
     "pcref_encrypt": (None, [_vp, C.c_int, _u32p, C.c_uint32, _u32p, C.c_uint32, C.c_size_t, _u32p, C.c_uint32,
                              _i32p, C.c_int]),
     "pcref_decrypt": (None, [_vp, C.c_int, _u32p, C.c_uint32, C.c_size_t, _u32p, C.c_uint32, _i32p, C.c_int]),
+    "pcref_decrypt_with_half": (None, [_vp, _u32p, C.c_uint32, _u32p, C.c_uint32, C.c_size_t, _u32p, C.c_uint32,
+                                       _i32p]),
+    "pcref_finish_split_encrypt": (None, [_vp, _u32p, C.c_uint32, _u32p, C.c_uint32, _u32p, C.c_uint32, C.c_size_t,
+                                          _u32p, C.c_uint32, _i32p]),
     "pcref_hom_add": (None, [_vp, _u32p, _u32p, _u32p, _u32p, C.c_size_t, C.c_uint32, _u32p, _u32p, _i32p]),
     "pcref_hom_scalar_mul": (None, [_vp, _u64p, _u32p, _u32p, C.c_size_t, C.c_uint32, _u32p, _u32p, _i32p]),
     "pcref_hom_matvec": (C.c_int, [_vp, _u32p, _u32p, _u64p, _u32p, _u32p, C.c_size_t, C.c_size_t, C.c_uint32,
@@ -139,6 +143,23 @@ class RefKey:
         st = np.zeros(n, np.int32)
         lib().pcref_decrypt(self.h, 1 if crt else 0, a(c), c.shape[1], n, a(m), self.L, a(st), threads)
         return m, st
+
+    def decrypt_with_half(self, c: np.ndarray, p2: np.ndarray):
+        c, p2 = np.ascontiguousarray(c, np.uint32), np.ascontiguousarray(p2, np.uint32)
+        n = c.shape[0]
+        m = np.zeros((n, self.L), np.uint32)
+        st = np.zeros(n, np.int32)
+        lib().pcref_decrypt_with_half(self.h, a(c), c.shape[1], a(p2), p2.shape[1], n, a(m), self.L, a(st))
+        return m, st
+
+    def finish_split_encrypt(self, m: np.ndarray, g: np.ndarray, r: np.ndarray):
+        m, g, r = (np.ascontiguousarray(v, np.uint32) for v in (m, g, r))
+        n = m.shape[0]
+        c = np.zeros((n, 2 * self.L), np.uint32)
+        st = np.zeros(n, np.int32)
+        lib().pcref_finish_split_encrypt(self.h, a(m), m.shape[1], a(g), g.shape[1], a(r), r.shape[1], n, a(c),
+                                         2 * self.L, a(st))
+        return c, st
 
     def __del__(self):
         try:

@@ -234,6 +234,8 @@ struct pcb_ctx {
   uint8_t* d_sched = nullptr;  // all exponent op streams, concatenated
   int off_enc_p = 0, len_enc_p = 0, off_enc_q = 0, len_enc_q = 0;
   int off_dec_p = 0, len_dec_p = 0, off_dec_q = 0, len_dec_q = 0;
+  int off_epsq = 0, len_epsq = 0, off_one = 0, len_one = 0;  // eps mod phi(q^2); e = 1
+  std::vector<uint8_t> half_blob;  // CrtDecConsts with h_p = q^-1 mu mod p, h_q = p^-1 mu mod q
   int off_pub = 0, len_pub = 0;  // exponent n at n^2 (direct encryption)
   uint32_t* d_n = nullptr;       // n (L limbs), n^2 (2L limbs) for the argument checks
   uint32_t* d_n2 = nullptr;
@@ -348,6 +350,27 @@ void build_dec(pcb_ctx* x) {
   x->q.to_limbs(k.q, H);
   x->n2.to_limbs(k.n2, 2 * S);
   x->dec_blob.assign(reinterpret_cast<uint8_t*>(&k), reinterpret_cast<uint8_t*>(&k) + sizeof(k));
+}
+
+// decrypt_with_half constants: dec_finish<S> on (x mod p^2, x mod q^2) of x = c^eps mod n^2 yields
+// L(x) mu mod n when h_p = q^-1 mu mod p and h_q = p^-1 mu mod q (L(x) = L_p(x_p) q^-1 mod p, ...).
+template <int S>
+void build_half(pcb_ctx* x) {
+  constexpr int H = S / 2;
+  CrtDecConsts<S> k;
+  std::memcpy(&k, x->dec_blob.data(), sizeof(k));
+  const HBN RH = HBN(1) << (32 * H);
+  const HBN eps = lcm(x->p - HBN(1), x->q - HBN(1));
+  HBN mu;
+  if (!mod_inverse(mod(eps, x->n), x->n, mu)) throw std::invalid_argument("degenerate key (mu)");  // paillier.cpp:78
+  for (int side = 0; side < 2; side++) {
+    const HBN& pr = side ? x->q : x->p;
+    const HBN& ot = side ? x->p : x->q;
+    HBN inv;
+    if (!mod_inverse(mod(ot, pr), pr, inv)) throw std::invalid_argument("p and q share a factor");
+    mod(mod(inv * mu, pr) * RH, pr).to_limbs(side ? k.hq : k.hp, H);
+  }
+  x->half_blob.assign(reinterpret_cast<uint8_t*>(&k), reinterpret_cast<uint8_t*>(&k) + sizeof(k));
 }
 
 pcb_status set_device(const pcb_ctx* x) { return cuda_check(cudaSetDevice(x->device)); }
@@ -485,6 +508,7 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
         case 64: {
           build_enc<64>(x.get());
           build_dec<64>(x.get());
+          build_half<64>(x.get());
           // RNS / tensor-core core for the CRT halves (default; PCB_RNS=0 selects the carry-chain
           // core).  Falls back to the carry core if the bases cannot be built for this key.
           const char* ev = getenv("PCB_RNS");
@@ -495,6 +519,7 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
         case 96: {
           build_enc<96>(x.get());
           build_dec<96>(x.get());
+          build_half<96>(x.get());
           // the CRT halves run on the radix-2^28 core (28 x 112 limbs, 2 lanes per residue)
           const HBN R = HBN(1) << (28 * 112);
           x->rp2 = r28_mod(p2, 28, 112);
@@ -521,6 +546,9 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
       add(mod(x->n, q2 - x->q), &x->off_enc_q, &x->len_enc_q);
       add(x->p - HBN(1), &x->off_dec_p, &x->len_dec_p);
       add(x->q - HBN(1), &x->off_dec_q, &x->len_dec_q);
+      const HBN eps = lcm(x->p - HBN(1), x->q - HBN(1));
+      add(mod(eps, q2 - x->q), &x->off_epsq, &x->len_epsq);  // decrypt_with_half's q side (paillier.cpp:366)
+      add(HBN(1), &x->off_one, &x->len_one);                 // plain reduction mod p^2
     }
     add(x->n, &x->off_pub, &x->len_pub);
     if (cudaSetDevice(device) != cudaSuccess) return PCB_E_CUDA;
@@ -1103,6 +1131,125 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
     else
       x->pow_full += (uint64_t)count;
   }
+  return e;
+}
+
+// ---- collaborative variant (paper Alg. 3) ---------------------------------------
+pcb_status pcb_decrypt_with_half(pcb_ctx* x, const uint32_t* c, const uint32_t* p2_power, uint32_t pw_limbs,
+                                 size_t count, uint32_t* m, int32_t* status, pcb_stream stream) {
+  if (!x || (count && (!c || !p2_power || !m)) || pw_limbs == 0 || pw_limbs > 2 * x->L) return PCB_E_SHAPE;
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (!x->use_rnsx) return PCB_E_UNSUPPORTED;  // 2048 / 3072-bit keys
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = x->S, L2 = 2 * (int)x->L;
+  Staged sc, sp, sm, ss;
+  uint32_t *pw = nullptr, *yp = nullptr, *yq = nullptr;
+  int32_t* stv = nullptr;
+  pcb_status e = stage_in(c, count * L2 * 4, st, &sc);
+  if (!e) e = stage_in(p2_power, count * pw_limbs * 4, st, &sp);
+  if (!e) e = stage_out(m, count * x->L * 4, st, &sm);
+  if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+  stv = (int32_t*)ss.dev;
+  if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = scratch_alloc(count * L2 * 4, (void**)&pw, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yp, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yq, st);
+  if (!e) e = launch_dec_prep((const uint32_t*)sc.dev, x->d_n2, (int)x->L, stv, count, st);  // c < n^2 (paillier.cpp:365)
+  if (!e) e = cuda_check(cudaMemset2DAsync(pw, L2 * 4, 0, L2 * 4, count, st));
+  if (!e)
+    e = cuda_check(cudaMemcpy2DAsync(pw, L2 * 4, sp.dev, pw_limbs * 4, pw_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
+  const double mm = 2.0 * S * S + S;
+  // p side: p2_power mod p^2 (reference: mod(p2_power, crt_.p2)); q side: c^(eps mod phi(q^2)) mod q^2
+  if (!e)
+    e = launch_rnsx(x->rx_p, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, pw, L2, nullptr, 0, count, yp, st, mm);
+  if (!e)
+    e = launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_epsq, x->len_epsq, kTab, (const uint32_t*)sc.dev, L2, nullptr,
+                    0, count, yq, st, ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm);
+  if (!e && S == 64)
+    e = launch_dec_finish<64>(*reinterpret_cast<const CrtDecConsts<64>*>(x->half_blob.data()), yp, yq, stv,
+                              (uint32_t*)sm.dev, (int)x->L, count, st);
+  if (!e && S == 96)
+    e = launch_dec_finish<96>(*reinterpret_cast<const CrtDecConsts<96>*>(x->half_blob.data()), yp, yq, stv,
+                              (uint32_t*)sm.dev, (int)x->L, count, st);
+  if (!e) e = unstage_out(m, &sm, st);
+  if (!e) e = unstage_out(status, &ss, st);
+  scratch_free(pw, st);
+  scratch_free(yp, st);
+  scratch_free(yq, st);
+  if (!ss.dev) scratch_free(stv, st);
+  const bool any_host = sc.host || sp.host || sm.host || ss.host;
+  unstage(&sc, st);
+  unstage(&sp, st);
+  unstage(&sm, st);
+  unstage(&ss, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!e) x->pow_half += (uint64_t)count;  // one half_pow per element (paillier.cpp:366)
+  return e;
+}
+
+pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* p2_g_power,
+                                    uint32_t pg_limbs, const uint32_t* r, size_t count, uint32_t* c, int32_t* status,
+                                    pcb_stream stream) {
+  if (!x || (count && (!m || !p2_g_power || !r || !c)) || pg_limbs == 0 || pg_limbs > 2 * x->L) return PCB_E_SHAPE;
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (!x->use_rnsx) return PCB_E_UNSUPPORTED;
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = x->S, L2 = 2 * (int)x->L;
+  Staged sm, sg, sr, sc, ss;
+  uint32_t *gw = nullptr, *gp = nullptr, *yp = nullptr, *yq = nullptr;
+  int32_t* stv = nullptr;
+  pcb_status e = stage_in(m, count * m_limbs * 4, st, &sm);
+  if (!e) e = stage_in(p2_g_power, count * pg_limbs * 4, st, &sg);
+  if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
+  if (!e) e = stage_out(c, count * L2 * 4, st, &sc);
+  if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+  stv = (int32_t*)ss.dev;
+  if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = scratch_alloc(count * L2 * 4, (void**)&gw, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&gp, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yp, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yq, st);
+  // argument checks m < n, r in [1, n) (paillier.cpp:409-412)
+  if (!e)
+    e = launch_enc_prep((const uint32_t*)sm.dev, (int)m_limbs, nullptr, 0, 0, 0, 0, nullptr, 0, nullptr, nullptr,
+                        (const uint32_t*)sr.dev, x->d_n, (int)x->L, stv, count, st);
+  if (!e) e = cuda_check(cudaMemset2DAsync(gw, L2 * 4, 0, L2 * 4, count, st));
+  if (!e)
+    e = cuda_check(cudaMemcpy2DAsync(gw, L2 * 4, sg.dev, pg_limbs * 4, pg_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
+  const double mm = 2.0 * S * S + S, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm;
+  // cp = (p2_g_power mod p^2) r^(n mod phi(p^2)) mod p^2;  cq = (1 + m n) r^(n mod phi(q^2)) mod q^2
+  if (!e) e = launch_rnsx(x->rx_p, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, gw, L2, nullptr, 0, count, gp, st, mm);
+  if (!e)
+    e = launch_rnsx(x->rx_p, kRxEncG, x->d_sched + x->off_enc_p, x->len_enc_p, kTab, (const uint32_t*)sr.dev,
+                    (int)x->L, gp, S, count, yp, st, alg);
+  if (!e)
+    e = launch_rnsx(x->rx_q, kRxEnc, x->d_sched + x->off_enc_q, x->len_enc_q, kTab, (const uint32_t*)sr.dev,
+                    (int)x->L, (const uint32_t*)sm.dev, (int)m_limbs, count, yq, st, alg);
+  if (!e && S == 64)
+    e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv,
+                          (uint32_t*)sc.dev, (int)x->L, count, st);
+  if (!e && S == 96)
+    e = launch_garner<96>(*reinterpret_cast<const CrtEncConsts<96>*>(x->enc_blob.data()), yp, yq, stv,
+                          (uint32_t*)sc.dev, (int)x->L, count, st);
+  if (!e) e = unstage_out(c, &sc, st);
+  if (!e) e = unstage_out(status, &ss, st);
+  scratch_free(gw, st);
+  scratch_free(gp, st);
+  scratch_free(yp, st);
+  scratch_free(yq, st);
+  if (!ss.dev) scratch_free(stv, st);
+  const bool any_host = sm.host || sg.host || sr.host || sc.host || ss.host;
+  unstage(&sm, st);
+  unstage(&sg, st);
+  unstage(&sr, st);
+  unstage(&sc, st);
+  unstage(&ss, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!e) x->pow_half += 2 * (uint64_t)count;  // two half_pows (paillier.cpp:412-413)
   return e;
 }
 

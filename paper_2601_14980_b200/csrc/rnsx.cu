@@ -463,9 +463,9 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
       const uint32_t* src = &zero;
       int nw = 1;
       int cst = kRxR2N;
-      if (P.mode == kRxEnc && first) {  // m n
+      if ((P.mode == kRxEnc || P.mode == kRxEncG) && first) {  // m n  (EncG: g, plain, via M mod N)
         if (live) { src = P.m + (size_t)el * P.m_words; nw = P.m_words; }
-        cst = kRxNM;
+        cst = P.mode == kRxEnc ? kRxNM : kRxOneM;
       } else if (P.mode == kRxDec && first) {  // c_hi 2^(32 S) M
         if (live) { src = P.x + (size_t)el * P.x_words + P.S; nw = P.x_words - P.S; }
         cst = kRxCR2N;
@@ -487,7 +487,7 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
         yb = tabp(op, tt);
         yvs = tab_vs;
       }
-    } else if (P.mode == kRxEnc) {
+    } else if (P.mode == kRxEnc || P.mode == kRxEncG) {
       yb = tabp(park, tt);
       yvs = tab_vs;
     } else {

@@ -13,7 +13,7 @@ namespace pcb {
 
 class HBN;
 
-enum : int { kRxEnc = 0, kRxDec = 1, kRxPow = 2, kRxProg = 3 };
+enum : int { kRxEnc = 0, kRxDec = 1, kRxPow = 2, kRxProg = 3, kRxEncG = 4 };  // EncG: g r^e, g < N given
 constexpr int kRxReplicas = 16;  // copies of the stream image (spreads the L2 reads of 148 SMs)
 enum : int { kRxOne = 0, kRxR2N = 1, kRxCR2N = 2, kRxNM = 3, kRxOneM = 4, kRxNumVec = 5 };
 

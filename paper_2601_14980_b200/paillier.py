@@ -308,6 +308,41 @@ class Paillier:
     def decrypt_vec(self, cs, use_crt: bool) -> list[int]:
         return self._dec_list(cs, use_crt)
 
+    # ---- collaborative variant (paper Alg. 3, paillier.cpp:363-426; protocol.cpp:11-18) ---------
+    def decrypt_with_half(self, c, p2_power: int) -> int:
+        """Paillier::decrypt_with_half: the p^2 side comes from an edge (delegated_power)."""
+        self._need_prv()
+        v = c.value if isinstance(c, Ciphertext) else int(c)
+        if v.bit_length() > 64 * self.L:
+            raise ValueError("ciphertext not below n^2")
+        W = 2 * self.L
+        p2 = int(p2_power) % (self.n * self.n)  # the GPU path reduces mod p^2; any representative < n^2
+        Cl, Pl = L.ints_to_limbs([v], W), L.ints_to_limbs([p2], W)
+        m = np.zeros((1, self.L), np.uint32)
+        st = np.zeros(1, np.int32)
+        _raise_for(L.lib().pcb_decrypt_with_half(self._ctx, L.ptr(Cl), L.ptr(Pl), W, 1, L.ptr(m), L.ptr(st), None),
+                   "decrypt_with_half")
+        _raise_for(int(st[0]), "element 0")
+        return L.limbs_to_int(m[0])
+
+    def finish_split_encrypt(self, m: int, p2_g_power: int, r: int) -> Ciphertext:
+        """Paillier::finish_split_encrypt: the p^2-side g-power comes from an edge."""
+        self._need_prv()
+        W = 2 * self.L
+        M, R = L.ints_to_limbs([m], self.L), L.ints_to_limbs([r], self.L)
+        G = L.ints_to_limbs([int(p2_g_power) % (self.n * self.n)], W)
+        c = np.zeros((1, W), np.uint32)
+        st = np.zeros(1, np.int32)
+        _raise_for(L.lib().pcb_finish_split_encrypt(self._ctx, L.ptr(M), self.L, L.ptr(G), W, L.ptr(R), 1, L.ptr(c),
+                                                    L.ptr(st), None), "finish_split_encrypt")
+        _raise_for(int(st[0]), "element 0")
+        return Ciphertext(L.limbs_to_int(c[0]), int(m).bit_length())
+
+    @staticmethod
+    def obfuscate_exponent(value: int, n_eps: int, mask: int) -> int:
+        """protocol.cpp:11-13: value + mask * n_eps (host-side integer)."""
+        return int(value) + (int(mask) & MASK64) * int(n_eps)
+
     # ---- homomorphic operations (paillier.cpp:428-493) ----------------------------------------
     def _nbits(self) -> int:
         return self.n.bit_length()

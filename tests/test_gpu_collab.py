@@ -1,0 +1,98 @@
+"""Collaborative variant (paper Alg. 3) through the C ABI on the GPU, against the
+compiled reference (Paillier::decrypt_with_half / finish_split_encrypt, paillier.cpp:363-414) and
+the restated edge-side worker delegated_power (protocol.cpp:15-18: base^(obf mod phi(p^2)) mod p^2
+with obf = obfuscate_exponent(value, n eps, mask), protocol.cpp:11-13)."""
+import random
+
+import numpy as np
+import pytest
+
+import refbind as R_
+from conftest import golden
+from paper_2601_14980_b200 import _lib as L
+from paper_2601_14980_b200 import paillier as P
+
+pytestmark = pytest.mark.gpu
+
+
+def _lcm(a, b):
+    import math
+
+    return a * b // math.gcd(a, b)
+
+
+@pytest.fixture(scope="module")
+def key2048():
+    k = golden("keys.json")[2]
+    return P.KeyPair(int(k["n"], 16), int(k["p"], 16), int(k["q"], 16), k["bits"]), k["seed"]
+
+
+def test_finish_split_encrypt_and_decrypt_with_half(key2048):
+    kp, seed = key2048
+    ph = P.Paillier(kp)
+    n, p, q = kp.n, kp.p, kp.q
+    n2, p2 = n * n, p * p
+    eps = _lcm(p - 1, q - 1)
+    phi_p2 = p2 - p
+    g = n + 1
+    rnd = random.Random(17)
+    count = 300  # > 2 tiles: every CTA path
+    ms = [rnd.getrandbits(50) for _ in range(count - 2)] + [0, n - 1]
+    rs = [rnd.randrange(1, n) for _ in range(count)]
+    masks = [rnd.getrandbits(64) for _ in range(count)]
+    # edge: delegated g-powers of the obfuscated plaintexts (protocol.cpp:248-249)
+    gp = [pow(g % p2, (m + k * n * eps) % phi_p2, p2) for m, k in zip(ms, masks)]
+    W = 2 * ph.L
+    M, R, G = L.ints_to_limbs(ms, ph.L), L.ints_to_limbs(rs, ph.L), L.ints_to_limbs(gp, W)
+    c = np.zeros((count, W), np.uint32)
+    st = np.zeros(count, np.int32)
+    rc = L.lib().pcb_finish_split_encrypt(ph._ctx, L.ptr(M), ph.L, L.ptr(G), W, L.ptr(R), count, L.ptr(c),
+                                          L.ptr(st), None)
+    assert rc == 0 and (st == 0).all()
+    # == the basic CRT encryption (the obfuscation cancels: g^(n eps) = 1 mod p^2)
+    cb = ph.encrypt_batch(M, R, use_crt=True)
+    assert (c == cb).all()
+    # edge: delegated decryption power of each ciphertext (protocol.cpp:226, 492)
+    cs = L.limbs_to_ints(c)
+    px = [pow(cv % p2, (eps + k * n * eps) % phi_p2, p2) for cv, k in zip(cs, masks)]
+    PX = L.ints_to_limbs(px, W)
+    m = np.zeros((count, ph.L), np.uint32)
+    st[:] = 0
+    rc = L.lib().pcb_decrypt_with_half(ph._ctx, L.ptr(c), L.ptr(PX), W, count, L.ptr(m), L.ptr(st), None)
+    assert rc == 0 and (st == 0).all()
+    assert L.limbs_to_ints(m) == ms
+    # the compiled reference gives the same ciphertexts / plaintexts
+    if R_.available():
+        ref = R_.RefKey.keygen(seed, kp.key_bits)
+        cref, sref = ref.finish_split_encrypt(M, G, R)
+        assert (sref == 0).all() and (cref == c).all()
+        mref, sref = ref.decrypt_with_half(c, PX)
+        assert (sref == 0).all() and (mref == m).all()
+    # single-value mirrors and the obfuscation helper
+    ob = P.Paillier.obfuscate_exponent(ms[0], n * eps, masks[0])
+    assert ob == ms[0] + masks[0] * n * eps
+    ct = ph.finish_split_encrypt(ms[0], pow(g % p2, ob % phi_p2, p2), rs[0])
+    assert ct.value == cs[0]
+    assert ph.decrypt_with_half(ct, px[0]) == ms[0]
+
+
+def test_collab_error_statuses(key2048):
+    kp, _ = key2048
+    ph = P.Paillier(kp)
+    W = 2 * ph.L
+    n2 = kp.n * kp.n
+    # c >= n^2 -> invalid_argument (paillier.cpp:365); non-unit p-half -> runtime_error (L check)
+    C_ = L.ints_to_limbs([n2 + 5, 5], W)  # n^2 + 5 is out of range; 5 with a zero p-half is a non-unit
+    PX = L.ints_to_limbs([1, 0], W)  # p-half 0: x = CRT(0, ...) not = 1 mod p
+    m = np.zeros((2, ph.L), np.uint32)
+    st = np.zeros(2, np.int32)
+    assert L.lib().pcb_decrypt_with_half(ph._ctx, L.ptr(C_), L.ptr(PX), W, 2, L.ptr(m), L.ptr(st), None) == 0
+    assert st[0] == L.PCB_E_CIPHER_RANGE and st[1] == L.PCB_E_NOT_UNIT
+    # m >= n and r = 0 -> invalid_argument (paillier.cpp:409-411)
+    M = L.ints_to_limbs([kp.n, 3], ph.L)
+    R = L.ints_to_limbs([5, 0], ph.L)
+    G = L.ints_to_limbs([1, 1], W)
+    c = np.zeros((2, W), np.uint32)
+    assert L.lib().pcb_finish_split_encrypt(ph._ctx, L.ptr(M), ph.L, L.ptr(G), W, L.ptr(R), 2, L.ptr(c), L.ptr(st),
+                                            None) == 0
+    assert st[0] == L.PCB_E_PLAINTEXT_RANGE and st[1] == L.PCB_E_RANDOMNESS_RANGE and not c.any()
