@@ -126,6 +126,17 @@ pcb_status pcb_decrypt(pcb_ctx* ctx, const uint32_t* c, size_t count, uint32_t* 
 pcb_status pcb_decrypt_with_half(pcb_ctx* ctx, const uint32_t* c, const uint32_t* p2_power, uint32_t pw_limbs,
                                  size_t count, uint32_t* m, int32_t* status, pcb_stream stream);
 
+/* An edge's CrtShare {p^2, phi(p^2)} (paillier.hpp:64-66) on the device: no other key material. */
+typedef struct pcb_share pcb_share;
+pcb_status pcb_share_create(pcb_share** share, int device, const uint32_t* p2, uint32_t p2_limbs,
+                            const uint32_t* phi_p2, uint32_t phi_limbs);
+void pcb_share_destroy(pcb_share* share);
+/* out_i = (base_i mod p^2)^(obf_i mod phi(p^2)) mod p^2 — delegated_power (protocol.cpp:15-18), with
+ * per-element exponents (e.g. obfuscate_exponent(value, n eps, mask), protocol.cpp:11-13).
+ * base: count x base_limbs (<= 2 x p^2 words), obf: count x obf_limbs, out: count x (p^2 words). */
+pcb_status pcb_delegated_power(pcb_share* share, const uint32_t* base, uint32_t base_limbs, const uint32_t* obf,
+                               uint32_t obf_limbs, size_t count, uint32_t* out, pcb_stream stream);
+
 /* c_i = CRT((p2_g_power_i mod p^2) r_i^(n mod phi(p^2)) mod p^2, (1 + m_i n) r_i^(n mod phi(q^2)) mod q^2)
  * — Paillier::finish_split_encrypt (paillier.cpp:402-414).  Statuses as pcb_encrypt. */
 pcb_status pcb_finish_split_encrypt(pcb_ctx* ctx, const uint32_t* m, uint32_t m_limbs, const uint32_t* p2_g_power,

@@ -67,6 +67,9 @@ SIGNATURES = {
     "pcb_encrypt_rn": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp, _vp]),
     "pcb_decrypt": (C.c_int, [_vp, _vp, C.c_size_t, _vp, C.c_int, _vp, _vp]),
     "pcb_decrypt_with_half": (C.c_int, [_vp, _vp, _vp, C.c_uint32, C.c_size_t, _vp, _vp, _vp]),
+    "pcb_share_create": (C.c_int, [C.POINTER(_vp), C.c_int, _vp, C.c_uint32, _vp, C.c_uint32]),
+    "pcb_share_destroy": (None, [_vp]),
+    "pcb_delegated_power": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_uint32, C.c_size_t, _vp, _vp]),
     "pcb_finish_split_encrypt": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp, _vp]),
     "pcb_hom_add": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
     "pcb_hom_scalar_mul": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),

@@ -1135,6 +1135,101 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
 }
 
 // ---- collaborative variant (paper Alg. 3) ---------------------------------------
+}  // extern "C"
+struct pcb_share {  // an edge's CrtShare (paillier.hpp:64-66): p^2 and phi(p^2) only
+  int device = 0;
+  HBN p2, phi;
+  int S = 0;
+  RnsXModulus md;
+};
+extern "C" {
+
+pcb_status pcb_share_create(pcb_share** out, int device, const uint32_t* p2, uint32_t p2_limbs, const uint32_t* phi_p2,
+                            uint32_t phi_limbs) {
+  if (!out || !p2 || !phi_p2 || !p2_limbs || !phi_limbs) return PCB_E_SHAPE;
+  *out = nullptr;
+  std::unique_ptr<pcb_share> sh(new (std::nothrow) pcb_share);
+  if (!sh) return PCB_E_ALLOC;
+  try {
+    sh->device = device;
+    sh->p2 = HBN::from_limbs(p2, p2_limbs);
+    sh->phi = HBN::from_limbs(phi_p2, phi_limbs);
+    if (!sh->p2.is_odd() || sh->phi.is_zero()) return PCB_E_SHAPE;
+    sh->S = (int)((sh->p2.bit_length() + 31) / 32);
+    int K = 0;
+    if (!rnsx_shape(32 * sh->S, &K) || sh->p2.bit_length() <= 1024) return PCB_E_UNSUPPORTED;  // 2048/3072-bit keys
+    if (cudaSetDevice(device) != cudaSuccess) return PCB_E_CUDA;
+    if (!rnsx_build(sh->p2, sh->p2, sh->S, K, &sh->md)) return PCB_E_UNSUPPORTED;
+  } catch (const std::bad_alloc&) {
+    return PCB_E_ALLOC;
+  } catch (...) {
+    return PCB_E_SHAPE;
+  }
+  *out = sh.release();
+  return PCB_OK;
+}
+
+void pcb_share_destroy(pcb_share* sh) {
+  if (!sh) return;
+  cudaSetDevice(sh->device);
+  rnsx_free(&sh->md);
+  delete sh;
+}
+
+// delegated_power (protocol.cpp:15-18): out_i = (base_i mod p^2)^(obf_i mod phi(p^2)) mod p^2.
+// The exponent reduction is host work (big-integer mod per element); the powers run on the RNS
+// core with a per-element 4-bit window table.
+pcb_status pcb_delegated_power(pcb_share* sh, const uint32_t* base, uint32_t base_limbs, const uint32_t* obf,
+                               uint32_t obf_limbs, size_t count, uint32_t* out, pcb_stream stream) {
+  if (!sh || (count && (!base || !obf || !out)) || base_limbs == 0 || base_limbs > (uint32_t)(2 * sh->S) || !obf_limbs)
+    return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  if (cudaSetDevice(sh->device) != cudaSuccess) return PCB_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = sh->S, W = 2 * S;
+  // exponents: obf mod phi(p^2) (host), S words each
+  std::vector<uint32_t> ob((size_t)count * obf_limbs), ex((size_t)count * S, 0);
+  if (is_device_ptr(obf)) {
+    if (cudaMemcpyAsync(ob.data(), obf, ob.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return PCB_E_CUDA;
+  } else {
+    std::memcpy(ob.data(), obf, ob.size() * 4);
+  }
+  size_t maxbits = 0;
+  try {
+    for (size_t i = 0; i < count; i++) {
+      const HBN e = mod(HBN::from_limbs(ob.data() + i * obf_limbs, obf_limbs), sh->phi);
+      maxbits = std::max(maxbits, e.bit_length());
+      e.to_limbs(ex.data() + i * S, S);
+    }
+  } catch (...) {
+    return PCB_E_SHAPE;
+  }
+  const int nwin = maxbits ? (int)((maxbits + 3) / 4) : 1;
+  Staged sb, so;
+  uint32_t *bw = nullptr, *ed = nullptr;
+  pcb_status e = stage_in(base, count * base_limbs * 4, st, &sb);
+  if (!e) e = stage_out(out, count * S * 4, st, &so);
+  if (!e) e = scratch_alloc(count * W * 4, (void**)&bw, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&ed, st);
+  if (!e) e = cuda_check(cudaMemset2DAsync(bw, W * 4, 0, W * 4, count, st));
+  if (!e) e = cuda_check(cudaMemcpy2DAsync(bw, W * 4, sb.dev, base_limbs * 4, base_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
+  if (!e) e = cuda_check(cudaMemcpyAsync(ed, ex.data(), ex.size() * 4, cudaMemcpyHostToDevice, st));
+  const double mm = 2.0 * S * S + S;
+  if (!e) e = launch_rnsx(sh->md, kRxPowVar, nullptr, nwin, 16, bw, W, ed, S, count, (uint32_t*)so.dev, st,
+                          (4.0 * nwin + nwin + 14.0) * mm);
+  if (!e) e = unstage_out(out, &so, st);
+  scratch_free(bw, st);
+  scratch_free(ed, st);
+  const bool any_host = sb.host || so.host;
+  unstage(&sb, st);
+  unstage(&so, st);
+  (void)any_host;
+  if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;  // ex (host) must outlive its copy
+  return e;
+}
+
 pcb_status pcb_decrypt_with_half(pcb_ctx* x, const uint32_t* c, const uint32_t* p2_power, uint32_t pw_limbs,
                                  size_t count, uint32_t* m, int32_t* status, pcb_stream stream) {
   if (!x || (count && (!c || !p2_power || !m)) || pw_limbs == 0 || pw_limbs > 2 * x->L) return PCB_E_SHAPE;

@@ -453,11 +453,33 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
   // ---- exponentiation programs (Enc / Dec / Pow): per-step operand selection and epilogue ------
   // `tt` selects the per-thread window table of tile slot tt (two tiles in flight when C::NT == 2)
   auto tabp = [&](int ent, int tt) { return tab_ptr(ent * C::NT + tt); };
+  // PowVar: 4-bit digit w of this element's exponent (dead lanes: 0)
+  auto digit = [&](int el, bool live, int w) -> int {
+    if (!live) return 0;
+    return (int)((P.m[(size_t)el * P.m_words + (w >> 3)] >> (4 * (w & 7))) & 15u);
+  };
   auto prep = [&](int s, uint32_t (&XB)[RPT], uint32_t (&XQ)[RPT], int tt, int el, bool live, bool& sq,
                   const uint32_t*& yb, int& yvs) {
     sq = false;
     yb = nullptr;
     yvs = 4;
+    if (P.mode == kRxPowVar && s >= npre) {  // table T_s = T_(s-1) x (s < 16), then 4-bit windows
+      if (s < 16) {
+        yb = tabp(1, tt);
+        yvs = tab_vs;
+      } else if (s < s_fin) {
+        const int k = s - 16;
+        if (k % 5 < 4) {
+          sq = true;
+        } else {
+          yb = tabp(digit(el, live, P.nops - 2 - k / 5), tt);
+          yvs = tab_vs;
+        }
+      } else {
+        yb = cv_ptr(kRxOne);
+      }
+      return;
+    }
     if (s < npre) {
       const bool first = npre == 2 && s == 0;
       const uint32_t* src = &zero;
@@ -466,11 +488,14 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
       if ((P.mode == kRxEnc || P.mode == kRxEncG) && first) {  // m n  (EncG: g, plain, via M mod N)
         if (live) { src = P.m + (size_t)el * P.m_words; nw = P.m_words; }
         cst = P.mode == kRxEnc ? kRxNM : kRxOneM;
-      } else if (P.mode == kRxDec && first) {  // c_hi 2^(32 S) M
+      } else if ((P.mode == kRxDec || P.mode == kRxPowVar) && first) {  // c_hi 2^(32 S) M
         if (live) { src = P.x + (size_t)el * P.x_words + P.S; nw = P.x_words - P.S; }
         cst = kRxCR2N;
       } else {  // r M / c_lo M / x M
-        if (live) { src = P.x + (size_t)el * P.x_words; nw = P.mode == kRxDec ? P.S : P.x_words; }
+        if (live) {
+          src = P.x + (size_t)el * P.x_words;
+          nw = (P.mode == kRxDec || P.mode == kRxPowVar) ? P.S : P.x_words;
+        }
       }
       conv_in<C>(XB, XQ, src, nw, T);
       yb = cv_ptr(cst);
@@ -495,6 +520,21 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
     }
   };
   auto post = [&](int s, uint32_t (&XB)[RPT], uint32_t (&XQ)[RPT], int tt, int el, bool live) {
+    if (P.mode == kRxPowVar && s < s_fin) {
+      if (s == 0) {
+        vec_op(tabp(park, tt), tab_vs, XB, XQ, 2);
+      } else if (s == 1) {  // x M = c_lo M + c_hi 2^(32S) M: table entry 1; entry 0 = M mod N (the one)
+        vec_op(tabp(park, tt), tab_vs, XB, XQ, 1);
+        vec_op(tabp(1, tt), tab_vs, XB, XQ, 2);
+        uint32_t OB[RPT], OQ[RPT];
+        vec_op(cv_ptr(kRxOneM), 4, OB, OQ, 0);
+        vec_op(tabp(0, tt), tab_vs, OB, OQ, 2);
+      } else if (s < 16) {
+        vec_op(tabp(s, tt), tab_vs, XB, XQ, 2);
+        if (s == 15) vec_op(tabp(digit(el, live, P.nops - 1), tt), tab_vs, XB, XQ, 0);  // top window
+      }
+      return;
+    }
     if (s < npre) {
       const bool first = npre == 2 && s == 0;
       if (first) {
@@ -922,7 +962,9 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
   const uint32_t tm = *tbase;
   // uniform step plan: [pre0] pre1 | x^2 | table (ntab-1) | main (nops-1) | final
   const int npre = P.mode == kRxPow ? 1 : 2;
-  const int s_x2 = npre, s_tab = s_x2 + 1, s_main = s_tab + (P.ntab - 1), s_fin = s_main + (P.nops - 1);
+  const int s_x2 = npre, s_tab = s_x2 + 1, s_main = s_tab + (P.ntab - 1);
+  int s_fin = s_main + (P.nops - 1);
+  if (P.mode == kRxPowVar) s_fin = 16 + 5 * (P.nops - 1);  // 2 pre + 14 table + 5 per window after the top
   const int nsteps = P.mode == kRxProg ? P.prog.nsteps : s_fin + 1;
   const int ntiles = (P.count + C::TILE - 1) / C::TILE;
   // units (tiles, or tile pairs when NT == 2) of this CTA: u = blockIdx.x + k gridDim.x; within a
@@ -1152,7 +1194,8 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
       prof_stop(pm, st, alg_mac32 * (double)count);
       double mps = 0;  // int8 MACs per tile-product: every slice is an M = 128 x N = ncol x K = 32 MMA
       for (int c = 0; c < C::NC; c++) mps += (double)C::TILE * C::ncol(c) * 32 * (C::KS1 + C::KS2);
-      const int nsteps = mode == kRxProg ? prog->nsteps : (mode == kRxPow ? 1 : 2) + ntab + nops;
+      const int nsteps = mode == kRxProg ? prog->nsteps
+                         : mode == kRxPowVar ? 17 + 5 * (nops - 1) : (mode == kRxPow ? 1 : 2) + ntab + nops;
       prof_add_int8(mps * nsteps * (double)(units * C::NT));
     }
     const cudaError_t ce = cudaGetLastError();

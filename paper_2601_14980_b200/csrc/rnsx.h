@@ -13,7 +13,9 @@ namespace pcb {
 
 class HBN;
 
-enum : int { kRxEnc = 0, kRxDec = 1, kRxPow = 2, kRxProg = 3, kRxEncG = 4 };  // EncG: g r^e, g < N given
+enum : int { kRxEnc = 0, kRxDec = 1, kRxPow = 2, kRxProg = 3, kRxEncG = 4, kRxPowVar = 5 };
+// EncG: g r^e with g < N given;  PowVar: x^(e_el) with a per-element exponent (m = exponent words,
+// nops = number of 4-bit windows, ntab = 16): the delegated power of the collaborative variant
 constexpr int kRxReplicas = 16;  // copies of the stream image (spreads the L2 reads of 148 SMs)
 enum : int { kRxOne = 0, kRxR2N = 1, kRxCR2N = 2, kRxNM = 3, kRxOneM = 4, kRxNumVec = 5 };
 

@@ -453,3 +453,48 @@ class Paillier:
         self._bump(bits)
         out = self.aggregate_batch(self._cw(cs))
         return Ciphertext(L.limbs_to_int(out), bits)
+
+
+class CrtShare:
+    """An edge's share of the private key (paillier.hpp:64-66: p^2 and phi(p^2)) on the device."""
+
+    def __init__(self, p2: int, phi_p2: int, device: int = 0):
+        self.p2, self.phi_p2 = int(p2), int(phi_p2)
+        self.S = (self.p2.bit_length() + 31) // 32
+        a = L.int_to_limbs(self.p2, self.S)
+        b = L.int_to_limbs(self.phi_p2, self.S)
+        h = C.c_void_p()
+        _raise_for(L.lib().pcb_share_create(C.byref(h), device, a.ctypes.data_as(L._u32p), self.S,
+                                            b.ctypes.data_as(L._u32p), self.S), "share")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and L is not None and L._lib is not None:
+            L._lib.pcb_share_destroy(h)
+            self._h = None
+
+    def delegated_power_batch(self, base, obf):
+        """base: (count, <= 2S) limbs, obf: (count, k) limbs -> (count, S) limbs of
+        (base mod p^2)^(obf mod phi(p^2)) mod p^2."""
+        base = np.ascontiguousarray(base, np.uint32)
+        obf = np.ascontiguousarray(obf, np.uint32)
+        out = np.zeros((base.shape[0], self.S), np.uint32)
+        _raise_for(L.lib().pcb_delegated_power(self._h, L.ptr(base), base.shape[1], L.ptr(obf), obf.shape[1],
+                                               base.shape[0], L.ptr(out), None), "delegated_power")
+        return out
+
+
+def crt_share(kp: KeyPair, device: int = 0) -> CrtShare:
+    """pcadmm::crt_share (paillier.hpp:95): what the master hands an edge in the collaborative variant."""
+    p2 = kp.p * kp.p
+    return CrtShare(p2, p2 - kp.p, device)
+
+
+def delegated_power(base: int, obf: int, share: CrtShare) -> int:
+    """protocol.cpp:15-18, one value."""
+    W = 2 * share.S
+    out = share.delegated_power_batch(L.ints_to_limbs([int(base) % (1 << (32 * W))], W),
+                                      L.ints_to_limbs([int(obf)], max(1, (int(obf).bit_length() + 31) // 32)))
+    return L.limbs_to_int(out[0])
+

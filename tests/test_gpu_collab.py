@@ -96,3 +96,23 @@ def test_collab_error_statuses(key2048):
     assert L.lib().pcb_finish_split_encrypt(ph._ctx, L.ptr(M), ph.L, L.ptr(G), W, L.ptr(R), 2, L.ptr(c), L.ptr(st),
                                             None) == 0
     assert st[0] == L.PCB_E_PLAINTEXT_RANGE and st[1] == L.PCB_E_RANDOMNESS_RANGE and not c.any()
+
+
+def test_delegated_power_edge_worker(key2048):
+    """The edge side of Alg. 3: per-element exponents on the RNS core, only {p^2, phi(p^2)} known."""
+    kp, _ = key2048
+    share = P.crt_share(kp)
+    p2, phi = kp.p * kp.p, kp.p * kp.p - kp.p
+    n2, eps = kp.n * kp.n, _lcm(kp.p - 1, kp.q - 1)
+    rnd = random.Random(23)
+    count = 260
+    bases = [rnd.randrange(0, n2) for _ in range(count - 4)] + [0, 1, p2, kp.n + 1]
+    obfs = [P.Paillier.obfuscate_exponent(rnd.getrandbits(50), kp.n * eps, rnd.getrandbits(64))
+            for _ in range(count - 3)] + [0, phi, 3 * phi + 5]
+    W = 2 * share.S
+    ow = max(1, max(o.bit_length() for o in obfs) // 32 + 1)
+    out = share.delegated_power_batch(L.ints_to_limbs(bases, W), L.ints_to_limbs(obfs, ow))
+    got = L.limbs_to_ints(out)
+    for i in range(count):
+        assert got[i] == pow(bases[i] % p2, obfs[i] % phi, p2), i
+    assert P.delegated_power(bases[5], obfs[5], share) == got[5]
