@@ -217,6 +217,15 @@ pcb_status pcb_decrypt_update_blocks(pcb_ctx* ctx, size_t nblocks, const uint32_
                                      double z_max, double delta, double kappa, double* x, double* z,
                                      double* v, int32_t* status, pcb_stream stream);
 
+/* pcb_decrypt_update_blocks of the collaborative variant: the p^2 side of every Dec comes from the
+ * edge (p2_power: count x 2L words, delegated_power of c with the obfuscated eps) and the master
+ * finishes with decrypt_with_half (protocol.cpp:490-492).  2048/3072-bit keys. */
+pcb_status pcb_decrypt_update_blocks_half(pcb_ctx* ctx, size_t nblocks, const uint32_t* sizes, const uint32_t* c,
+                                          const uint32_t* p2_power, const uint64_t* rowsum, const uint64_t* q_z,
+                                          const uint64_t* q_nv, double z_min, double z_max, double delta,
+                                          double kappa, double* x, double* z, double* v, int32_t* status,
+                                          pcb_stream stream);
+
 /* ---- generic primitive + measurement ------------------------------------------------------ */
 
 /* y_i = x_i^e mod m for an odd modulus m (m_limbs <= 96) and a batch-uniform exponent e —

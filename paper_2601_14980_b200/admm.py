@@ -58,6 +58,7 @@ class SessionConfig:
     window: int = 6
     seed: int = 1
     over_k: bool = False  # YScaling::full
+    variant: str = "basic"  # "collab": paper Alg. 3, the p^2 side of every Enc/Dec delegated to the edges
 
 
 @dataclass
@@ -243,6 +244,18 @@ class EncryptedSession(ShardedDriver):
         _raise_for(self.lib.pcb_ctx_set_priority(self.master._ctx, 1), "priority")
         _raise_for(self.lib.pcb_ctx_set_priority(self.edge._ctx, 1), "priority")
         _raise_for(self.lib.pcb_ctx_set_priority(self.pre._ctx, 0), "priority")
+        if cfg.variant == "collab":
+            # the edges' CrtShare {p^2, phi(p^2)} (paillier.hpp:64-66); n eps and the masks of
+            # obfuscate_exponent (protocol.cpp:11-13, 335-356): any mask gives the same powers
+            from .paillier import crt_share
+
+            self.share = crt_share(keys, device)
+            import math
+
+            lam = (keys.p - 1) * (keys.q - 1) // math.gcd(keys.p - 1, keys.q - 1)
+            self.n_eps = keys.n * int(lam)
+            self.eps = int(lam)
+            self.mask_rng = Rng(cfg.seed ^ 0x636F6C6C61622121)
 
     def _stream(self):
         import torch
@@ -345,11 +358,50 @@ class EncryptedSession(ShardedDriver):
             _raise_for(self.lib.pcb_sample_r(self.pre._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
                        "sample_r")
             self.rng_r.state = s_.value
-            if self.n_own:
+            if self.n_own and self.cfg.variant == "collab":
+                self.rn[slot][:, : self.L].copy_(self.rall.index_select(0, self.rperm))  # r itself (Enc is online)
+            elif self.n_own:
                 r_in = self.rall.index_select(0, self.rperm).contiguous()
                 _raise_for(self.lib.pcb_encrypt(self.pre._ctx, L.ptr(self.m0), 1, L.ptr(r_in), r_in.shape[0],
                                                 L.ptr(self.rn[slot]), 1, None, st), "offline encryption")
             self.rn_ready[slot].record(ps)
+
+    def _masks(self, count: int) -> list[int]:
+        return [self.mask_rng.next() for _ in range(count)]
+
+    def _collab_encrypt(self, q, r, ct):
+        """Alg. 3 encryption: the edge returns g^(obf(q) mod phi(p^2)) mod p^2 (delegated_power,
+        protocol.cpp:248-249), the master finishes with finish_split_encrypt (paillier.cpp:402-414)."""
+        import torch
+
+        qs = q.cpu().numpy().view(np.uint64).reshape(-1).tolist()
+        obf = [int(v) + k * self.n_eps for v, k in zip(qs, self._masks(len(qs)))]
+        ow = max(1, max(o.bit_length() for o in obf) // 32 + 1)
+        g = np.zeros((len(qs), 2 * self.share.S), np.uint32)
+        g[:] = L.int_to_limbs(self.master.n + 1, 2 * self.share.S)
+        gp = self.share.delegated_power_batch(g, L.ints_to_limbs(obf, ow))
+        G = torch.from_numpy(gp.view(np.int32)).to(self.dev)
+        st = np.zeros(len(qs), np.int32)
+        out = torch.empty_like(ct)
+        torch.cuda.current_stream(self.device).synchronize()
+        _raise_for(self.lib.pcb_finish_split_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(G), gp.shape[1], L.ptr(r),
+                                                     len(qs), L.ptr(out), L.ptr(st), None),
+                   "finish_split_encrypt")
+        return out
+
+    def _collab_dec_powers(self, upd):
+        """Edge side of Alg. 3 decryption: upd^(obf_dec mod phi(p^2)) mod p^2 (protocol.cpp:226, 492)."""
+        import torch
+
+        torch.cuda.current_stream(self.device).synchronize()
+        n = upd.shape[0]
+        obf_dec = [self.eps + k * self.n_eps for k in self._masks(n)]
+        ow = max(1, max(o.bit_length() for o in obf_dec) // 32 + 1)
+        px = self.share.delegated_power_batch(upd.cpu().numpy().view(np.uint32), L.ints_to_limbs(obf_dec, ow))
+        W = 2 * self.L
+        full = np.zeros((n, W), np.uint32)
+        full[:, : px.shape[1]] = px
+        return torch.from_numpy(full.view(np.int32)).to(self.dev)
 
     def step_all(self, t: int) -> int:
         """The iteration on the high-priority session stream, joined back to the caller's stream."""
@@ -382,8 +434,11 @@ class EncryptedSession(ShardedDriver):
             vin = torch.cat([self.z[lo:lo + n], -self.v[lo:lo + n]]).contiguous()
             q, clamps = self._quantize(vin, spec, fine=False)
             ct = torch.empty((2 * n, W), dtype=torch.int32, device=self.dev)
-            _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(self.rn[slot]), 2 * n, L.ptr(ct),
-                                               None, st), "Enc z, -v")
+            if cfg.variant == "collab":
+                ct = self._collab_encrypt(q, self.rn[slot][:, : self.L].contiguous(), ct)
+            else:
+                _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(self.rn[slot]), 2 * n,
+                                                   L.ptr(ct), None, st), "Enc z, -v")
         self.enc_done.record(cur)
         if t + 1 < cfg.iters:
             self._precompute(1 - slot)
@@ -393,9 +448,16 @@ class EncryptedSession(ShardedDriver):
             _raise_for(self.lib.pcb_edge_step_blocks(self.edge._ctx, len(sz), sz.ctypes.data, L.ptr(self.alpha_hat),
                                                      L.ptr(self.expo), L.ptr(ct[:n]), L.ptr(ct[n:]), cfg.window,
                                                      L.ptr(upd), st), "edge step")
-            _raise_for(self.lib.pcb_decrypt_update_blocks(self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd),
-                                                          L.ptr(self.rowsum), L.ptr(q[:n]), L.ptr(q[n:]), spec[0],
-                                                          spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
-                                                          L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None,
-                                                          st), "master update")
+            if cfg.variant == "collab":  # edge: delegated Dec powers; master: decrypt_with_half + update
+                px = self._collab_dec_powers(upd)
+                _raise_for(self.lib.pcb_decrypt_update_blocks_half(
+                    self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(px), L.ptr(self.rowsum),
+                    L.ptr(q[:n]), L.ptr(q[n:]), spec[0], spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
+                    L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None, st), "master update (collab)")
+            else:
+                _raise_for(self.lib.pcb_decrypt_update_blocks(self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd),
+                                                              L.ptr(self.rowsum), L.ptr(q[:n]), L.ptr(q[n:]), spec[0],
+                                                              spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
+                                                              L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None,
+                                                              st), "master update")
         return clamps

@@ -1136,6 +1136,30 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
 
 // ---- collaborative variant (paper Alg. 3) ---------------------------------------
 }  // extern "C"
+// device core of decrypt_with_half: c (count x 2L), pw (count x 2L: the p-half, any representative)
+static pcb_status dwh_core(pcb_ctx* x, const uint32_t* c, const uint32_t* pw, size_t count, uint32_t* m, int32_t* stv,
+                           cudaStream_t st) {
+  const int S = x->S, L2 = 2 * (int)x->L;
+  uint32_t *yp = nullptr, *yq = nullptr;
+  pcb_status e = scratch_alloc(count * S * 4, (void**)&yp, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yq, st);
+  if (!e) e = launch_dec_prep(c, x->d_n2, (int)x->L, stv, count, st);  // c < n^2 (paillier.cpp:365)
+  const double mm = 2.0 * S * S + S;
+  // p side: p2_power mod p^2 (reference: mod(p2_power, crt_.p2)); q side: c^(eps mod phi(q^2)) mod q^2
+  if (!e) e = launch_rnsx(x->rx_p, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, pw, L2, nullptr, 0, count, yp, st, mm);
+  if (!e)
+    e = launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_epsq, x->len_epsq, kTab, c, L2, nullptr, 0, count, yq, st,
+                    ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm);
+  if (!e && S == 64)
+    e = launch_dec_finish<64>(*reinterpret_cast<const CrtDecConsts<64>*>(x->half_blob.data()), yp, yq, stv, m,
+                              (int)x->L, count, st);
+  if (!e && S == 96)
+    e = launch_dec_finish<96>(*reinterpret_cast<const CrtDecConsts<96>*>(x->half_blob.data()), yp, yq, stv, m,
+                              (int)x->L, count, st);
+  scratch_free(yp, st);
+  scratch_free(yq, st);
+  return e;
+}
 struct pcb_share {  // an edge's CrtShare (paillier.hpp:64-66): p^2 and phi(p^2) only
   int device = 0;
   HBN p2, phi;
@@ -1240,7 +1264,7 @@ pcb_status pcb_decrypt_with_half(pcb_ctx* x, const uint32_t* c, const uint32_t* 
   cudaStream_t st = (cudaStream_t)stream;
   const int S = x->S, L2 = 2 * (int)x->L;
   Staged sc, sp, sm, ss;
-  uint32_t *pw = nullptr, *yp = nullptr, *yq = nullptr;
+  uint32_t* pw = nullptr;
   int32_t* stv = nullptr;
   pcb_status e = stage_in(c, count * L2 * 4, st, &sc);
   if (!e) e = stage_in(p2_power, count * pw_limbs * 4, st, &sp);
@@ -1249,30 +1273,14 @@ pcb_status pcb_decrypt_with_half(pcb_ctx* x, const uint32_t* c, const uint32_t* 
   stv = (int32_t*)ss.dev;
   if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
   if (!e) e = scratch_alloc(count * L2 * 4, (void**)&pw, st);
-  if (!e) e = scratch_alloc(count * S * 4, (void**)&yp, st);
-  if (!e) e = scratch_alloc(count * S * 4, (void**)&yq, st);
-  if (!e) e = launch_dec_prep((const uint32_t*)sc.dev, x->d_n2, (int)x->L, stv, count, st);  // c < n^2 (paillier.cpp:365)
   if (!e) e = cuda_check(cudaMemset2DAsync(pw, L2 * 4, 0, L2 * 4, count, st));
   if (!e)
     e = cuda_check(cudaMemcpy2DAsync(pw, L2 * 4, sp.dev, pw_limbs * 4, pw_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
-  const double mm = 2.0 * S * S + S;
-  // p side: p2_power mod p^2 (reference: mod(p2_power, crt_.p2)); q side: c^(eps mod phi(q^2)) mod q^2
-  if (!e)
-    e = launch_rnsx(x->rx_p, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, pw, L2, nullptr, 0, count, yp, st, mm);
-  if (!e)
-    e = launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_epsq, x->len_epsq, kTab, (const uint32_t*)sc.dev, L2, nullptr,
-                    0, count, yq, st, ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm);
-  if (!e && S == 64)
-    e = launch_dec_finish<64>(*reinterpret_cast<const CrtDecConsts<64>*>(x->half_blob.data()), yp, yq, stv,
-                              (uint32_t*)sm.dev, (int)x->L, count, st);
-  if (!e && S == 96)
-    e = launch_dec_finish<96>(*reinterpret_cast<const CrtDecConsts<96>*>(x->half_blob.data()), yp, yq, stv,
-                              (uint32_t*)sm.dev, (int)x->L, count, st);
+  (void)S;
+  if (!e) e = dwh_core(x, (const uint32_t*)sc.dev, pw, count, (uint32_t*)sm.dev, stv, st);
   if (!e) e = unstage_out(m, &sm, st);
   if (!e) e = unstage_out(status, &ss, st);
   scratch_free(pw, st);
-  scratch_free(yp, st);
-  scratch_free(yq, st);
   if (!ss.dev) scratch_free(stv, st);
   const bool any_host = sc.host || sp.host || sm.host || ss.host;
   unstage(&sc, st);
@@ -1771,10 +1779,14 @@ pcb_status pcb_edge_step_blocks(pcb_ctx* x, size_t nblocks, const uint32_t* size
   return edge_entry(x, nblocks, sizes, alpha, expo, zc, vc, window, out, stream);
 }
 
+extern "C++" {
+static pcb_status dwh_core(pcb_ctx* x, const uint32_t* c, const uint32_t* pw, size_t count, uint32_t* m, int32_t* stv,
+                           cudaStream_t st);
+}
 static pcb_status update_entry(pcb_ctx* x, size_t nblk, const uint32_t* sizes, const uint32_t* c,
                                const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv, double z_min,
                                double z_max, double delta, double kappa, double* xo, double* zo, double* vo,
-                               int32_t* status, pcb_stream stream) {
+                               int32_t* status, pcb_stream stream, const uint32_t* p2pow = nullptr) {
   if (!x || (nblk && !sizes)) return PCB_E_SHAPE;
   size_t count = 0;
   std::vector<long long> seg(nblk + 1, 0);
@@ -1805,7 +1817,11 @@ static pcb_status update_entry(pcb_ctx* x, size_t nblk, const uint32_t* sizes, c
   if (!e) e = scratch_alloc(count * x->L * 4, (void**)&m, st);
   if (!e) e = scratch_alloc(seg.size() * 8, (void**)&segd, st);
   if (!e) e = cuda_check(cudaMemcpyAsync(segd, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, st));
-  if (!e) e = dec_core(x, (const uint32_t*)sc.dev, count, m, stv, st);
+  Staged sp;
+  if (p2pow && !x->use_rnsx) e = e ? e : PCB_E_UNSUPPORTED;
+  if (!e && p2pow) e = stage_in(p2pow, count * 2 * x->L * 4, st, &sp);
+  if (!e) e = p2pow ? dwh_core(x, (const uint32_t*)sc.dev, (const uint32_t*)sp.dev, count, m, stv, st)  // collaborative
+                    : dec_core(x, (const uint32_t*)sc.dev, count, m, stv, st);
   if (!e)
     e = launch_update(m, (int)x->L, (const uint64_t*)sr.dev, (const uint64_t*)sz.dev, (const uint64_t*)sn.dev, z_min,
                       z_max, delta, kappa, (double*)sx.dev, (double*)szz.dev, (double*)sv.dev, stv, count, segd,
@@ -1824,10 +1840,10 @@ static pcb_status update_entry(pcb_ctx* x, size_t nblk, const uint32_t* sizes, c
   if (!ss.dev) scratch_free(stv, st);
   scratch_free(m, st);
   scratch_free(segd, st);
-  for (auto* p : {&sc, &sr, &sz, &sn, &sx, &szz, &sv, &ss}) unstage(p, st);
+  for (auto* p : {&sc, &sr, &sz, &sn, &sx, &szz, &sv, &ss, &sp}) unstage(p, st);
   cudaStreamSynchronize(st);
   if (!e) {
-    x->pow_half += 2 * (uint64_t)count;
+    x->pow_half += (p2pow ? 1 : 2) * (uint64_t)count;
     for (int32_t v : hst)
       if (v != PCB_OK) return (pcb_status)v;  // first failure, like the reference's throw
   }
@@ -1847,6 +1863,15 @@ pcb_status pcb_decrypt_update_blocks(pcb_ctx* x, size_t nblocks, const uint32_t*
                                      double z_max, double delta, double kappa, double* xo, double* zo, double* vo,
                                      int32_t* status, pcb_stream stream) {
   return update_entry(x, nblocks, sizes, c, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, status, stream);
+}
+
+pcb_status pcb_decrypt_update_blocks_half(pcb_ctx* x, size_t nblocks, const uint32_t* sizes, const uint32_t* c,
+                                          const uint32_t* p2_power, const uint64_t* rowsum, const uint64_t* q_z,
+                                          const uint64_t* q_nv, double z_min, double z_max, double delta, double kappa,
+                                          double* xo, double* zo, double* vo, int32_t* status, pcb_stream stream) {
+  if (!p2_power) return PCB_E_SHAPE;
+  return update_entry(x, nblocks, sizes, c, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, status, stream,
+                      p2_power);
 }
 
 pcb_status pcb_quantize(const double* v, size_t count, double z_min, double z_max, double delta, int fine,

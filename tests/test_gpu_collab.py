@@ -116,3 +116,25 @@ def test_delegated_power_edge_worker(key2048):
     for i in range(count):
         assert got[i] == pow(bases[i] % p2, obfs[i] % phi, p2), i
     assert P.delegated_power(bases[5], obfs[5], share) == got[5]
+
+
+def test_collab_session_equals_basic():
+    """The collaborative session (delegated p^2 powers, finish_split_encrypt, decrypt_with_half)
+    gives the same trajectory as the basic one (test_protocol.cpp:173, 202)."""
+    import admm_oracle as AO
+    from paper_2601_14980_b200 import admm as ADMM
+
+    a, y, _ = AO.gen_gaussian_problem(24, 40, 0.1, 4)
+    sizes = AO.split_columns(40, 2)
+    fac, at = [], 0
+    for c in sizes:
+        fac.append(AO.node_factor(a[:, at:at + c], y, 1.0, 2))
+        at += c
+    spec = AO.session_bounds(a, y, 1.0, 1.0, 3, sizes, 1.5, 1e15, fac)
+    keys = P.keygen(P.Rng(1 ^ 0x6B657967656E2E2E), 2048)
+    basic = ADMM.EncryptedSession(keys, ADMM.SessionConfig(nodes=2, iters=3)).run(a, y, factors=fac, spec=spec)
+    collab = ADMM.EncryptedSession(keys, ADMM.SessionConfig(nodes=2, iters=3, variant="collab")).run(
+        a, y, factors=fac, spec=spec)
+    for t in range(3):
+        assert collab.x_trace[t].tolist() == basic.x_trace[t].tolist(), t
+    assert collab.z.tolist() == basic.z.tolist() and collab.v.tolist() == basic.v.tolist()
