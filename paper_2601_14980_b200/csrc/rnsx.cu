@@ -74,7 +74,7 @@ struct Cfg {
   static constexpr uint32_t OFF_BAR = OFF_SLT + NSLICE * 16 + NSTG * 8;
   static constexpr uint32_t OFF_RING = (OFF_BAR + 512 + 1023) & ~1023u;
   static constexpr int NSTAGE_FIT = (int)((227u * 1024u - OFF_RING) / SLOT);
-  static constexpr int NSTAGE = (NSTAGE_FIT > 12 ? 12 : NSTAGE_FIT) & ~1;  // even: slots are released in pairs
+  static constexpr int NSTAGE = NSTAGE_FIT > 12 ? 12 : NSTAGE_FIT;
   static constexpr uint32_t SMEM = OFF_RING + NSTAGE * SLOT;
   __host__ __device__ static constexpr int ptc(int c) { return c < NC - 1 ? TPC : PTL; }
   __host__ __device__ static constexpr int ncol(int c) { return 16 * ptc(c); }
@@ -776,8 +776,7 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
       const int i0 = gm ? NG1 : 0, i1 = gm ? C::NSLICE : NG1;
 #pragma unroll 1
       for (int i = i0; i < i1; i++, issued++) {
-        // slots are released in pairs by the MMA warp (commit on the odd slot) except under cta_group::2
-    if (issued >= (uint32_t)C::NSTAGE) umma::mbar_wait(empty + (C::CG == 2 ? pslot : (pslot | 1u)), pph ^ 1);
+        if (issued >= (uint32_t)C::NSTAGE) umma::mbar_wait(empty + pslot, pph ^ 1);
         const uint2 d = stg[i];
         if (lane == 0) {
           umma::mbar_arrive_expect_tx(full + pslot, C::CG == 2 ? d.y >> 1 : d.y);
@@ -844,11 +843,7 @@ __device__ __noinline__ void mma_fast(uint8_t* sm, uint32_t tm, uint64_t* bars, 
           umma::mbar_wait(full + cslot, cph);
           mma_elect(dt, hi | (uint64_t)(alo + (uint32_t)k * (2 * C::TILE * 16 / 16)),
                     hi | (uint64_t)((bslot & 0x3FFFu) | (ncol << 16)), idesc, (uint32_t)k);
-          // release ring slots in pairs: a commit costs ~60 clk (profiles/r01_mma_rate_commit_each.txt);
-          // the commit on odd slot 2i+1 covers the MMAs of slots 2i and 2i+1
-          if (cslot & 1) {
-            if (cl == 2) commit_elect_mc(empty + cslot, 0x3); else commit_elect(empty + cslot);
-          }
+          if (cl == 2) commit_elect_mc(empty + cslot, 0x3); else commit_elect(empty + cslot);
           bslot += SLOT16;
           if (++cslot == (uint32_t)C::NSTAGE) { cslot = 0; cph ^= 1; bslot = ring16; }
         }
