@@ -349,6 +349,7 @@ def main() -> None:
     engine = lib.pcb_ctx_engine(ph._ctx)
     int8_macs = lib.pcb_profile_int8_macs()
     tensor = None
+    traffic = None
     if engine == 3:
         kname = "pcb::rnsx_kernel<72> (streaming RNS Montgomery, tcgen05 kind::i8 base extensions)"
         dtype = "u32 RNS residues (IMAD) + u8 byte planes on tcgen05 kind::i8 (s32 accumulate); FP64 quantizer"
@@ -361,6 +362,9 @@ def main() -> None:
             if os.path.exists(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")) else {}
         i8_peak = float(mp.get("bf16_tflops", 2250.0))  # int8 T MAC/s = 2 x (bf16 TFLOP/s / 2)
         i8_ach = int8_macs / (ms.value / 1e3) / 1e12
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_bench_rnsx_traffic.json")
+        if os.path.exists(tpath):  # DRAM bytes per launch of this kernel from one ncu --set full capture
+            traffic = json.load(open(tpath))["traffic_bytes_per_launch"]
         tensor = {"bound": "tensor", "achieved": i8_ach, "peak": i8_peak, "unit": "T int8 MAC/s", "frac": i8_ach / i8_peak,
                   "int8_macs": int8_macs,
                   "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops / 2 (int8 dense = 2x bf16 on tcgen05)"
@@ -429,7 +433,7 @@ def main() -> None:
             "parity_check": ok,
             "enc_dec_mac32_per_s": value * (ENC_MAC + DEC_MAC),
             "roofline": {"bound": "imad", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TMAC32/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": kname, "note": rnote,
+                         "frac": achieved / peak, "traffic": traffic, "kernel": kname, "note": rnote,
                          "launches": int(nl.value), "kernel_ms": ms.value, "share_of_step": side_share,
                          "peak_source": "pcb_imad_peak (IMAD.WIDE.U32 chains on all SMs), measured in this run",
                          "tensor_int8": tensor},
