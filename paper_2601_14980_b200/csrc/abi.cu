@@ -248,6 +248,15 @@ struct pcb_ctx {
   bool use_rns = false;
   RnsXModulus rx_p, rx_q;        // p^2, q^2 for the streaming RNS core (rnsx.cu)
   bool use_rnsx = false;
+  // split CRT encryption (2048-bit keys): r^n mod p^2 = ((r mod p)^q mod p)^p mod p^2, since u^p
+  // mod p^2 depends only on u mod p; stage 1 on the carry-chain core mod p (1024 bits), stage 2
+  // on the RNS core with the 1024-bit exponent p (half the exponent bits of n).  Same for q.
+  bool enc_split = false;
+  bool enc_split_rns = false;           // stage 1 on the RNS core (K = 48) instead
+  RnsXModulus rx1_p, rx1_q;             // p, q on the RNS core
+  ModCtx<32> m1p, m1q;                  // p, q (32 limbs, R = 2^1024)
+  std::vector<uint32_t> r3_p1, r3_q1;   // R^3 mod p, R^3 mod q
+  int off_ep = 0, len_ep = 0, off_eq = 0, len_eq = 0;  // exponents p and q
   RnsXModulus rx_n2;             // n^2 on the streaming RNS core (matvec, public-key ops)
   bool use_rx_n2 = false;
   std::vector<uint32_t> rp2_nR, rq2_nR, rp2_R3, rq2_R3;
@@ -502,6 +511,18 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
         int K = 0;
         if ((!ev || atoi(ev) != 0) && (x->S == 64 || x->S == 96) && rnsx_shape((int)(32 * x->S), &K))
           x->use_rnsx = rnsx_build(p2, x->n, x->S, K, &x->rx_p) && rnsx_build(q2, x->n, x->S, K, &x->rx_q);
+        const char* es = getenv("PCB_ENC_SPLIT");
+        if (x->use_rnsx && x->S == 64 && x->p.bit_length() <= 1024 && x->q.bit_length() <= 1024 &&
+            (!es || atoi(es) != 0)) {
+          x->enc_split = true;
+          const HBN R3 = HBN(1) << (3 * 1024);
+          fill_mod<32>(x->m1p, x->p);
+          fill_mod<32>(x->m1q, x->q);
+          x->r3_p1 = mod(R3, x->p).limbs(32);
+          x->r3_q1 = mod(R3, x->q).limbs(32);
+          if (!es || atoi(es) == 2)  // default: stage 1 on the RNS core; PCB_ENC_SPLIT=1 selects the carry core
+            x->enc_split_rns = rnsx_build(x->p, x->n, 32, 48, &x->rx1_p) && rnsx_build(x->q, x->n, 32, 48, &x->rx1_q);
+        }
       }
       switch (x->S) {
         case 32: build_enc<32>(x.get()); build_dec<32>(x.get()); break;
@@ -549,6 +570,8 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
       const HBN eps = lcm(x->p - HBN(1), x->q - HBN(1));
       add(mod(eps, q2 - x->q), &x->off_epsq, &x->len_epsq);  // decrypt_with_half's q side (paillier.cpp:366)
       add(HBN(1), &x->off_one, &x->len_one);                 // plain reduction mod p^2
+      add(x->p, &x->off_ep, &x->len_ep);                     // split encryption (enc_split)
+      add(x->q, &x->off_eq, &x->len_eq);
     }
     add(x->n, &x->off_pub, &x->len_pub);
     if (cudaSetDevice(device) != cudaSuccess) return PCB_E_CUDA;
@@ -633,6 +656,8 @@ void pcb_ctx_destroy(pcb_ctx* x) {
   rnsx_free(&x->rx_p);
   rnsx_free(&x->rx_q);
   rnsx_free(&x->rx_n2);
+  rnsx_free(&x->rx1_p);
+  rnsx_free(&x->rx1_q);
   delete x;
 }
 
@@ -729,7 +754,41 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
   const int ml = v ? mql : (int)m_limbs;
   const uint8_t* opp = x->d_sched + x->off_enc_p;
   const uint8_t* opq = x->d_sched + x->off_enc_q;
-  if (!e && x->use_rnsx) {
+  if (!e && x->use_rnsx && x->enc_split) {
+    const double mm = 2.0 * S * S + S, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm + 2 * mm;
+    const uint8_t* oep = x->d_sched + x->off_ep;
+    const uint8_t* oeq = x->d_sched + x->off_eq;
+    uint32_t *up = nullptr, *uq = nullptr;
+    e = scratch_alloc(count * 32 * 4, (void**)&up, st);
+    if (!e) e = scratch_alloc(count * 32 * 4, (void**)&uq, st);
+    // stage 1: u = r^q mod p (kSideDec reduces the 2048-bit r: r R = r_lo R + r_hi R^2);
+    // stage 2: (1 + m n) u^p mod p^2.  The canonical work is accounted on stage 2.
+    if (!e)
+      e = fork_join(
+          x, st,
+          [&](cudaStream_t s2) {
+            pcb_status e2 =
+                x->enc_split_rns
+                    ? launch_rnsx(x->rx1_p, kRxDec, oeq, x->len_eq, kTab, r, (int)x->L, nullptr, 0, count, up, s2, 0.0)
+                    : launch_side<32>(x->m1p, x->r3_p1.data(), oeq, x->len_eq, kTab, kSideDec, r, (int)x->L, nullptr, 0,
+                                      stv, count, up, s2, -1);
+            if (!e2) e2 = launch_rnsx(x->rx_p, kRxEnc, oep, x->len_ep, kTab, up, 32, mm_, ml, count, yp, s2, alg);
+            return e2;
+          },
+          [&](cudaStream_t s2) {
+            pcb_status e2 =
+                x->enc_split_rns
+                    ? launch_rnsx(x->rx1_q, kRxDec, oep, x->len_ep, kTab, r, (int)x->L, nullptr, 0, count, uq, s2, 0.0)
+                    : launch_side<32>(x->m1q, x->r3_q1.data(), oep, x->len_ep, kTab, kSideDec, r, (int)x->L, nullptr, 0,
+                                      stv, count, uq, s2, -1);
+            if (!e2) e2 = launch_rnsx(x->rx_q, kRxEnc, oeq, x->len_eq, kTab, uq, 32, mm_, ml, count, yq, s2, alg);
+            return e2;
+          },
+          count);
+    if (!e) e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
+    scratch_free(up, st);
+    scratch_free(uq, st);
+  } else if (!e && x->use_rnsx) {
     const double mm = 2.0 * S * S + S, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm + 2 * mm;
     e = fork_join(
         x, st,

@@ -200,7 +200,8 @@ pcb_status launch_side(const ModCtx<S>& mod, const uint32_t* c1, const uint8_t* 
   if (prof_enabled()) pm = prof_start(st);
   side_kernel<S><<<blocks, kThreadsPerBlock, smem, st>>>(P);
   count_launch();
-  if (prof_enabled()) prof_stop(pm, st, canon_mac32(S, ebits_canon) * (double)count);
+  // ebits_canon < 0: a stage whose canonical work is accounted on another launch
+  if (prof_enabled()) prof_stop(pm, st, ebits_canon < 0 ? 0.0 : canon_mac32(S, ebits_canon) * (double)count);
   scratch_free(P.tab, st);
   return cuda_check(cudaGetLastError());
 }

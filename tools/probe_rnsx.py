@@ -1,6 +1,6 @@
 """Development probe: streaming RNS core (PCB_RNSX=1 context) vs the default engine.
 Bit-for-bit comparison of CRT Enc and Dec on the same inputs, and throughput of both.
-usage: probe_rnsx.py BITS N [N ...]"""
+usage: probe_rnsx.py BITS N [N ...]   (PROBE_ENV=VAR compares VAR=0 against VAR=1 instead of PCB_RNSX)"""
 import json
 import os
 import sys
@@ -27,11 +27,13 @@ def key(bits):
 bits = int(sys.argv[1])
 sizes = [int(a) for a in sys.argv[2:]] or [1024]
 kp = key(bits)
-os.environ["PCB_RNSX"] = "0"  # baseline: the previous default core for this key size
+VAR = os.environ.get("PROBE_ENV", "PCB_RNSX")
+VALS = os.environ.get("PROBE_VALS", "0,1").split(",")
+os.environ[VAR] = VALS[0]  # baseline: the previous default core for this key size
 base = P.Paillier(kp)
-os.environ["PCB_RNSX"] = "1"
+os.environ[VAR] = VALS[1]
 rx = P.Paillier(kp)
-os.environ.pop("PCB_RNSX", None)
+os.environ.pop(VAR, None)
 from paper_2601_14980_b200 import _lib as L  # noqa: E402
 
 eng = [L.lib().pcb_ctx_engine(base._ctx), L.lib().pcb_ctx_engine(rx._ctx)] if hasattr(base, "_ctx") else None
