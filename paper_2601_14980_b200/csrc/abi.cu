@@ -257,6 +257,7 @@ struct pcb_ctx {
   ModCtx<32> m1p, m1q;                  // p, q (32 limbs, R = 2^1024)
   std::vector<uint32_t> r3_p1, r3_q1;   // R^3 mod p, R^3 mod q
   int off_ep = 0, len_ep = 0, off_eq = 0, len_eq = 0;  // exponents p and q
+  int w1 = 32;                          // words of p, q (stage-1 outputs)
   RnsXModulus rx_n2;             // n^2 on the streaming RNS core (matvec, public-key ops)
   bool use_rx_n2 = false;
   std::vector<uint32_t> rp2_nR, rq2_nR, rp2_R3, rq2_R3;
@@ -512,16 +513,23 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
         if ((!ev || atoi(ev) != 0) && (x->S == 64 || x->S == 96) && rnsx_shape((int)(32 * x->S), &K))
           x->use_rnsx = rnsx_build(p2, x->n, x->S, K, &x->rx_p) && rnsx_build(q2, x->n, x->S, K, &x->rx_q);
         const char* es = getenv("PCB_ENC_SPLIT");
-        if (x->use_rnsx && x->S == 64 && x->p.bit_length() <= 1024 && x->q.bit_length() <= 1024 &&
+        const size_t hb = (size_t)16 * x->S;  // half the p^2 width: p, q bits
+        if (x->use_rnsx && (x->S == 64 || x->S == 96) && x->p.bit_length() <= hb && x->q.bit_length() <= hb &&
             (!es || atoi(es) != 0)) {
-          x->enc_split = true;
-          const HBN R3 = HBN(1) << (3 * 1024);
-          fill_mod<32>(x->m1p, x->p);
-          fill_mod<32>(x->m1q, x->q);
-          x->r3_p1 = mod(R3, x->p).limbs(32);
-          x->r3_q1 = mod(R3, x->q).limbs(32);
-          if (!es || atoi(es) == 2)  // default: stage 1 on the RNS core; PCB_ENC_SPLIT=1 selects the carry core
-            x->enc_split_rns = rnsx_build(x->p, x->n, 32, 48, &x->rx1_p) && rnsx_build(x->q, x->n, 32, 48, &x->rx1_q);
+          x->w1 = x->S / 2;
+          const int K1 = x->S == 64 ? 48 : 64;
+          // default: stage 1 on the RNS core; PCB_ENC_SPLIT=1 selects the carry core (1024-bit p only)
+          if (!es || atoi(es) == 2 || x->S != 64)
+            x->enc_split_rns =
+                rnsx_build(x->p, x->n, x->w1, K1, &x->rx1_p) && rnsx_build(x->q, x->n, x->w1, K1, &x->rx1_q);
+          if (x->S == 64) {
+            const HBN R3 = HBN(1) << (3 * 1024);
+            fill_mod<32>(x->m1p, x->p);
+            fill_mod<32>(x->m1q, x->q);
+            x->r3_p1 = mod(R3, x->p).limbs(32);
+            x->r3_q1 = mod(R3, x->q).limbs(32);
+          }
+          x->enc_split = x->S == 64 || x->enc_split_rns;
         }
       }
       switch (x->S) {
@@ -759,8 +767,9 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
     const uint8_t* oep = x->d_sched + x->off_ep;
     const uint8_t* oeq = x->d_sched + x->off_eq;
     uint32_t *up = nullptr, *uq = nullptr;
-    e = scratch_alloc(count * 32 * 4, (void**)&up, st);
-    if (!e) e = scratch_alloc(count * 32 * 4, (void**)&uq, st);
+    const int w1 = x->w1;
+    e = scratch_alloc(count * w1 * 4, (void**)&up, st);
+    if (!e) e = scratch_alloc(count * w1 * 4, (void**)&uq, st);
     // stage 1: u = r^q mod p (kSideDec reduces the 2048-bit r: r R = r_lo R + r_hi R^2);
     // stage 2: (1 + m n) u^p mod p^2.  The canonical work is accounted on stage 2.
     if (!e)
@@ -772,7 +781,7 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
                     ? launch_rnsx(x->rx1_p, kRxDec, oeq, x->len_eq, kTab, r, (int)x->L, nullptr, 0, count, up, s2, 0.0)
                     : launch_side<32>(x->m1p, x->r3_p1.data(), oeq, x->len_eq, kTab, kSideDec, r, (int)x->L, nullptr, 0,
                                       stv, count, up, s2, -1);
-            if (!e2) e2 = launch_rnsx(x->rx_p, kRxEnc, oep, x->len_ep, kTab, up, 32, mm_, ml, count, yp, s2, alg);
+            if (!e2) e2 = launch_rnsx(x->rx_p, kRxEnc, oep, x->len_ep, kTab, up, w1, mm_, ml, count, yp, s2, alg);
             return e2;
           },
           [&](cudaStream_t s2) {
@@ -781,11 +790,12 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
                     ? launch_rnsx(x->rx1_q, kRxDec, oep, x->len_ep, kTab, r, (int)x->L, nullptr, 0, count, uq, s2, 0.0)
                     : launch_side<32>(x->m1q, x->r3_q1.data(), oep, x->len_ep, kTab, kSideDec, r, (int)x->L, nullptr, 0,
                                       stv, count, uq, s2, -1);
-            if (!e2) e2 = launch_rnsx(x->rx_q, kRxEnc, oeq, x->len_eq, kTab, uq, 32, mm_, ml, count, yq, s2, alg);
+            if (!e2) e2 = launch_rnsx(x->rx_q, kRxEnc, oeq, x->len_eq, kTab, uq, w1, mm_, ml, count, yq, s2, alg);
             return e2;
           },
           count);
-    if (!e) e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
+    if (!e && S == 64) e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
+    if (!e && S == 96) e = launch_garner<96>(*reinterpret_cast<const CrtEncConsts<96>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
     scratch_free(up, st);
     scratch_free(uq, st);
   } else if (!e && x->use_rnsx) {

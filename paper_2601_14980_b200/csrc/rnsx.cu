@@ -1545,7 +1545,7 @@ pcb_status launch_rnsx(const RnsXModulus& md, int mode, const uint8_t* ops, int 
       if (md.K == 112) return launch_cfg<Cfg<112, 1, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
     }
   }
-  if (md.K == 72 || md.K == 48) {  // two tiles in flight per CTA (the K <= 72 register budget allows it)
+  if (md.K == 72 || md.K == 48 || md.K == 64) {  // two tiles in flight per CTA (the K <= 72 register budget allows it)
     const char* ppv = getenv("PCB_RNSX_PP");
     const bool pp = !ppv || atoi(ppv) != 0;  // default on; PCB_RNSX_PP=0 runs one tile per CTA
     int dev = 0, nsm = 148;
@@ -1554,10 +1554,13 @@ pcb_status launch_rnsx(const RnsXModulus& md, int mode, const uint8_t* ops, int 
     if (pp && count >= (size_t)nsm * 2 * 128) {  // pairs only pay once every SM has two tiles
       if (md.K == 72)
         return launch_cfg<Cfg<72, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
+      if (md.K == 64)
+        return launch_cfg<Cfg<64, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
       return launch_cfg<Cfg<48, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
     }
   }
   PCB_RX(48)
+  PCB_RX(64)
   PCB_RX(72)
   PCB_RX(112)
   PCB_RX(144)
