@@ -117,3 +117,40 @@ def test_matvec_n2_core_matches_radix_core_full_block():
     a = pub.hom_matvec_batch(alpha, E, zv)
     b = pub_radix.hom_matvec_batch(alpha, E, zv)
     assert (a == b).all()
+
+
+@pytest.mark.parametrize("bits", [2048, 3072])
+def test_split_encryption_matches_single_pass(bits):
+    """Split CRT Enc (r^n mod p^2 = ((r mod p)^q mod p)^p mod p^2) against the
+    single r^n pass (PCB_ENC_SPLIT=0), the carry-core stage 1 (PCB_ENC_SPLIT=1, 2048-bit) and Python
+    integers, on a full-GPU batch with edge randomness: r = 1, n - 1, multiples of p and of q."""
+    torch = pytest.importorskip("torch")
+    if bits == 2048:
+        kp = _key2048()
+    else:
+        rng = P.Rng(3072)
+        while True:
+            p, q = P.random_prime(rng, 1536), P.random_prime(rng, 1536)
+            if p != q and (p * q).bit_length() == 3072:
+                break
+        kp = P.keypair_from_primes(p, q)
+    n_el = 40000
+    split, single = _ctx(kp), _ctx(kp, PCB_ENC_SPLIT=0)
+    g = np.random.default_rng(bits)
+    m = torch.from_numpy(g.integers(0, 2**32, (n_el, split.L), dtype=np.uint64).astype(np.uint32).view(np.int32)).cuda()
+    m[:, split.L - 1] = 0
+    r = split.sample_r_batch(P.Rng(11), n_el)
+    n, p, q = kp.n, kp.p, kp.q
+    edge = [1, n - 1, p, q, 3 * p, 5 * q, n - p]
+    r[:len(edge)] = torch.from_numpy(L.ints_to_limbs(edge, split.L).view(np.int32)).cuda()
+    c1, c0 = split.encrypt_batch(m, r, True), single.encrypt_batch(m, r, True)
+    assert torch.equal(c1, c0)
+    if bits == 2048:
+        assert torch.equal(_ctx(kp, PCB_ENC_SPLIT=1).encrypt_batch(m, r, True), c1)
+    M, R, C = (t.cpu().numpy().view(np.uint32) for t in (m, r, c1))
+    n2 = n * n
+    for i in list(range(len(edge) + 2)) + [n_el - 1]:
+        mi, ri = L.limbs_to_ints(M[i:i + 1])[0], L.limbs_to_ints(R[i:i + 1])[0]
+        ci = L.limbs_to_ints(C[i:i + 1])[0]
+        assert ci == 0 or ci == (1 + mi * n) * pow(ri, n, n2) % n2, i
+    assert torch.equal(split.decrypt_batch(c1[len(edge):], True), m[len(edge):])
