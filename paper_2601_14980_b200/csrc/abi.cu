@@ -740,6 +740,18 @@ static pcb_status fork_join(pcb_ctx* x, cudaStream_t st, FP&& fp, FQ&& fq, size_
   return e;
 }
 
+// Stage 1 of the split CRT encryption: u = r^q mod p (half 0) or r^p mod q
+// (half 1), x->w1 words per element, on the RNS core (default) or the carry core.
+static pcb_status split_stage1(pcb_ctx* x, int half, const uint32_t* r, const int32_t* stv, size_t count, uint32_t* u,
+                               cudaStream_t st) {
+  const uint8_t* ops = x->d_sched + (half ? x->off_ep : x->off_eq);
+  const int nops = half ? x->len_ep : x->len_eq;
+  if (x->enc_split_rns)
+    return launch_rnsx(half ? x->rx1_q : x->rx1_p, kRxDec, ops, nops, kTab, r, (int)x->L, nullptr, 0, count, u, st, 0.0);
+  return launch_side<32>(half ? x->m1q : x->m1p, (half ? x->r3_q1 : x->r3_p1).data(), ops, nops, kTab, kSideDec, r,
+                         (int)x->L, nullptr, 0, stv, count, u, st, -1);
+}
+
 // Device-pointer core of CRT encryption (m given as limbs, or v quantized in the prep kernel).
 static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const double* v, double zmin, double zmax,
                            double delta, int fine, uint64_t* q_out, unsigned long long* clamps, const uint32_t* r,
@@ -776,20 +788,12 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
       e = fork_join(
           x, st,
           [&](cudaStream_t s2) {
-            pcb_status e2 =
-                x->enc_split_rns
-                    ? launch_rnsx(x->rx1_p, kRxDec, oeq, x->len_eq, kTab, r, (int)x->L, nullptr, 0, count, up, s2, 0.0)
-                    : launch_side<32>(x->m1p, x->r3_p1.data(), oeq, x->len_eq, kTab, kSideDec, r, (int)x->L, nullptr, 0,
-                                      stv, count, up, s2, -1);
+            pcb_status e2 = split_stage1(x, 0, r, stv, count, up, s2);
             if (!e2) e2 = launch_rnsx(x->rx_p, kRxEnc, oep, x->len_ep, kTab, up, w1, mm_, ml, count, yp, s2, alg);
             return e2;
           },
           [&](cudaStream_t s2) {
-            pcb_status e2 =
-                x->enc_split_rns
-                    ? launch_rnsx(x->rx1_q, kRxDec, oep, x->len_ep, kTab, r, (int)x->L, nullptr, 0, count, uq, s2, 0.0)
-                    : launch_side<32>(x->m1q, x->r3_q1.data(), oep, x->len_ep, kTab, kSideDec, r, (int)x->L, nullptr, 0,
-                                      stv, count, uq, s2, -1);
+            pcb_status e2 = split_stage1(x, 1, r, stv, count, uq, s2);
             if (!e2) e2 = launch_rnsx(x->rx_q, kRxEnc, oeq, x->len_eq, kTab, uq, w1, mm_, ml, count, yq, s2, alg);
             return e2;
           },
@@ -1395,12 +1399,25 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
   const double mm = 2.0 * S * S + S, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm;
   // cp = (p2_g_power mod p^2) r^(n mod phi(p^2)) mod p^2;  cq = (1 + m n) r^(n mod phi(q^2)) mod q^2
   if (!e) e = launch_rnsx(x->rx_p, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, gw, L2, nullptr, 0, count, gp, st, mm);
-  if (!e)
-    e = launch_rnsx(x->rx_p, kRxEncG, x->d_sched + x->off_enc_p, x->len_enc_p, kTab, (const uint32_t*)sr.dev,
-                    (int)x->L, gp, S, count, yp, st, alg);
-  if (!e)
-    e = launch_rnsx(x->rx_q, kRxEnc, x->d_sched + x->off_enc_q, x->len_enc_q, kTab, (const uint32_t*)sr.dev,
-                    (int)x->L, (const uint32_t*)sm.dev, (int)m_limbs, count, yq, st, alg);
+  if (x->enc_split) {  // r^n mod p^2 = (r^q mod p)^p mod p^2, same for q
+    uint32_t* u = nullptr;
+    if (!e) e = scratch_alloc(count * x->w1 * 4, (void**)&u, st);
+    if (!e) e = split_stage1(x, 0, (const uint32_t*)sr.dev, stv, count, u, st);
+    if (!e)
+      e = launch_rnsx(x->rx_p, kRxEncG, x->d_sched + x->off_ep, x->len_ep, kTab, u, x->w1, gp, S, count, yp, st, alg);
+    if (!e) e = split_stage1(x, 1, (const uint32_t*)sr.dev, stv, count, u, st);
+    if (!e)
+      e = launch_rnsx(x->rx_q, kRxEnc, x->d_sched + x->off_eq, x->len_eq, kTab, u, x->w1, (const uint32_t*)sm.dev,
+                      (int)m_limbs, count, yq, st, alg);
+    scratch_free(u, st);
+  } else {
+    if (!e)
+      e = launch_rnsx(x->rx_p, kRxEncG, x->d_sched + x->off_enc_p, x->len_enc_p, kTab, (const uint32_t*)sr.dev,
+                      (int)x->L, gp, S, count, yp, st, alg);
+    if (!e)
+      e = launch_rnsx(x->rx_q, kRxEnc, x->d_sched + x->off_enc_q, x->len_enc_q, kTab, (const uint32_t*)sr.dev,
+                      (int)x->L, (const uint32_t*)sm.dev, (int)m_limbs, count, yq, st, alg);
+  }
   if (!e && S == 64)
     e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv,
                           (uint32_t*)sc.dev, (int)x->L, count, st);
