@@ -82,7 +82,7 @@ struct Cfg {
   static_assert(NSTAGE >= 4, "stream ring");
   static_assert((3 * NSTAGE + 2 * NB + 2 * NT) * 8 + 4 <= 512, "barriers");
   static_assert(CG == 1 || (CG == 2 && NT == 1), "pair MMA only with one tile per CTA");
-  static_assert(NT == 1 || NT == 2, "tiles in flight");
+  static_assert(NT >= 1 && NT <= 3, "tiles in flight");
 };
 
 struct XArgs {
@@ -612,6 +612,47 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
     }
     return;
   }
+  if constexpr (C::NT == 3) {
+    // Three tiles in flight (small K): the same rotation as above over tiles 0, 1, 2.
+    constexpr int NT = C::NT;
+    double* sS0 = reinterpret_cast<double*>(T.sm + C::OFF_S);
+#pragma unroll 1
+    for (int k = 0; k < mine; k++) {
+      const int pr = blockIdx.x + k * gridDim.x;
+      int elt[NT];
+      bool lv[NT];
+#pragma unroll
+      for (int t = 0; t < NT; t++) {
+        elt[t] = (NT * pr + t) * C::TILE + T.e;
+        lv[t] = elt[t] < P.count;
+      }
+      uint32_t XB[NT][RPT], XQ[NT][RPT];
+      bool sq;
+      const uint32_t* yb;
+      int yvs;
+#pragma unroll 1
+      for (int s = 0; s < nsteps; s++) {
+#pragma unroll
+        for (int t = 0; t < NT; t++) {
+          if (s > 0) {
+            rx_e2<C>(XB[t], T);
+            post(s - 1, XB[t], XQ[t], t, elt[t], lv[t]);
+          }
+          prep(s, XB[t], XQ[t], t, elt[t], lv[t], sq, yb, yvs);
+          rx_s1<C>(XB[t], XQ[t], sq, yb, yvs, T, T.sm + C::OFF_A1 + t * C::ABLK, T.a1 + 2 * t);
+        }
+#pragma unroll
+        for (int t = 0; t < NT; t++)
+          rx_e1<C>(XQ[t], T, T.sm + C::OFF_A2 + t * C::ABLK, sS0 + t * C::G * C::TILE, T.a2 + 2 * t);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; t++) {
+        rx_e2<C>(XB[t], T);
+        post(nsteps - 1, XB[t], XQ[t], t, elt[t], lv[t]);
+      }
+    }
+    return;
+  }
 #pragma unroll 1
   for (int k = 0; k < mine; k++) {
     const int tile = blockIdx.x + k * gridDim.x;
@@ -772,7 +813,7 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
   for (uint32_t pr = 0; pr < nprod; pr++) {
 #pragma unroll 1
     for (int seg = 0; seg < 2 * C::NT; seg++) {  // G1 per tile, then G2 per tile (MMA issue order)
-      const int gm = C::NT == 2 ? seg >> 1 : seg;
+      const int gm = seg / C::NT;
       const int i0 = gm ? NG1 : 0, i1 = gm ? C::NSLICE : NG1;
 #pragma unroll 1
       for (int i = i0; i < i1; i++, issued++) {
@@ -822,7 +863,7 @@ __device__ __noinline__ void mma_fast(uint8_t* sm, uint32_t tm, uint64_t* bars, 
   for (uint32_t pr = 0; pr < nprod; pr++) {
 #pragma unroll 1
     for (int seg = 0; seg < 2 * C::NT; seg++) {
-      const int gm = C::NT == 2 ? seg >> 1 : seg, tt = C::NT == 2 ? (seg & 1) : 0;
+      const int gm = seg / C::NT, tt = seg % C::NT;
       umma::mbar_wait(abar + 2 * tt + gm, pr & 1);
       umma::tmem_fence_after();
       const uint32_t alo = (gm ? a2lo : a1lo) + tt * ABLK16;
@@ -877,7 +918,7 @@ __device__ __noinline__ void mma_role(uint8_t* sm, uint32_t tm, uint64_t* bars, 
   for (uint32_t pr = 0; pr < nprod; pr++) {
 #pragma unroll 1
     for (int seg = 0; seg < 2 * C::NT; seg++) {  // G1 per tile, then G2 per tile
-    const int gm = C::NT == 2 ? seg >> 1 : seg, tt = C::NT == 2 ? (seg & 1) : 0;
+    const int gm = seg / C::NT, tt = seg % C::NT;
     const int i0 = gm ? NG1 : 0, i1 = gm ? C::NSLICE : NG1;
     e = slt[i0];
 #pragma unroll 1
@@ -1551,6 +1592,9 @@ pcb_status launch_rnsx(const RnsXModulus& md, int mode, const uint8_t* ops, int 
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const char* p3v = getenv("PCB_RNSX_NT3");
+    if (pp && md.K == 48 && p3v && atoi(p3v) != 0 && count >= (size_t)nsm * 3 * 128)
+      return launch_cfg<Cfg<48, 3>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
     if (pp && count >= (size_t)nsm * 2 * 128) {  // pairs only pay once every SM has two tiles
       if (md.K == 72)
         return launch_cfg<Cfg<72, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
