@@ -517,7 +517,7 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
         if (x->use_rnsx && (x->S == 64 || x->S == 96) && x->p.bit_length() <= hb && x->q.bit_length() <= hb &&
             (!es || atoi(es) != 0)) {
           x->w1 = x->S / 2;
-          const int K1 = x->S == 64 ? 48 : 64;
+          const int K1 = x->S == 64 ? 40 : 56;  // M > (2K+2)^2 p with 30-bit primes
           // default: stage 1 on the RNS core; PCB_ENC_SPLIT=1 selects the carry core (1024-bit p only)
           if (!es || atoi(es) == 2 || x->S != 64)
             x->enc_split_rns =

@@ -48,7 +48,14 @@ namespace {
 // 4 PTc columns the primes sit in quads of <= 4 primes x 4 bytes ([quad][byte][prime]), so one
 // tcgen05.ld x16 returns four complete primes.
 // slices per stream stage: bigger bulk copies where the ring has room (8+ stages either way)
-__host__ __device__ constexpr int sps_for(int) { return 1; }  // one <= 8 KB slice per stage
+__host__ __device__ constexpr int sps_for(int) { return 1; }
+// primes in quad j of a chunk with ptc primes per thread group (4, or 2 for a ragged tail)
+__host__ __device__ constexpr int rnsx_qt(int ptc, int j) {
+  return ptc % 4 == 0 ? 4 : (ptc == 2 ? 2 : (4 * j < ptc - 2 ? 4 : 2));
+}
+__host__ __device__ constexpr int rnsx_slot(int ptc, int g, int j) {
+  return (ptc % 4 == 0 || ptc == 2) ? g * ptc + 4 * j : (4 * j < ptc - 2 ? 16 * j + 4 * g : 16 * (ptc / 4) + 2 * g);
+}  // one <= 8 KB slice per stage
 
 template <int K_, int NT_ = 1, int CG_ = 1>
 struct Cfg {
@@ -78,7 +85,10 @@ struct Cfg {
   static constexpr uint32_t SMEM = OFF_RING + NSTAGE * SLOT;
   __host__ __device__ static constexpr int ptc(int c) { return c < NC - 1 ? TPC : PTL; }
   __host__ __device__ static constexpr int ncol(int c) { return 16 * ptc(c); }
-  static_assert(PL % 8 == 0 && (PTL == 2 || PTL % 4 == 0), "ragged chunk: 8 or a multiple of 16 primes");
+  // first prime (within chunk c) of quad j of thread group g: group-major when every group's run is
+  // 16-byte aligned (ptc a multiple of 4, or 2); otherwise quad-major, groups interleaved per quad
+  __host__ __device__ static constexpr int slot(int c, int g, int j) { return rnsx_slot(ptc(c), g, j); }
+  static_assert(PL % 8 == 0, "ragged chunk: a multiple of 8 primes (quads of 4, the last one of 2 or 4)");
   static_assert(NSTAGE >= 4, "stream ring");
   static_assert((3 * NSTAGE + 2 * NB + 2 * NT) * 8 + 4 <= 512, "barriers");
   static_assert(CG == 1 || (CG == 2 && NT == 1), "pair MMA only with one tile per CTA");
@@ -224,7 +234,7 @@ __device__ __forceinline__ void rx_s1(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
     for (int j = 0; j < (ptc + 3) / 4; j++) {
       constexpr int dummy = 0;
       (void)dummy;
-      const int QT = ptc < 4 ? ptc : 4;
+      const int QT = rnsx_qt(ptc, j);  // last quad of a ragged chunk: 2 primes
       const int w0 = C::TPC * c + 4 * j, q = w0 / 4;
       uint32_t yb[4] = {}, yq[4] = {}, xi[4];
       if (!sq) {
@@ -244,7 +254,7 @@ __device__ __forceinline__ void rx_s1(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
         xi[t] = mulr(mulr(XB[w], vb, ra.x, ra.y), ra.z, ra.x, ra.y);
         XQ[w] = mulr(XQ[w], vq, rq.x, rq.y);
       }
-      uint8_t* dst = A1 + umma::kmajor_off(T.e, 4 * (C::CP * c + T.g * ptc + 4 * j), C::TILE);
+      uint8_t* dst = A1 + umma::kmajor_off(T.e, 4 * (C::CP * c + C::slot(c, T.g, j)), C::TILE);
       if (QT == 4) stq<4>(dst, xi); else stq<2>(dst, xi);
     }
   }
@@ -263,7 +273,7 @@ __device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t
     const int ptc = C::ptc(c), nq = (ptc + 3) / 4;
 #pragma unroll
     for (int j = 0; j < nq; j++) {
-      const int QT = ptc < 4 ? ptc : 4;
+      const int QT = rnsx_qt(ptc, j);  // last quad of a ragged chunk: 2 primes
       uint32_t D[16], xp[4];
       if (QT == 4) d_quad<C, 4>(T, ptc, j, j == 0, j == nq - 1, D); else d_quad<C, 2>(T, ptc, j, j == 0, j == nq - 1, D);
 #pragma unroll
@@ -279,7 +289,7 @@ __device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t
         xp[t] = mulr(r, rr.x, rq.x, rq.y);
         sp = __fma_rn((double)xp[t], __hiloint2double((int)rr.z, (int)rr.y), sp);  // beta needs 2^-20 only
       }
-      uint8_t* dst = A2 + umma::kmajor_off(T.e, 4 * (C::CP * c + T.g * ptc + 4 * j), C::TILE);
+      uint8_t* dst = A2 + umma::kmajor_off(T.e, 4 * (C::CP * c + C::slot(c, T.g, j)), C::TILE);
       if (QT == 4) stq<4>(dst, xp); else stq<2>(dst, xp);
     }
   }
@@ -305,7 +315,7 @@ __device__ __forceinline__ void rx_e2(uint32_t (&XB)[C::RPT], Thr<C>& T) {
     const int ptc = C::ptc(c), nq = (ptc + 3) / 4;
 #pragma unroll
     for (int j = 0; j < nq; j++) {
-      const int QT = ptc < 4 ? ptc : 4;
+      const int QT = rnsx_qt(ptc, j);  // last quad of a ragged chunk: 2 primes
       uint32_t D[16];
       if (QT == 4) d_quad<C, 4>(T, ptc, j, j == 0, j == nq - 1, D); else d_quad<C, 2>(T, ptc, j, j == 0, j == nq - 1, D);
 #pragma unroll
@@ -434,8 +444,8 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
               const int ptc = C::ptc(c);
 #pragma unroll
               for (int j = 0; j < (ptc + 3) / 4; j++) {
-                const int QT = ptc < 4 ? ptc : 4, w0 = C::TPC * c + 4 * j;
-                uint32_t* d = o + C::CP * c + T.g * ptc + 4 * j;
+                const int QT = rnsx_qt(ptc, j), w0 = C::TPC * c + 4 * j;
+                uint32_t* d = o + C::CP * c + C::slot(c, T.g, j);
                 if (QT == 4) stq<4>(d, &XQ[w0]); else stq<2>(d, &XQ[w0]);
               }
             }
@@ -558,8 +568,8 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
           const int ptc = C::ptc(c);
 #pragma unroll
           for (int j = 0; j < (ptc + 3) / 4; j++) {
-            const int QT = ptc < 4 ? ptc : 4, w0 = C::TPC * c + 4 * j;
-            uint32_t* d = o + C::CP * c + T.g * ptc + 4 * j;
+            const int QT = rnsx_qt(ptc, j), w0 = C::TPC * c + 4 * j;
+            uint32_t* d = o + C::CP * c + C::slot(c, T.g, j);
             if (QT == 4) stq<4>(d, &XQ[w0]); else stq<2>(d, &XQ[w0]);
           }
         }
@@ -1324,13 +1334,14 @@ bool rnsx_shape(int bits, int* K) {
 bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
   if (N.bit_length() > (size_t)(32 * S) || !N.is_odd() || K <= 0 || K > 144) return false;
   const int G = 4, CP = 64, TPC = CP / G, NC = (K + CP - 1) / CP, PL = K - CP * (NC - 1), PTL = PL / 4;
-  if (PL % 8 || !(PTL == 2 || PTL % 4 == 0)) return false;
+  if (PL % 8) return false;
+  (void)PTL;
   auto ptc = [&](int c) { return c < NC - 1 ? TPC : PTL; };
   const int RPT = TPC * (NC - 1) + PTL, NQ = (RPT + 3) / 4, NV = 2 * NQ;
   // thread-local residue w of thread group g <-> prime index
   auto prime_of = [&](int g, int w) {
     const int c = w / TPC, t = w % TPC;
-    return CP * c + g * ptc(c) + t;
+    return CP * c + rnsx_slot(ptc(c), g, t / 4) + t % 4;
   };
   std::vector<uint32_t> pr;
   for (uint32_t c = (1u << 30) - 1; pr.size() < 2 * (size_t)K; c -= 2)
@@ -1427,7 +1438,7 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
   for (int gm = 0; gm < 2; gm++) {
     const int ks = gm ? KS2 : KS1;
     for (int c = 0; c < NC; c++) {
-      const int pt = ptc(c), qt = pt < 4 ? pt : 4, ncol = 16 * pt;
+      const int pt = ptc(c), ncol = 16 * pt;
       for (int s = 0; s < ks; s++) {
         const size_t off = img.size();
         img.resize(off + (size_t)ncol * 32, 0);
@@ -1436,8 +1447,10 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
         uint8_t* dst = img.data() + off;
         for (int nl = 0; nl < ncol; nl++) {
           // column nl of the chunk: thread group g, quad j, byte b, prime t within the quad
-          const int g = nl / (4 * pt), r = nl % (4 * pt), j = r / (4 * qt), b = (r % (4 * qt)) / qt, t = r % qt;
-          const int o = CP * c + g * pt + 4 * j + t;  // output prime (B' for GEMM 1, B for GEMM 2)
+          // (full quads of 4 primes = 16 columns first; a ragged chunk's last quad may hold 2)
+          const int g = nl / (4 * pt), r = nl % (4 * pt), j = r / 16, qt = pt - 4 * j < 4 ? pt - 4 * j : 4,
+                    b = (r - 16 * j) / qt, t = (r - 16 * j) % qt;
+          const int o = CP * c + rnsx_slot(pt, g, j) + t;  // output prime (B' for GEMM 1, B for GEMM 2)
           const uint32_t m = gm ? B[o] : Bp[o];
           for (int kk2 = 0; kk2 < 32; kk2++) {
             const int k = 32 * s + kk2, src = k / 4, a = k % 4;
@@ -1586,25 +1599,25 @@ pcb_status launch_rnsx(const RnsXModulus& md, int mode, const uint8_t* ops, int 
       if (md.K == 112) return launch_cfg<Cfg<112, 1, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
     }
   }
-  if (md.K == 72 || md.K == 48 || md.K == 64) {  // two tiles in flight per CTA (the K <= 72 register budget allows it)
+  if (md.K == 72 || md.K == 40 || md.K == 56) {  // two tiles in flight per CTA (the K <= 72 register budget allows it)
     const char* ppv = getenv("PCB_RNSX_PP");
     const bool pp = !ppv || atoi(ppv) != 0;  // default on; PCB_RNSX_PP=0 runs one tile per CTA
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const char* p3v = getenv("PCB_RNSX_NT3");
-    if (pp && md.K == 48 && p3v && atoi(p3v) != 0 && count >= (size_t)nsm * 3 * 128)
-      return launch_cfg<Cfg<48, 3>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
+    if (pp && md.K == 40 && p3v && atoi(p3v) != 0 && count >= (size_t)nsm * 3 * 128)
+      return launch_cfg<Cfg<40, 3>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
     if (pp && count >= (size_t)nsm * 2 * 128) {  // pairs only pay once every SM has two tiles
       if (md.K == 72)
         return launch_cfg<Cfg<72, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
-      if (md.K == 64)
-        return launch_cfg<Cfg<64, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
-      return launch_cfg<Cfg<48, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
+      if (md.K == 56)
+        return launch_cfg<Cfg<56, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
+      return launch_cfg<Cfg<40, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
     }
   }
-  PCB_RX(48)
-  PCB_RX(64)
+  PCB_RX(40)
+  PCB_RX(56)
   PCB_RX(72)
   PCB_RX(112)
   PCB_RX(144)
