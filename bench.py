@@ -386,7 +386,7 @@ def main() -> None:
     tensor = None
     traffic = None
     if engine == 3:
-        kname = ("pcb::rnsx_kernel<72> (+ rnsx_kernel<48> for stage 1 of the split CRT Enc; streaming RNS Montgomery, "
+        kname = ("pcb::rnsx_kernel<72> (+ rnsx_kernel<40> for stage 1 of the split CRT Enc; streaming RNS Montgomery, "
                  "tcgen05 kind::i8 base extensions)")
         dtype = "u32 RNS residues (IMAD) + u8 byte planes on tcgen05 kind::i8 (s32 accumulate); FP64 quantizer"
         rnote = ("canonical CIOS MAC32 of the reference algorithm per Enc/Dec (BASELINE.md 2.1) per second; the RNS "
