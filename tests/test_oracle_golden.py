@@ -121,3 +121,24 @@ def test_hom_ops_semantics_toy():
         O.hom_add(kp, enc[16], 5, enc[16], 5)
     c, b = O.hom_scalar_mul(kp, 3, enc[5], 3)
     assert O.decrypt(kp, c) == 15
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2])
+def test_split_encryption_identity_on_golden_vectors(idx):
+    """The split CRT encryption reproduces the reference's ciphertexts:
+    r^n mod p^2 == ((r mod p)^q mod p)^p mod p^2 (and the same with p, q swapped), combined by CRT,
+    on every golden (m, r, c) vector, plus r multiples of p and q."""
+    k, e = golden("keys.json")[idx], golden("encrypt.json")[idx]
+    p, q = H(k["p"]), H(k["q"])
+    n, p2, q2 = p * q, p * p, q * q
+    rs = [H(r) for r in e["r"]] + [1, p, 2 * q, n - 1]
+    for r in rs:
+        assert pow(r, n, p2) == pow(pow(r % p, q, p), p, p2)
+        assert pow(r, n, q2) == pow(pow(r % q, p, q), q, q2)
+    kp = O.finish_keys(p, q, k["bits"])
+    for m, r, c in zip(e["m"], e["r"], e["c"]):
+        m, r = H(m), H(r)
+        cp = (1 + m * n) * pow(pow(r % p, q, p), p, p2) % p2
+        cq = (1 + m * n) * pow(pow(r % q, p, q), q, q2) % q2
+        c_split = (cp + p2 * ((cq - cp) * pow(p2, -1, q2) % q2)) % (n * n)
+        assert c_split == H(c) == O.crt_encrypt_with_r(kp, m, r)
