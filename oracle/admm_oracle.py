@@ -150,3 +150,53 @@ def shadow_session(factors, sizes, spec, rho, lam, iters):
                 v[g] = xv - zz
         trace.append(list(x))
     return trace, z, v
+
+
+def shadow_session_ref(factors, sizes, spec, rho, lam, iters, capture_q: bool = False):
+    """shadow_session with the per-element integer work done by the COMPILED reference
+    (oracle/_ref/libpcref.so through refbind: gamma1/gamma2 quantize.cpp:31-41,
+    combined_quantized_update quantize.cpp:66-82, inverse_quantize_x quantize.cpp:84-112), so the
+    headline shapes (N_k = 512, 1024) finish in seconds.  The float glue (soft threshold and the
+    v update, protocol.cpp:504-511, admm.cpp:18-22) is elementwise IEEE arithmetic in numpy, the
+    same operations in the same order as the scalar restatement above.  capture_q: also return, per
+    iteration, the quantized (q_z, q_nv) of every block in block order (what the master encrypts)."""
+    import refbind as RB
+
+    zmin, zmax, delta = spec
+    blks, at = [], 0
+    for (b_bar, alpha), c in zip(factors, sizes):
+        qa, _, rc = RB.gamma1(np.asarray(alpha, np.float64), zmin, zmax, delta)
+        assert rc == 0
+        qb, _, rc = RB.gamma2(np.asarray(b_bar, np.float64).reshape(-1), zmin, zmax, delta)
+        assert rc == 0
+        qb = qb.reshape(c, c)
+        rowsum = qb.sum(axis=1, dtype=np.uint64)  # < c * 2^50: exact in u64
+        blks.append((at, c, np.ascontiguousarray(qa), np.ascontiguousarray(qb), np.ascontiguousarray(rowsum)))
+        at += c
+    n = at
+    x, z, v = np.zeros(n), np.zeros(n), np.zeros(n)
+    kappa = lam / rho
+    trace, qtrace = [], []
+    lib = RB.lib()
+    for _ in range(iters):
+        qs = []
+        for off, c, qa, qb, rowsum in blks:
+            sl = slice(off, off + c)
+            q_z, _, _ = RB.gamma2(z[sl].copy(), zmin, zmax, delta)
+            q_nv, _, _ = RB.gamma2(-v[sl], zmin, zmax, delta)
+            qs.append((q_z, q_nv))
+            q = np.zeros(2 * c, np.uint64)
+            lib.pcref_combined_update(RB.a(qa), RB.a(qb), RB.a(q_z), RB.a(q_nv), c, c, RB.a(q))
+            xk = np.zeros(c)
+            lib.pcref_inverse_quantize_x(RB.a(q), RB.a(rowsum), RB.a(q_z), RB.a(q_nv), c, c, zmin, zmax, delta,
+                                         RB.a(xk))
+            x[sl] = xk
+            xv = xk + v[sl]
+            zz = np.where(xv > kappa, xv - kappa, np.where(xv < -kappa, xv + kappa, 0.0))
+            z[sl] = zz
+            v[sl] = xv - zz
+        trace.append(x.copy())
+        qtrace.append(qs)
+    if capture_q:
+        return trace, z, v, qtrace
+    return trace, z, v

@@ -239,6 +239,9 @@ class EncryptedSession(ShardedDriver):
         self.edge = Paillier(PublicKey(keys.n, keys.key_bits), device=device)
         self.L = self.master.L
         self.lib = L.lib()
+        # capture = {"iters": T}: keep the quantized state and the enc_state ciphertexts of the first
+        # T iterations (tests compare them with the reference's encrypt_vec, protocol.cpp:410, 473)
+        self.capture = None
         # the iteration's critical path (online Enc -> edge step -> Dec + update) runs at high
         # stream priority; the offline r^n precompute of the next iteration only fills idle SMs
         _raise_for(self.lib.pcb_ctx_set_priority(self.master._ctx, 1), "priority")
@@ -302,6 +305,20 @@ class EncryptedSession(ShardedDriver):
         n_own = int(self.own_sizes.sum())
         self.own_lo = self.offs[own[0]] if own else 0
         self.n_own = n_own
+        # streams, events and the master r-stream buffers exist on every rank, including one that
+        # owns no block (world > nodes): it still advances the shared r stream each iteration
+        self.pstream = torch.cuda.Stream(device=self.device, priority=0)  # least priority (offline work)
+        self.mstream = torch.cuda.Stream(device=self.device, priority=-1)  # critical path
+        self.rn_ready = [torch.cuda.Event() for _ in range(2)]
+        self.enc_done = torch.cuda.Event()
+        self.rall = torch.empty((2 * sum(self.sizes), self.L), dtype=torch.int32, device=self.dev)
+        self.rn = [torch.empty((2 * n_own, 2 * self.L), dtype=torch.int32, device=self.dev) for _ in range(2)]
+        # per-element statuses of the asynchronous encryptions, checked once per iteration after
+        # the update's own stream synchronisation (no extra host sync on the critical path)
+        self.st_pre = [torch.zeros(2 * n_own, dtype=torch.int32, device=self.dev) for _ in range(2)]
+        self.st_enc = torch.zeros(2 * n_own, dtype=torch.int32, device=self.dev)
+        self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.rperm = torch.zeros(0, dtype=torch.int64, device=self.dev)
         if n_own == 0:
             return 0
         b_all = torch.cat([self.factors[k][0].reshape(-1) for k in own]).contiguous()
@@ -334,13 +351,7 @@ class EncryptedSession(ShardedDriver):
             perm_z.extend(range(2 * o, 2 * o + c))
             perm_v.extend(range(2 * o + c, 2 * o + 2 * c))
         self.rperm = torch.tensor(perm_z + perm_v, dtype=torch.int64, device=self.dev)
-        self.rall = torch.empty((2 * sum(self.sizes), self.L), dtype=torch.int32, device=self.dev)
-        self.rn = [torch.empty((2 * n_own, 2 * self.L), dtype=torch.int32, device=self.dev) for _ in range(2)]
         self.m0 = torch.zeros((2 * n_own, 1), dtype=torch.int32, device=self.dev)
-        self.pstream = torch.cuda.Stream(device=self.device, priority=0)  # least priority (offline work)
-        self.mstream = torch.cuda.Stream(device=self.device, priority=-1)  # critical path
-        self.rn_ready = [torch.cuda.Event() for _ in range(2)]
-        self.enc_done = torch.cuda.Event()
         return cl_b + cla[0] + cla[1]
 
 
@@ -363,7 +374,8 @@ class EncryptedSession(ShardedDriver):
             elif self.n_own:
                 r_in = self.rall.index_select(0, self.rperm).contiguous()
                 _raise_for(self.lib.pcb_encrypt(self.pre._ctx, L.ptr(self.m0), 1, L.ptr(r_in), r_in.shape[0],
-                                                L.ptr(self.rn[slot]), 1, None, st), "offline encryption")
+                                                L.ptr(self.rn[slot]), 1, L.ptr(self.st_pre[slot]), st),
+                           "offline encryption")
             self.rn_ready[slot].record(ps)
 
     def _masks(self, count: int) -> list[int]:
@@ -428,6 +440,8 @@ class EncryptedSession(ShardedDriver):
         cur.wait_event(self.rn_ready[slot])
         n = self.n_own
         clamps = 0
+        if n and cfg.variant != "collab":
+            self.bad |= self.st_pre[slot].ne(0).any().to(torch.int32)
         if n:
             lo = self.own_lo
             W = 2 * self.L
@@ -438,7 +452,11 @@ class EncryptedSession(ShardedDriver):
                 ct = self._collab_encrypt(q, self.rn[slot][:, : self.L].contiguous(), ct)
             else:
                 _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(self.rn[slot]), 2 * n,
-                                                   L.ptr(ct), None, st), "Enc z, -v")
+                                                   L.ptr(ct), L.ptr(self.st_enc), st), "Enc z, -v")
+                self.bad |= self.st_enc.ne(0).any().to(torch.int32)
+            if self.capture is not None and t < self.capture.get("iters", 0):
+                self.capture.setdefault("q", []).append(q.clone())
+                self.capture.setdefault("ct", []).append(ct.clone())
         self.enc_done.record(cur)
         if t + 1 < cfg.iters:
             self._precompute(1 - slot)
@@ -460,4 +478,7 @@ class EncryptedSession(ShardedDriver):
                                                               spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
                                                               L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None,
                                                               st), "master update")
+            # the update synchronised the session stream: the encryption statuses are ready
+            if int(self.bad.item()):
+                raise ValueError("encryption argument out of range (crt_encrypt_with_r, paillier.cpp:322-323)")
         return clamps

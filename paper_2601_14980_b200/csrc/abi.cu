@@ -125,6 +125,35 @@ void unstage(Staged* s, cudaStream_t st) {
   s->host = false;
 }
 
+
+// ---- per-element status when the caller passes status = NULL ---------------------------------
+// The reference throws on the first bad element (paillier.cpp:242, 322-323, 348, 36-39); with no
+// status array the ABI returns that element's code instead of silently handing back 0 / garbage.
+__global__ void first_bad_kernel(const int32_t* st, size_t n, unsigned long long* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    if (st[i] != 0) atomicMin(out, ((unsigned long long)i << 32) | (uint32_t)st[i]);
+}
+
+// Scans stv[0, count) for the first non-OK element; synchronises `st` (only called when the caller
+// asked for no status array, i.e. for a single error code).
+pcb_status first_failure(const int32_t* stv, size_t count, cudaStream_t st) {
+  unsigned long long* d = nullptr;
+  unsigned long long h = ~0ull;
+  pcb_status e = scratch_alloc(8, (void**)&d, st);
+  if (!e) e = cuda_check(cudaMemsetAsync(d, 0xff, 8, st));
+  if (!e) {
+    const int thr = 256;
+    const int blocks = (int)std::min<size_t>((count + thr - 1) / thr, 148 * 8);
+    first_bad_kernel<<<blocks, thr, 0, st>>>(stv, count, d);
+    e = cuda_check(cudaGetLastError());
+  }
+  if (!e) e = cuda_check(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st));
+  scratch_free(d, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (e) return e;
+  return h == ~0ull ? PCB_OK : (pcb_status)(int32_t)(uint32_t)(h & 0xffffffffu);
+}
+
 // ---- constants ------------------------------------------------------------------------------
 static uint32_t neg_inv32(uint32_t m0) {
   uint32_t inv = 1;
@@ -496,7 +525,9 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
     x->nbits = (uint32_t)x->n.bit_length();
     x->L = (x->nbits + 31) / 32;
     x->S2 = kernel_width_wide(2 * x->L);
-    if (x->S2 == 0) return PCB_E_SHAPE;
+    // Keys above 3072 bits (the reference's keygen also offers 4096, paillier.cpp:107-109) need an
+    // 8192-bit n^2 core that this build does not have: refuse them explicitly, not as a shape error.
+    if (x->S2 == 0) return x->nbits > 3072 ? PCB_E_UNSUPPORTED : PCB_E_SHAPE;
     x->has_prv = p && q;
     if (x->has_prv) {
       x->p = HBN::from_limbs(p, pq_limbs);
@@ -1107,6 +1138,7 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
                             (uint32_t*)sc.dev, st);
     if (!e) e = unstage_out(c, &sc, st);
     if (!e) e = unstage_out(status, &ss, st);
+    if (!e && !status) e = first_failure(stv, count, st);
     if (!ss.dev) scratch_free(stv, st);
     const bool any_host = sm.host || sr.host || sc.host || ss.host;
     unstage(&sm, st);
@@ -1121,11 +1153,15 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
   if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
   if (!e) e = stage_out(c, count * 2 * x->L * 4, st, &sc);
   if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+  int32_t* stv = (int32_t*)ss.dev;
+  if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
   if (!e)
     e = enc_core(x, (const uint32_t*)sm.dev, m_limbs, nullptr, 0, 0, 0, 0, nullptr, nullptr, (const uint32_t*)sr.dev,
-                 count, (uint32_t*)sc.dev, (int32_t*)ss.dev, st);
+                 count, (uint32_t*)sc.dev, stv, st);
   if (!e) e = unstage_out(c, &sc, st);
   if (!e) e = unstage_out(status, &ss, st);
+  if (!e && !status) e = first_failure(stv, count, st);
+  if (!ss.dev) scratch_free(stv, st);
   const bool any_host = sm.host || sr.host || sc.host || ss.host;
   unstage(&sm, st);
   unstage(&sr, st);
@@ -1168,6 +1204,7 @@ pcb_status pcb_encrypt_rn(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const
                        (uint32_t*)sc.dev, 1, st);
   if (!e) e = unstage_out(c, &sc, st);
   if (!e) e = unstage_out(status, &ss, st);
+  if (!e && !status) e = first_failure(stv, count, st);
   scratch_free(b, st);
   if (!ss.dev) scratch_free(stv, st);
   const bool any_host = sm.host || sr.host || sc.host || ss.host;
@@ -1190,9 +1227,13 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
   pcb_status e = stage_in(c, count * 2 * x->L * 4, st, &sc);
   if (!e) e = stage_out(m, count * x->L * 4, st, &sm);
   if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
-  if (!e) e = dec_core(x, (const uint32_t*)sc.dev, count, (uint32_t*)sm.dev, (int32_t*)ss.dev, st);
+  int32_t* stv = (int32_t*)ss.dev;
+  if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = dec_core(x, (const uint32_t*)sc.dev, count, (uint32_t*)sm.dev, stv, st);
   if (!e) e = unstage_out(m, &sm, st);
   if (!e) e = unstage_out(status, &ss, st);
+  if (!e && !status) e = first_failure(stv, count, st);
+  if (!ss.dev) scratch_free(stv, st);
   const bool any_host = sc.host || sm.host || ss.host;
   unstage(&sc, st);
   unstage(&sm, st);
@@ -1353,6 +1394,7 @@ pcb_status pcb_decrypt_with_half(pcb_ctx* x, const uint32_t* c, const uint32_t* 
   if (!e) e = dwh_core(x, (const uint32_t*)sc.dev, pw, count, (uint32_t*)sm.dev, stv, st);
   if (!e) e = unstage_out(m, &sm, st);
   if (!e) e = unstage_out(status, &ss, st);
+  if (!e && !status) e = first_failure(stv, count, st);
   scratch_free(pw, st);
   if (!ss.dev) scratch_free(stv, st);
   const bool any_host = sc.host || sp.host || sm.host || ss.host;
@@ -1426,6 +1468,7 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
                           (uint32_t*)sc.dev, (int)x->L, count, st);
   if (!e) e = unstage_out(c, &sc, st);
   if (!e) e = unstage_out(status, &ss, st);
+  if (!e && !status) e = first_failure(stv, count, st);
   scratch_free(gw, st);
   scratch_free(gp, st);
   scratch_free(yp, st);

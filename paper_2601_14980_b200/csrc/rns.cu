@@ -21,6 +21,7 @@
 // residues [36h, 36h+36) and the B' residues [36h, 36h+36) of element e = 32 (warp%4) + lane.
 // Shared memory: W1 (288 x 288 B), W2 (288 x 320 B), the A tile (128 x 320 B), all in the
 // no-swizzle K-major core-matrix layout of umma.cuh.  One thread issues the MMAs.
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -479,14 +480,18 @@ pcb_status launch_rns(const RnsModulus& md, int mode, const uint8_t* ops, int no
   P.count = (int)count;
   P.mode = mode;
   P.S = md.S;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(rns_pow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_BYTES) != cudaSuccess)
-      return PCB_E_CUDA;
-    attr = true;
-  }
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
+  // The >48 KB dynamic-smem opt-in is a per-device function attribute: remember it per device
+  // (bit dev of an atomic mask), so a second context on another device, or another host
+  // thread, never launches without it.  Setting it twice is harmless.
+  static std::atomic<uint64_t> attr_dev{0};
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_dev.load(std::memory_order_acquire) & bit)) {
+    if (cudaFuncSetAttribute(rns_pow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_BYTES) != cudaSuccess)
+      return PCB_E_CUDA;
+    attr_dev.fetch_or(bit, std::memory_order_acq_rel);
+  }
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int ntiles = (int)((count + TILE - 1) / TILE);
   const int blocks = ntiles < nsm ? ntiles : nsm;

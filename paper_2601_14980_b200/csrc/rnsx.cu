@@ -21,6 +21,7 @@
 //
 // CTA = 16 compute warps (4 per TMEM lane quadrant; warp w: lanes 32 (w%4).., prime group
 // g = w/4) + 1 role warp; one 128-element tile at a time, persistent over tiles.
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -499,12 +500,13 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
         if (live) { src = P.m + (size_t)el * P.m_words; nw = P.m_words; }
         cst = P.mode == kRxEnc ? kRxNM : kRxOneM;
       } else if ((P.mode == kRxDec || P.mode == kRxPowVar) && first) {  // c_hi 2^(32 S) M
-        if (live) { src = P.x + (size_t)el * P.x_words + P.S; nw = P.x_words - P.S; }
+        // inputs narrower than S words (unbalanced primes: x_words < S) have no high half
+        if (live && P.x_words > P.S) { src = P.x + (size_t)el * P.x_words + P.S; nw = P.x_words - P.S; }
         cst = kRxCR2N;
       } else {  // r M / c_lo M / x M
         if (live) {
           src = P.x + (size_t)el * P.x_words;
-          nw = (P.mode == kRxDec || P.mode == kRxPowVar) ? P.S : P.x_words;
+          nw = (P.mode == kRxDec || P.mode == kRxPowVar) ? min(P.S, P.x_words) : P.x_words;
         }
       }
       conv_in<C>(XB, XQ, src, nw, T);
@@ -1186,14 +1188,18 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
     const char* d = getenv("PCB_RNSX_DBG");
     P.dbg = d ? atoi(d) : 0;
   }
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(rnsx_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
-      return PCB_E_CUDA;
-    attr = true;
-  }
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
+  // The >48 KB dynamic-smem opt-in is a per-device function attribute: remember it per device
+  // (bit dev of an atomic mask), so a second context on another device, or another host
+  // thread, never launches without it.  Setting it twice is harmless.
+  static std::atomic<uint64_t> attr_dev{0};
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_dev.load(std::memory_order_acquire) & bit)) {
+    if (cudaFuncSetAttribute(rnsx_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
+      return PCB_E_CUDA;
+    attr_dev.fetch_or(bit, std::memory_order_acq_rel);
+  }
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const int ntiles = (int)((count + C::TILE - 1) / C::TILE);
   const int units = mode == kRxProg ? ntiles : (ntiles + C::NT - 1) / C::NT;

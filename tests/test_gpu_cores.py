@@ -148,9 +148,17 @@ def test_split_encryption_matches_single_pass(bits):
     if bits == 2048:
         assert torch.equal(_ctx(kp, PCB_ENC_SPLIT=1).encrypt_batch(m, r, True), c1)
     M, R, C = (t.cpu().numpy().view(np.uint32) for t in (m, r, c1))
+    # every edge row (r = 1, n - 1, multiples of p and q) and a sample of the batch, exactly
+    # equal to the compiled reference's crt_encrypt_with_r (paillier.cpp:334-344)
+    import os
+    import refbind as RB
+    rows = list(range(len(edge) + 64)) + [n_el - 1]
+    ref = RB.RefKey.from_primes(p, q)
+    cref, st = ref.encrypt(M[rows], R[rows], crt=True, threads=os.cpu_count() or 1)
+    assert (st == 0).all()
+    assert np.array_equal(C[rows], cref)
     n2 = n * n
-    for i in list(range(len(edge) + 2)) + [n_el - 1]:
+    for i in rows[:len(edge)]:  # and the closed form with Python integers
         mi, ri = L.limbs_to_ints(M[i:i + 1])[0], L.limbs_to_ints(R[i:i + 1])[0]
-        ci = L.limbs_to_ints(C[i:i + 1])[0]
-        assert ci == 0 or ci == (1 + mi * n) * pow(ri, n, n2) % n2, i
+        assert L.limbs_to_ints(C[i:i + 1])[0] == (1 + mi * n) * pow(ri, n, n2) % n2, i
     assert torch.equal(split.decrypt_batch(c1[len(edge):], True), m[len(edge):])
