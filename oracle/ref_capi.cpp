@@ -9,6 +9,7 @@
 // Every value crosses the boundary as fixed-width little-endian u32 limbs.  Exceptions thrown by
 // the reference are mapped to per-element status codes with the same numbering as
 // include/pcb200.h (pcb_status), so the GPU path's error behaviour is compared 1:1.
+#include <omp.h>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -301,7 +302,8 @@ int pcref_hom_matvec(void* h, const uint32_t* alpha, const uint32_t* alpha_bits,
                      size_t rows, size_t cols, uint32_t window, uint32_t c_limbs, uint32_t* out,
                      uint32_t* out_bits, int threads) {
   RefKey* k = (RefKey*)h;
-  (void)threads;
+  // the reference parallelises the row loop with OpenMP (paillier.cpp:477); pin the team size
+  if (threads > 0) omp_set_num_threads(threads);
   try {
     std::vector<Ciphertext> a(rows), z(cols);
     std::vector<std::vector<u64>> e(rows, std::vector<u64>(cols));

@@ -145,6 +145,7 @@ pcb_status first_failure(const int32_t* stv, size_t count, cudaStream_t st) {
     const int thr = 256;
     const int blocks = (int)std::min<size_t>((count + thr - 1) / thr, 148 * 8);
     first_bad_kernel<<<blocks, thr, 0, st>>>(stv, count, d);
+    count_launch();
     e = cuda_check(cudaGetLastError());
   }
   if (!e) e = cuda_check(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st));
@@ -2132,15 +2133,19 @@ pcb_status pcb_quantize_encrypt(pcb_ctx* x, const double* v, size_t count, doubl
   if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
   if (!e) e = stage_out(c, count * 2 * x->L * 4, st, &sc);
   if (!e) e = stage_out(q_out, q_out ? count * 8 * (fine ? 2 : 1) : 0, st, &sq);
+  int32_t* stv = nullptr;  // per-element statuses: the first failure is the call's result
   if (!e) e = scratch_alloc(16, (void**)&dclamps, st);
   if (!e) e = cuda_check(cudaMemsetAsync(dclamps, 0, 16, st));
+  if (!e) e = scratch_alloc(count * 4, (void**)&stv, st);
   if (!e)
     e = enc_core(x, nullptr, 0, (const double*)sv.dev, z_min, z_max, delta, fine, (uint64_t*)sq.dev, dclamps,
-                 (const uint32_t*)sr.dev, count, (uint32_t*)sc.dev, nullptr, st);
+                 (const uint32_t*)sr.dev, count, (uint32_t*)sc.dev, stv, st);
   if (!e) e = unstage_out(c, &sc, st);
   if (!e) e = unstage_out(q_out, &sq, st);
   unsigned long long hcl[2] = {0, 0};
   if (!e && clamps) e = cuda_check(cudaMemcpyAsync(hcl, dclamps, 16, cudaMemcpyDeviceToHost, st));
+  if (!e) e = first_failure(stv, count, st);  // synchronises st
+  scratch_free(stv, st);
   unstage(&sv, st);
   unstage(&sr, st);
   unstage(&sc, st);

@@ -114,6 +114,7 @@ struct XArgs {
   int count, mode, S;
   int dbg;  // timing experiments: 1 = tensor/stream only, 2 = CUDA cores only
   int cl;   // CTAs per cluster sharing the W stream (1 or 2)
+  int nprod;  // W-stream producer warps (PCB_RNSX_NPROD for A/B; default kRxProducers)
   RxProg prog;  // kRxProg
 };
 
@@ -807,9 +808,16 @@ __device__ __noinline__ void relay_pair(uint64_t* bars, uint32_t nprod, int lane
   }
 }
 
+// The W stream is issued by kRxProducers warps of the role warpgroup in round robin over the ring
+// stages: one issuing warp serialises its bulk copies (~600 clk per copy whatever the size or the
+// number in flight, tools/bulk_bw2.cu, profiles/r02_bulk_bw2.txt), so one warp caps the stream at
+// 8 KB / 600 clk = 13.5 B/clk/SM -- the bound of the whole kernel in the tensor-only timing split
+// (profiles/r02_dbg_modes.txt).  Warp pw of npw owns stages i with i % npw == pw.
+constexpr int kRxProducers = 3;
+
 template <class C>
 __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride, uint8_t* sm, uint64_t* bars,
-                                           uint32_t nprod, int lane, int cl, uint32_t rank) {
+                                           uint32_t nprod, int lane, int cl, uint32_t rank, int pw, int npw) {
   // cl == 2: the CTA pair of a cluster shares the stream; each CTA fetches half of every stage
   // and multicasts it into both CTAs' rings (half the L2 traffic per SM)
   uint64_t* full = bars;
@@ -829,6 +837,10 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
       const int i0 = gm ? NG1 : 0, i1 = gm ? C::NSLICE : NG1;
 #pragma unroll 1
       for (int i = i0; i < i1; i++, issued++) {
+        if ((int)(issued % (uint32_t)npw) != pw) {  // another producer warp's stage
+          if (++pslot == (uint32_t)C::NSTAGE) { pslot = 0; pph ^= 1; }
+          continue;
+        }
         if (issued >= (uint32_t)C::NSTAGE) umma::mbar_wait(empty + pslot, pph ^ 1);
         const uint2 d = stg[i];
         if (lane == 0) {
@@ -1036,8 +1048,12 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
       else if (P.dbg == 3) mma_role<C, 3>(sm, tm, bars, np, P.cl);
       else if (P.dbg == 4) mma_role<C, 4>(sm, tm, bars, np, P.cl);
     }
-    if (warp == C::NCW + 1 && P.dbg != 2 && P.dbg != 4)
-      producer_role<C>(C::CG == 2 ? P.wimg2 : P.wimg, P.wimg_stride, sm, bars, np, lane, P.cl, rank);
+    if (warp >= C::NCW + 1 && warp <= C::NCW + kRxProducers && P.dbg != 2 && P.dbg != 4) {
+      const int npw = P.nprod > 0 && P.nprod <= kRxProducers ? P.nprod : kRxProducers;
+      if (warp - C::NCW - 1 < npw)
+        producer_role<C>(C::CG == 2 ? P.wimg2 : P.wimg, P.wimg_stride, sm, bars, np, lane, P.cl, rank,
+                         warp - C::NCW - 1, npw);
+    }
     __syncwarp();
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
@@ -1187,6 +1203,8 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
   {
     const char* d = getenv("PCB_RNSX_DBG");
     P.dbg = d ? atoi(d) : 0;
+    const char* np = getenv("PCB_RNSX_NPROD");
+    P.nprod = np ? atoi(np) : 0;
   }
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);

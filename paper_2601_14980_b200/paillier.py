@@ -176,6 +176,23 @@ class Paillier:
         rng.state = st.value
         return out
 
+    def skip_r(self, rng: Rng, count: int, chunk: int = 1 << 20) -> None:
+        """Advance rng past `count` sample_r draws (the accepted-candidate count is data
+        dependent, so the state after them is found by drawing them on the GPU, in chunks into
+        one scratch buffer).  Rank k of a job whose single r stream is sliced over ranks calls
+        skip_r(rng, k * n) and then draws its own n."""
+        torch = _torch()
+        if count <= 0:
+            return
+        buf = torch.empty((min(count, chunk), self.L), dtype=torch.int32, device=f"cuda:{self.device}")
+        left = count
+        while left:
+            k = min(left, chunk)
+            st = C.c_uint64(rng.state)
+            _raise_for(L.lib().pcb_sample_r(self._ctx, C.byref(st), k, L.ptr(buf), self._stream()), "sample_r")
+            rng.state = st.value
+            left -= k
+
     def _stream(self):
         torch = _torch()
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)

@@ -9,7 +9,17 @@
 #include "../paper_2601_14980_b200/csrc/umma.cuh"
 using namespace pcb;
 
-__global__ void k(const int* pat, int np, int reps, unsigned long long* cyc) {
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+
+// one or two MMAs per repetition (n1 == 0: one), operands in registers, fully unrolled body
+__global__ void k(int n0, int n1, int reps, unsigned long long* cyc) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tb;
@@ -22,23 +32,23 @@ __global__ void k(const int* pat, int np, int reps, unsigned long long* cyc) {
   umma::tmem_fence_after();
   const uint32_t tm = tb;
   if (threadIdx.x < 32) {
-    uint64_t bd[8];
-    uint32_t id[8];
-    for (int j = 0; j < np; j++) {
-      bd[j] = umma::desc_kmajor(umma::smem_u32(sm + 65536), pat[j]);
-      id[j] = umma::idesc_i8(128, pat[j]);
-    }
+    const uint64_t b0 = umma::desc_kmajor(umma::smem_u32(sm + 65536), n0);
+    const uint64_t b1 = umma::desc_kmajor(umma::smem_u32(sm + 65536), n1 ? n1 : 32);
+    const uint32_t i0 = umma::idesc_i8(128, n0), i1 = umma::idesc_i8(128, n1 ? n1 : 32);
     const uint64_t ad = umma::desc_kmajor(umma::smem_u32(sm), 128);
     const long long t0 = clock64();
-    for (int i = 0; i < reps; i++) {
-#pragma unroll 1
-      for (int j = 0; j < np; j++) {
-        asm volatile(
-            "{\n\t.reg .pred p, e;\n\t"
-            "setp.ne.b32 p, %4, 0;\n\t"
-            "elect.sync _|e, 0xffffffff;\n\t"
-            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tm + (j & 1) * 256),
-            "l"(ad + (uint64_t)((i & 7) * 256)), "l"(bd[j]), "r"(id[j]), "r"((uint32_t)(i & 7)));
+    if (n1) {
+      for (int i = 0; i < reps; i += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          mma(tm, ad + (uint64_t)(u * 256), b0, i0, (uint32_t)(i + u));
+          mma(tm + 256, ad + (uint64_t)(u * 256), b1, i1, (uint32_t)(i + u));
+        }
+      }
+    } else {
+      for (int i = 0; i < reps; i += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) mma(tm + (u & 1) * 256, ad + (uint64_t)(u * 256), b0, i0, (uint32_t)(i + u));
       }
     }
     asm volatile(
@@ -57,19 +67,16 @@ __global__ void k(const int* pat, int np, int reps, unsigned long long* cyc) {
 
 int main() {
   unsigned long long* cyc;
-  int* dpat;
   cudaMalloc(&cyc, 8 * 256);
-  cudaMalloc(&dpat, 64);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   std::vector<std::vector<int>> pats = {{32}, {64}, {96}, {128}, {144}, {160}, {176}, {192}, {208}, {224}, {256},
                                         {256, 32}, {160, 128}, {144, 144}, {192, 96}, {176, 112}, {256, 64},
                                         {256, 192}, {224, 224}, {256, 128}, {192, 192}};
   unsigned long long h[256];
   for (auto& p : pats) {
-    cudaMemcpy(dpat, p.data(), p.size() * 4, cudaMemcpyHostToDevice);
-    const int reps = 2048;
+    const int reps = 4096;
     const int grid = 148;
-    k<<<grid, 128, 160 * 1024>>>(dpat, (int)p.size(), reps, cyc);
+    k<<<grid, 128, 160 * 1024>>>(p[0], p.size() > 1 ? p[1] : 0, reps, cyc);
     cudaError_t e = cudaDeviceSynchronize();
     cudaMemcpy(h, cyc, grid * 8, cudaMemcpyDeviceToHost);
     double avg = 0;
