@@ -132,6 +132,7 @@ def run_admm(args, rank: int, world: int, local: int):
            "config": {"workload": "cfg3 LASSO N=4096, M=512 (recorded choice), K=8 blocks, 2048-bit key, Delta=1e15",
                       "iterations_timed": args.admm_iters, "warmup_iterations": args.admm_warmup,
                       "blocks_per_gpu": 8 // world if 8 % world == 0 else None},
+           "iter_seconds": [round(v, 5) for v in res.iter_seconds],
            "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall}
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = admm_cpu_leg(sess, res)
@@ -423,8 +424,8 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=2, help="timed end-to-end steps (>= 1)")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--admm-iters", type=int, default=3, help="timed cfg3 ADMM iterations (0 = skip)")
-    ap.add_argument("--admm-warmup", type=int, default=1)
+    ap.add_argument("--admm-iters", type=int, default=5, help="timed cfg3 ADMM iterations (0 = skip)")
+    ap.add_argument("--admm-warmup", type=int, default=2)
     ap.add_argument("--cfg4-n", type=int, default=1 << 22, help="cfg4 3072-bit values per job, sliced over ranks (0 = skip)")
     ap.add_argument("--cfg5-iters", type=int, default=0, help="timed cfg5 ADMM iterations (N=65536, 64 blocks; 0 = skip)")
     args = ap.parse_args()

@@ -16,6 +16,9 @@ Algorithm (Bajard-Imbert RNS Montgomery; approximate first base extension, exact
        = q + alpha M in B', alpha < 2k
     4. r~'_j = REDC(t~'_j C2_j) + REDC(qh'_j C3_j) (-2m' if >= 2m'),
        C2 = M^-1 2^32, C3 = N M^-1 2^64 (mod m'_j)
+       fused form (rnsx.cu rx_e1, round 2): GEMM 1 on W1'_ji = M_i C3_j mod m'_j gives
+       V'_j = sum_i xi_i W1'_ji = qh'_j C3_j 2^32 (mod m'_j), and r~'_j = REDC(t~'_j C2_j + V'_j)
+       in one REDC (t~' C2 + V' < 2 m'^2 + 2^49, so the result stays < 2m')
     5. xi'_j = REDC(r~'_j C4_j), C4 = M'_j^-1;  beta = floor(sum_j xi'_j / m'_j + 2^-20)
     6. r~_i = REDC(sum_j xi'_j W2_ij + beta W2_ik),  W2_ij = M'_j 2^64 mod m_i,
        W2_ik = -M' 2^64 mod m_i                                       (GEMM 2, exact)
@@ -88,6 +91,9 @@ class RnsCtx:
         self.C2 = np.array([pow(M, -1, m) * (1 << 32) % m for m in Bp], np.uint64)
         self.C3 = np.array([N * pow(M, -1, m) * (1 << 64) % m for m in Bp], np.uint64)
         self.C4 = np.array([pow(Mp // m, -1, m) for m in Bp], np.uint64)
+        C3i = [N * pow(M, -1, m) * (1 << 64) % m for m in Bp]
+        self.W1f = np.array([[(M // mi) * c3 % mj for mi in B] for mj, c3 in zip(Bp, C3i)], np.uint64)
+        self.fused = True  # the fused GEMM-1 epilogue of rnsx.cu (step 4, fused form)
         self.invBp = np.array([1.0 / m for m in Bp], np.float64)
         W2 = [[(Mp // mj) * (1 << 64) % mi for mj in Bp] + [(-Mp * (1 << 64)) % mi] for mi in B]
         self.W2 = np.array(W2, np.uint64)  # [i][j], column k = beta coefficient
@@ -137,9 +143,12 @@ class RnsCtx:
         ta = self.redc(xa * ya, mB, self.minvB)
         tb = self.redc(xb * yb, mBp, self.minvBp)
         xi = self.redc(ta * self.C1, mB, self.minvB)
-        qh = self.redc(self.gemm_bytes(xi, self.W1, mBp), mBp, self.minvBp)
-        r1 = self.redc(tb * self.C2, mBp, self.minvBp) + self.redc(qh * self.C3, mBp, self.minvBp)
-        r1 = np.where(r1 >= 2 * mBp, r1 - 2 * mBp, r1)
+        if self.fused:
+            r1 = self.redc(tb * self.C2 + self.gemm_bytes(xi, self.W1f, mBp), mBp, self.minvBp)
+        else:
+            qh = self.redc(self.gemm_bytes(xi, self.W1, mBp), mBp, self.minvBp)
+            r1 = self.redc(tb * self.C2, mBp, self.minvBp) + self.redc(qh * self.C3, mBp, self.minvBp)
+            r1 = np.where(r1 >= 2 * mBp, r1 - 2 * mBp, r1)
         xip = self.redc(r1 * self.C4, mBp, self.minvBp)
         S = float(np.sum(xip.astype(np.float64) * self.invBp))
         beta = int(np.floor(S + 2.0 ** -20))

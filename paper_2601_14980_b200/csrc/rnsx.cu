@@ -284,9 +284,9 @@ __device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t
         const uint4 rq = T.rc[w * 3 + 1], rr = T.rc[w * 3 + 2];
         const uint64_t V = (uint64_t)D[t] + ((uint64_t)D[QT + t] << 8) + ((uint64_t)D[2 * QT + t] << 16) +
                            ((uint64_t)D[3 * QT + t] << 24);
-        const uint32_t qh = redc(V, rq.x, rq.y);
-        uint32_t r = mulr(XQ[w], rq.z, rq.x, rq.y) + mulr(qh, rq.w, rq.x, rq.y);
-        if (r >= 2 * rq.x) r -= 2 * rq.x;
+        // GEMM 1 runs on W1' = M_i C3_j mod m'_j, so V = qh C3 2^32 (mod m'_j) and the new B'
+        // residue is one REDC of t' C2 + V (< 2m'^2 + 2^49 < 2^62: REDC < 2m', lazy)
+        const uint32_t r = redc((uint64_t)XQ[w] * rq.z + V, rq.x, rq.y);
         XQ[w] = r;
         xp[t] = mulr(r, rr.x, rq.x, rq.y);
         sp = __fma_rn((double)xp[t], __hiloint2double((int)rr.z, (int)rr.y), sp);  // beta needs 2^-20 only
@@ -470,6 +470,14 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
     if (!live) return 0;
     return (int)((P.m[(size_t)el * P.m_words + (w >> 3)] >> (4 * (w & 7))) & 15u);
   };
+  // op byte of the current step, loaded one step ahead: a byte LDG consumed right away by the
+  // step's branch put an L2 round trip on every step's critical path (ncu source view,
+  // profiles/r02_rnsx72_bench_ncu.json)
+  uint32_t op_cur = 0, op_next = 0;
+  const bool has_ops = P.mode != kRxPowVar && P.mode != kRxProg && P.ops != nullptr;
+  auto op_load = [&](int s) -> uint32_t {
+    return (has_ops && s >= s_main && s < s_fin) ? (uint32_t)P.ops[s - s_main + 1] : 0u;
+  };
   auto prep = [&](int s, uint32_t (&XB)[RPT], uint32_t (&XQ)[RPT], int tt, int el, bool live, bool& sq,
                   const uint32_t*& yb, int& yvs) {
     sq = false;
@@ -518,7 +526,7 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
       yb = tabp(park_x2, tt);
       yvs = tab_vs;
     } else if (s < s_fin) {
-      const uint8_t op = P.ops[s - s_main + 1];
+      const uint32_t op = op_cur;
       if (op == kOpSquare) {
         sq = true;
       } else {
@@ -601,8 +609,11 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
       bool sq;
       const uint32_t* yb;
       int yvs;
+      op_next = op_load(0);
 #pragma unroll 1
       for (int s = 0; s < nsteps; s++) {
+        op_cur = op_next;
+        op_next = op_load(s + 1);
         if (s > 0) {
           rx_e2<C>(XBa, T);
           post(s - 1, XBa, XQa, 0, ela, la);
@@ -643,8 +654,11 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
       bool sq;
       const uint32_t* yb;
       int yvs;
+      op_next = op_load(0);
 #pragma unroll 1
       for (int s = 0; s < nsteps; s++) {
+        op_cur = op_next;
+        op_next = op_load(s + 1);
 #pragma unroll
         for (int t = 0; t < NT; t++) {
           if (s > 0) {
@@ -672,8 +686,11 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
     const int el = tile * C::TILE + T.e;
     const bool live = el < P.count;
     uint32_t XB[RPT], XQ[RPT];
+    op_next = op_load(0);
 #pragma unroll 1
     for (int s = 0; s < nsteps; s++) {
+      op_cur = op_next;
+      op_next = op_load(s + 1);
       bool sq;
       const uint32_t* yb;
       int yvs;
@@ -1450,8 +1467,9 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
   // ncol(c) rows x 32 bytes in the K-major core-matrix layout (R = ncol(c))
   const int K1 = 4 * K, K2 = 4 * K + 32, KS1 = K1 / 32, KS2 = K2 / 32;
   std::vector<uint32_t> W1((size_t)K * K), W2((size_t)K * (K + 1));
+  // W1'_ji = M_i C3_j mod m'_j: the GEMM-1 epilogue's REDC(qh C3) folded into the matrix (rx_e1)
   for (int j = 0; j < K; j++)
-    for (int i = 0; i < K; i++) W1[(size_t)j * K + i] = (uint32_t)((uint64_t)mprod_mod(B, i, Bp[j]) * one[K + j] % Bp[j]);
+    for (int i = 0; i < K; i++) W1[(size_t)j * K + i] = (uint32_t)((uint64_t)mprod_mod(B, i, Bp[j]) * c3[j] % Bp[j]);
   for (int i = 0; i < K; i++) {
     const uint32_t m = B[i];
     for (int j = 0; j < K; j++) W2[(size_t)i * (K + 1) + j] = (uint32_t)((uint64_t)mprod_mod(Bp, j, m) * q64[i] % m);
