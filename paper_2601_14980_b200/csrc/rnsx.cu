@@ -38,6 +38,13 @@
 #include "rnsx.h"
 #include "umma.cuh"
 
+#ifndef PCB_RNSX_ROLE_WARPS
+#define PCB_RNSX_ROLE_WARPS 4
+#endif
+#ifndef PCB_RNSX_SLOT
+#define PCB_RNSX_SLOT 0  // 0: a third of the shared memory left for the ring (Cfg::SLOT)
+#endif
+
 namespace pcb {
 
 namespace {
@@ -57,6 +64,25 @@ __host__ __device__ constexpr int rnsx_qt(int ptc, int j) {
 __host__ __device__ constexpr int rnsx_slot(int ptc, int g, int j) {
   return (ptc % 4 == 0 || ptc == 2) ? g * ptc + 4 * j : (4 * j < ptc - 2 ? 16 * j + 4 * g : 16 * (ptc / 4) + 2 * g);
 }  // one <= 8 KB slice per stage
+// GEMM-output chunks: 64 primes (N = 256 columns) each and a ragged last one -- except K = 72,
+// which runs as 32 + 40 primes (N = 128 + 160).  The MMA costs max(N / 2, 32 + N / 4) clk at
+// M = 128, K = 32 B (tools/mma_mix.cu, profiles/r02_mma_mix.txt), so {256, 32} takes 171 clk per
+// k-step and {128, 160} 144 (the ideal), and 160-column buffers give a 3-deep TMEM ring.  Every
+// chunk but the last must be a multiple of 16 primes: a thread's residues are read in quads of 4.
+__host__ __device__ constexpr int rnsx_nchunks(int K) { return K == 72 ? 2 : (K + 63) / 64; }
+__host__ __device__ constexpr int rnsx_chunk_primes(int K, int c) {
+  return K == 72 ? (c == 0 ? 32 : 40) : (c < rnsx_nchunks(K) - 1 ? 64 : K - 64 * (rnsx_nchunks(K) - 1));
+}
+__host__ __device__ constexpr int rnsx_chunk_first(int K, int c) {
+  int f = 0;
+  for (int i = 0; i < c; i++) f += rnsx_chunk_primes(K, i);
+  return f;
+}
+__host__ __device__ constexpr int rnsx_max_chunk(int K) {
+  int m = 0;
+  for (int i = 0; i < rnsx_nchunks(K); i++) m = rnsx_chunk_primes(K, i) > m ? rnsx_chunk_primes(K, i) : m;
+  return m;
+}
 
 template <int K_, int NT_ = 1, int CG_ = 1>
 struct Cfg {
@@ -64,33 +90,49 @@ struct Cfg {
   // CG = 2: the CTA pair of a cluster runs every MMA as one cta_group::2 MMA (M = 256, the leader
   // issues); each CTA holds half of every W slice (N / 2 rows), so each SM streams half the bytes
   static constexpr int CG = CG_;
-  static constexpr int CP = 64, TPC = CP / G;  // primes per full chunk (256 TMEM columns), per thread
-  static constexpr int NC = (K + CP - 1) / CP, PL = K - CP * (NC - 1), PTL = PL / 4;
-  static constexpr int RPT = TPC * (NC - 1) + PTL;  // residues per thread per base
+  static constexpr int NC = rnsx_nchunks(K);      // GEMM-output chunks (rnsx_chunk_primes)
+  static constexpr int RPT = K / G;                // residues per thread per base
   static constexpr int NQ = (RPT + 3) / 4;         // 4-word vectors per thread per base
   static constexpr int NV = 2 * NQ;                // ... per operand (B quads, then B' quads)
   static constexpr int K1 = 4 * K, K2 = 4 * K + 32, KS1 = K1 / 32, KS2 = K2 / 32;
   static constexpr int NSLICE = NC * (KS1 + KS2);  // MMAs (and streamed slices) per product
   static constexpr int SPS = sps_for(K);           // slices per stream stage (one bulk copy)
   static constexpr int NSTG = (NSLICE + SPS - 1) / SPS;  // stages per product
-  static constexpr int SLOT = 8192 * SPS / CG;     // ring slot: SPS slices of <= 256 x 32 bytes (CG = 2: halves)
-  static constexpr int NB = 2, BUFC = 256, TMC = 512;  // TMEM ring: 2 buffers of 256 columns
-  static constexpr int TILE = 128, NCW = 16, NCT = 32 * NCW, NTHR = NCT + 128;  // + role warpgroup
+  // TMEM ring: buffers of the widest chunk (rounded to 32 columns), as many as fit in 512 (<= 3)
+  static constexpr int BUFC = (16 * (rnsx_max_chunk(K) / G) + 31) / 32 * 32, TMC = 512;
+  static constexpr int NB = TMC / BUFC > 3 ? 3 : TMC / BUFC;
+  // + role warps: one MMA issuer and W-stream producers; RW = 8 (two warpgroups at 32 registers)
+  // still leaves the compute warps their 112 (16 x 32 x 112 + 8 x 32 x 32 = 64 K registers)
+  static constexpr int TILE = 128, NCW = 16, NCT = 32 * NCW, RW = PCB_RNSX_ROLE_WARPS, NTHR = NCT + 32 * RW;
   static constexpr uint32_t ABLK = TILE * (K1 + K2);  // A1 + A2 of one tile
   static constexpr uint32_t OFF_A1 = 0, OFF_A2 = OFF_A1 + TILE * K1, OFF_CONS = NT * ABLK;
   static constexpr uint32_t OFF_S = OFF_CONS + K * 48, OFF_SLT = OFF_S + NT * G * TILE * 8;
   static constexpr uint32_t OFF_BAR = OFF_SLT + NSLICE * 16 + NSTG * 8;
   static constexpr uint32_t OFF_RING = (OFF_BAR + 512 + 1023) & ~1023u;
+  // ring slot (CG = 2: halves of one 8 KB slice).  A stage holds spc(c) consecutive slices of one
+  // chunk: one issuing warp serialises its bulk copies at ~600 clk each whatever their size
+  // (profiles/r02_bulk_bw2.txt), so fewer, bigger stages stream more bytes (20 KB stages: Dec
+  // 2048 -10 %, profiles/r02_rnsx_slot_ab.txt).  Default: a third of the ring space, capped at
+  // the largest chunk's GEMM-2 slices.
+  static constexpr uint32_t SLOT_AUTO_ = ((227u * 1024u - OFF_RING) / 3u) & ~1023u;
+  static constexpr uint32_t SLOT_CAP_ = (uint32_t)KS2 * 16u * (uint32_t)(rnsx_max_chunk(K) / 4) * 32u;
+  static constexpr int SLOT = CG == 2 ? 8192 / CG
+                              : (PCB_RNSX_SLOT > 0 ? PCB_RNSX_SLOT : (int)(SLOT_AUTO_ < SLOT_CAP_ ? SLOT_AUTO_ : SLOT_CAP_));
   static constexpr int NSTAGE_FIT = (int)((227u * 1024u - OFF_RING) / SLOT);
   static constexpr int NSTAGE = NSTAGE_FIT > 12 ? 12 : NSTAGE_FIT;
   static constexpr uint32_t SMEM = OFF_RING + NSTAGE * SLOT;
-  __host__ __device__ static constexpr int ptc(int c) { return c < NC - 1 ? TPC : PTL; }
+  __host__ __device__ static constexpr int ptc(int c) { return rnsx_chunk_primes(K, c) / G; }
+  __host__ __device__ static constexpr int cp0(int c) { return rnsx_chunk_first(K, c); }      // first prime
+  __host__ __device__ static constexpr int cw0(int c) { return rnsx_chunk_first(K, c) / G; }  // first thread residue
   __host__ __device__ static constexpr int ncol(int c) { return 16 * ptc(c); }
+  __host__ __device__ static constexpr int spc(int c) { return CG == 2 ? 1 : SLOT / (ncol(c) * 32); }
   // first prime (within chunk c) of quad j of thread group g: group-major when every group's run is
   // 16-byte aligned (ptc a multiple of 4, or 2); otherwise quad-major, groups interleaved per quad
   __host__ __device__ static constexpr int slot(int c, int g, int j) { return rnsx_slot(ptc(c), g, j); }
-  static_assert(PL % 8 == 0, "ragged chunk: a multiple of 8 primes (quads of 4, the last one of 2 or 4)");
-  static_assert(NSTAGE >= 4, "stream ring");
+  static_assert(K % 8 == 0 && rnsx_chunk_primes(K, NC - 1) % 8 == 0 && (NC == 1 || rnsx_chunk_first(K, NC - 1) % 16 == 0),
+                "chunks: the last a multiple of 8 primes, all others of 16 (thread residues in quads of 4)");
+  static_assert(NB >= 2, "TMEM ring");
+  static_assert(NSTAGE >= 3 && SLOT >= 8192 / CG, "stream ring");
   static_assert((3 * NSTAGE + 2 * NB + 2 * NT) * 8 + 4 <= 512, "barriers");
   static_assert(CG == 1 || (CG == 2 && NT == 1), "pair MMA only with one tile per CTA");
   static_assert(NT >= 1 && NT <= 3, "tiles in flight");
@@ -237,7 +279,7 @@ __device__ __forceinline__ void rx_s1(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
       constexpr int dummy = 0;
       (void)dummy;
       const int QT = rnsx_qt(ptc, j);  // last quad of a ragged chunk: 2 primes
-      const int w0 = C::TPC * c + 4 * j, q = w0 / 4;
+      const int w0 = C::cw0(c) + 4 * j, q = w0 / 4;
       uint32_t yb[4] = {}, yq[4] = {}, xi[4];
       if (!sq) {
         if (QT == 4) {
@@ -256,7 +298,7 @@ __device__ __forceinline__ void rx_s1(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
         xi[t] = mulr(mulr(XB[w], vb, ra.x, ra.y), ra.z, ra.x, ra.y);
         XQ[w] = mulr(XQ[w], vq, rq.x, rq.y);
       }
-      uint8_t* dst = A1 + umma::kmajor_off(T.e, 4 * (C::CP * c + C::slot(c, T.g, j)), C::TILE);
+      uint8_t* dst = A1 + umma::kmajor_off(T.e, 4 * (C::cp0(c) + C::slot(c, T.g, j)), C::TILE);
       if (QT == 4) stq<4>(dst, xi); else stq<2>(dst, xi);
     }
   }
@@ -280,7 +322,7 @@ __device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t
       if (QT == 4) d_quad<C, 4>(T, ptc, j, j == 0, j == nq - 1, D); else d_quad<C, 2>(T, ptc, j, j == 0, j == nq - 1, D);
 #pragma unroll
       for (int t = 0; t < QT; t++) {
-        const int w = C::TPC * c + 4 * j + t;
+        const int w = C::cw0(c) + 4 * j + t;
         const uint4 rq = T.rc[w * 3 + 1], rr = T.rc[w * 3 + 2];
         const uint64_t V = (uint64_t)D[t] + ((uint64_t)D[QT + t] << 8) + ((uint64_t)D[2 * QT + t] << 16) +
                            ((uint64_t)D[3 * QT + t] << 24);
@@ -291,7 +333,7 @@ __device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t
         xp[t] = mulr(r, rr.x, rq.x, rq.y);
         sp = __fma_rn((double)xp[t], __hiloint2double((int)rr.z, (int)rr.y), sp);  // beta needs 2^-20 only
       }
-      uint8_t* dst = A2 + umma::kmajor_off(T.e, 4 * (C::CP * c + C::slot(c, T.g, j)), C::TILE);
+      uint8_t* dst = A2 + umma::kmajor_off(T.e, 4 * (C::cp0(c) + C::slot(c, T.g, j)), C::TILE);
       if (QT == 4) stq<4>(dst, xp); else stq<2>(dst, xp);
     }
   }
@@ -322,7 +364,7 @@ __device__ __forceinline__ void rx_e2(uint32_t (&XB)[C::RPT], Thr<C>& T) {
       if (QT == 4) d_quad<C, 4>(T, ptc, j, j == 0, j == nq - 1, D); else d_quad<C, 2>(T, ptc, j, j == 0, j == nq - 1, D);
 #pragma unroll
       for (int t = 0; t < QT; t++) {
-        const int w = C::TPC * c + 4 * j + t;
+        const int w = C::cw0(c) + 4 * j + t;
         const uint4 ra = T.rc[w * 3];
         const uint64_t V = (uint64_t)D[t] + ((uint64_t)D[QT + t] << 8) + ((uint64_t)D[2 * QT + t] << 16) +
                            ((uint64_t)D[3 * QT + t] << 24);
@@ -446,8 +488,8 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
               const int ptc = C::ptc(c);
 #pragma unroll
               for (int j = 0; j < (ptc + 3) / 4; j++) {
-                const int QT = rnsx_qt(ptc, j), w0 = C::TPC * c + 4 * j;
-                uint32_t* d = o + C::CP * c + C::slot(c, T.g, j);
+                const int QT = rnsx_qt(ptc, j), w0 = C::cw0(c) + 4 * j;
+                uint32_t* d = o + C::cp0(c) + C::slot(c, T.g, j);
                 if (QT == 4) stq<4>(d, &XQ[w0]); else stq<2>(d, &XQ[w0]);
               }
             }
@@ -579,8 +621,8 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
           const int ptc = C::ptc(c);
 #pragma unroll
           for (int j = 0; j < (ptc + 3) / 4; j++) {
-            const int QT = rnsx_qt(ptc, j), w0 = C::TPC * c + 4 * j;
-            uint32_t* d = o + C::CP * c + C::slot(c, T.g, j);
+            const int QT = rnsx_qt(ptc, j), w0 = C::cw0(c) + 4 * j;
+            uint32_t* d = o + C::cp0(c) + C::slot(c, T.g, j);
             if (QT == 4) stq<4>(d, &XQ[w0]); else stq<2>(d, &XQ[w0]);
           }
         }
@@ -830,11 +872,12 @@ __device__ __noinline__ void relay_pair(uint64_t* bars, uint32_t nprod, int lane
 // number in flight, tools/bulk_bw2.cu, profiles/r02_bulk_bw2.txt), so one warp caps the stream at
 // 8 KB / 600 clk = 13.5 B/clk/SM -- the bound of the whole kernel in the tensor-only timing split
 // (profiles/r02_dbg_modes.txt).  Warp pw of npw owns stages i with i % npw == pw.
-constexpr int kRxProducers = 3;
+constexpr int kRxProducers = PCB_RNSX_ROLE_WARPS - 1;
 
 template <class C>
 __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride, uint8_t* sm, uint64_t* bars,
-                                           uint32_t nprod, int lane, int cl, uint32_t rank, int pw, int npw) {
+                                           uint32_t nprod, int lane, int cl, uint32_t rank, int pw, int npw,
+                                           bool multi_slice) {
   // cl == 2: the CTA pair of a cluster shares the stream; each CTA fetches half of every stage
   // and multicasts it into both CTAs' rings (half the L2 traffic per SM)
   uint64_t* full = bars;
@@ -843,39 +886,46 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
   const uint2* stg = reinterpret_cast<const uint2*>(sm + C::OFF_SLT + C::NSLICE * 16);
   // every SM streams the same matrices: spread the reads over kRxReplicas copies (L2 slices)
   const uint8_t* wimg = wimg0 + (size_t)(blockIdx.x % kRxReplicas) * wstride;
-  static_assert(C::SPS == 1, "one slice per stage: stages never straddle a GEMM");
-  constexpr int NG1 = C::NC * C::KS1;
+  // stages: spc consecutive slices of one chunk (contiguous in the image; every slice of a chunk
+  // has the same size); the debug interpreter (mma_role, dbg 1/3) and the CTA pair use one slice
   uint32_t issued = 0, pslot = 0, pph = 0;
 #pragma unroll 1
   for (uint32_t pr = 0; pr < nprod; pr++) {
 #pragma unroll 1
     for (int seg = 0; seg < 2 * C::NT; seg++) {  // G1 per tile, then G2 per tile (MMA issue order)
       const int gm = seg / C::NT;
-      const int i0 = gm ? NG1 : 0, i1 = gm ? C::NSLICE : NG1;
+      const int ks = gm ? C::KS2 : C::KS1;
+      int i0 = gm ? C::NC * C::KS1 : 0;
+#pragma unroll
+      for (int c = 0; c < C::NC; c++) {
+        const int sp = multi_slice ? C::spc(c) : 1;
 #pragma unroll 1
-      for (int i = i0; i < i1; i++, issued++) {
-        if ((int)(issued % (uint32_t)npw) != pw) {  // another producer warp's stage
-          if (++pslot == (uint32_t)C::NSTAGE) { pslot = 0; pph ^= 1; }
-          continue;
-        }
-        if (issued >= (uint32_t)C::NSTAGE) umma::mbar_wait(empty + pslot, pph ^ 1);
-        const uint2 d = stg[i];
-        if (lane == 0) {
-          umma::mbar_arrive_expect_tx(full + pslot, C::CG == 2 ? d.y >> 1 : d.y);
-          if (C::CG == 2) {  // wimg is the split-halves image: this CTA's half of the slice
-            const uint32_t half = d.y >> 1;
-            umma::bulk_g2s(ring + pslot * C::SLOT, wimg + (size_t)d.x * 16 + rank * half, half, full + pslot);
-            (void)cl;
-          } else if (cl == 2) {
-            const uint32_t half = d.y >> 1;
-            umma::bulk_g2s_mc(ring + pslot * C::SLOT + rank * half, wimg + (size_t)d.x * 16 + rank * half, half,
-                              full + pslot, 0x3);
-          } else {
-            umma::bulk_g2s(ring + pslot * C::SLOT, wimg + (size_t)d.x * 16, d.y, full + pslot);
+        for (int k = 0; k < ks; k += sp, issued++) {
+          if ((int)(issued % (uint32_t)npw) != pw) {  // another producer warp's stage
+            if (++pslot == (uint32_t)C::NSTAGE) { pslot = 0; pph ^= 1; }
+            continue;
           }
+          if (issued >= (uint32_t)C::NSTAGE) umma::mbar_wait(empty + pslot, pph ^ 1);
+          const uint2 d = stg[i0 + k];
+          const uint32_t bytes = d.y * (uint32_t)(ks - k < sp ? ks - k : sp);
+          if (lane == 0) {
+            umma::mbar_arrive_expect_tx(full + pslot, C::CG == 2 ? bytes >> 1 : bytes);
+            if (C::CG == 2) {  // wimg is the split-halves image: this CTA's half of the slice
+              const uint32_t half = bytes >> 1;
+              umma::bulk_g2s(ring + pslot * C::SLOT, wimg + (size_t)d.x * 16 + rank * half, half, full + pslot);
+              (void)cl;
+            } else if (cl == 2) {
+              const uint32_t half = bytes >> 1;
+              umma::bulk_g2s_mc(ring + pslot * C::SLOT + rank * half, wimg + (size_t)d.x * 16 + rank * half, half,
+                                full + pslot, 0x3);
+            } else {
+              umma::bulk_g2s(ring + pslot * C::SLOT, wimg + (size_t)d.x * 16, bytes, full + pslot);
+            }
+          }
+          __syncwarp();
+          if (++pslot == (uint32_t)C::NSTAGE) { pslot = 0; pph ^= 1; }
         }
-        __syncwarp();
-        if (++pslot == (uint32_t)C::NSTAGE) { pslot = 0; pph ^= 1; }
+        i0 += ks;
       }
     }
   }
@@ -887,7 +937,6 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
 // slot release (one 8 KB slice per ring stage).
 template <class C>
 __device__ __noinline__ void mma_fast(uint8_t* sm, uint32_t tm, uint64_t* bars, uint32_t nprod, int cl) {
-  static_assert(C::SPS == 1, "one slice per stage");
   uint64_t* full = bars;
   uint64_t* empty = bars + C::NSTAGE;
   uint64_t* dfull = bars + 2 * C::NSTAGE;
@@ -915,19 +964,29 @@ __device__ __noinline__ void mma_fast(uint8_t* sm, uint32_t tm, uint64_t* bars, 
         (void)dummy;
         const uint32_t ncol = (uint32_t)C::ncol(c);
         const uint32_t idesc = umma::idesc_i8(C::TILE, (int)ncol);
+        const int sp = C::spc(c);  // slices per ring stage (one bulk copy)
         if (dcnt >= (uint32_t)C::NB) {
           umma::mbar_wait(dfree + dbi, dph ^ 1);
           umma::tmem_fence_after();
         }
         const uint32_t dt = tm + dbi * C::BUFC;
+        uint32_t boff = 0;
+        int ks_in = 0;
 #pragma unroll 1
         for (int k = 0; k < ks; k++) {
-          umma::mbar_wait(full + cslot, cph);
+          if (ks_in == 0) {
+            umma::mbar_wait(full + cslot, cph);
+            boff = 0;
+          }
           mma_elect(dt, hi | (uint64_t)(alo + (uint32_t)k * (2 * C::TILE * 16 / 16)),
-                    hi | (uint64_t)((bslot & 0x3FFFu) | (ncol << 16)), idesc, (uint32_t)k);
-          if (cl == 2) commit_elect_mc(empty + cslot, 0x3); else commit_elect(empty + cslot);
-          bslot += SLOT16;
-          if (++cslot == (uint32_t)C::NSTAGE) { cslot = 0; cph ^= 1; bslot = ring16; }
+                    hi | (uint64_t)(((bslot + boff) & 0x3FFFu) | (ncol << 16)), idesc, (uint32_t)k);
+          boff += ncol * 2;  // one slice: ncol rows x 32 bytes, in 16-byte units
+          if (++ks_in == sp || k == ks - 1) {
+            ks_in = 0;
+            if (cl == 2) commit_elect_mc(empty + cslot, 0x3); else commit_elect(empty + cslot);
+            bslot += SLOT16;
+            if (++cslot == (uint32_t)C::NSTAGE) { cslot = 0; cph ^= 1; bslot = ring16; }
+          }
         }
         commit_elect(dfull + dbi);
         dcnt++;
@@ -1069,7 +1128,7 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
       const int npw = P.nprod > 0 && P.nprod <= kRxProducers ? P.nprod : kRxProducers;
       if (warp - C::NCW - 1 < npw)
         producer_role<C>(C::CG == 2 ? P.wimg2 : P.wimg, P.wimg_stride, sm, bars, np, lane, P.cl, rank,
-                         warp - C::NCW - 1, npw);
+                         warp - C::NCW - 1, npw, P.dbg == 0 && C::CG == 1);
     }
     __syncwarp();
   } else {
@@ -1374,15 +1433,17 @@ bool rnsx_shape(int bits, int* K) {
 
 bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
   if (N.bit_length() > (size_t)(32 * S) || !N.is_odd() || K <= 0 || K > 144) return false;
-  const int G = 4, CP = 64, TPC = CP / G, NC = (K + CP - 1) / CP, PL = K - CP * (NC - 1), PTL = PL / 4;
-  if (PL % 8) return false;
-  (void)PTL;
-  auto ptc = [&](int c) { return c < NC - 1 ? TPC : PTL; };
-  const int RPT = TPC * (NC - 1) + PTL, NQ = (RPT + 3) / 4, NV = 2 * NQ;
+  const int G = 4, NC = rnsx_nchunks(K);
+  for (int c = 0; c < NC; c++)
+    if (rnsx_chunk_primes(K, c) % 8) return false;
+  auto ptc = [&](int c) { return rnsx_chunk_primes(K, c) / G; };
+  const int RPT = K / G, NQ = (RPT + 3) / 4, NV = 2 * NQ;
   // thread-local residue w of thread group g <-> prime index
   auto prime_of = [&](int g, int w) {
-    const int c = w / TPC, t = w % TPC;
-    return CP * c + rnsx_slot(ptc(c), g, t / 4) + t % 4;
+    int c = 0;
+    while (w >= rnsx_chunk_first(K, c + 1) / G && c + 1 < NC) c++;
+    const int t = w - rnsx_chunk_first(K, c) / G;
+    return rnsx_chunk_first(K, c) + rnsx_slot(ptc(c), g, t / 4) + t % 4;
   };
   std::vector<uint32_t> pr;
   for (uint32_t c = (1u << 30) - 1; pr.size() < 2 * (size_t)K; c -= 2)
@@ -1492,7 +1553,7 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
           // (full quads of 4 primes = 16 columns first; a ragged chunk's last quad may hold 2)
           const int g = nl / (4 * pt), r = nl % (4 * pt), j = r / 16, qt = pt - 4 * j < 4 ? pt - 4 * j : 4,
                     b = (r - 16 * j) / qt, t = (r - 16 * j) % qt;
-          const int o = CP * c + rnsx_slot(pt, g, j) + t;  // output prime (B' for GEMM 1, B for GEMM 2)
+          const int o = rnsx_chunk_first(K, c) + rnsx_slot(pt, g, j) + t;  // output prime (B' for GEMM 1, B for GEMM 2)
           const uint32_t m = gm ? B[o] : Bp[o];
           for (int kk2 = 0; kk2 < 32; kk2++) {
             const int k = 32 * s + kk2, src = k / 4, a = k % 4;
@@ -1603,7 +1664,7 @@ void rnsx_free(RnsXModulus* md) {
 }
 
 int rnsx_rec_words(const RnsXModulus& md) {
-  const int NC = (md.K + 63) / 64, RPT = 16 * (NC - 1) + (md.K - 64 * (NC - 1)) / 4;
+  const int RPT = md.K / 4;
   return 4 * 2 * ((RPT + 3) / 4) * 4;
 }
 
