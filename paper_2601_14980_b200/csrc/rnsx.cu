@@ -512,13 +512,23 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
     if (!live) return 0;
     return (int)((P.m[(size_t)el * P.m_words + (w >> 3)] >> (4 * (w & 7))) & 15u);
   };
-  // op byte of the current step, loaded one step ahead: a byte LDG consumed right away by the
-  // step's branch put an L2 round trip on every step's critical path (ncu source view,
-  // profiles/r02_rnsx72_bench_ncu.json)
-  uint32_t op_cur = 0, op_next = 0;
+  // Op bytes of the exponent schedule, 32 steps per warp-wide vector: lane l holds the op of step
+  // base + l, the next vector is loaded 32 steps ahead and the current op comes out of a shuffle.
+  // (A scalar byte load consumed by the step's branch -- or prefetched one step ahead into a
+  // uniform register, which the compiler did right after the load -- put an L2 round trip on
+  // every step's critical path; ncu source view, profiles/r02_rnsx72_bench_ncu.json.)
   const bool has_ops = P.mode != kRxPowVar && P.mode != kRxProg && P.ops != nullptr;
-  auto op_load = [&](int s) -> uint32_t {
+  uint32_t op_cur = 0, opv_cur = 0, opv_next = 0;
+  auto opv_load = [&](int s0) -> uint32_t {
+    const int s = s0 + T.lane;
     return (has_ops && s >= s_main && s < s_fin) ? (uint32_t)P.ops[s - s_main + 1] : 0u;
+  };
+  auto op_step = [&](int s) {
+    if ((s & 31) == 0) {
+      opv_cur = s == 0 ? opv_load(0) : opv_next;
+      opv_next = opv_load(s + 32);
+    }
+    op_cur = __shfl_sync(0xffffffffu, opv_cur, s & 31);
   };
   auto prep = [&](int s, uint32_t (&XB)[RPT], uint32_t (&XQ)[RPT], int tt, int el, bool live, bool& sq,
                   const uint32_t*& yb, int& yvs) {
@@ -651,11 +661,9 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
       bool sq;
       const uint32_t* yb;
       int yvs;
-      op_next = op_load(0);
 #pragma unroll 1
       for (int s = 0; s < nsteps; s++) {
-        op_cur = op_next;
-        op_next = op_load(s + 1);
+        op_step(s);
         if (s > 0) {
           rx_e2<C>(XBa, T);
           post(s - 1, XBa, XQa, 0, ela, la);
@@ -696,11 +704,9 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
       bool sq;
       const uint32_t* yb;
       int yvs;
-      op_next = op_load(0);
 #pragma unroll 1
       for (int s = 0; s < nsteps; s++) {
-        op_cur = op_next;
-        op_next = op_load(s + 1);
+        op_step(s);
 #pragma unroll
         for (int t = 0; t < NT; t++) {
           if (s > 0) {
@@ -728,11 +734,9 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
     const int el = tile * C::TILE + T.e;
     const bool live = el < P.count;
     uint32_t XB[RPT], XQ[RPT];
-    op_next = op_load(0);
 #pragma unroll 1
     for (int s = 0; s < nsteps; s++) {
-      op_cur = op_next;
-      op_next = op_load(s + 1);
+      op_step(s);
       bool sq;
       const uint32_t* yb;
       int yvs;

@@ -1,0 +1,75 @@
+"""Summarise an ncu --set full capture of the bench's dominant kernel (tools/gpu_bench_profile.sh)
+into profiles/<name>.json: DRAM traffic per launch, pipe utilisation, stall samples and where the
+long-scoreboard stalls sit.  Usage: python tools/ncu_bench_summary.py gpurun_out/r02_rnsx72_bench.ncu-rep out.json"""
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep, out = sys.argv[1], sys.argv[2]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+d = dict(zip(rows[0], rows[2]))
+f = lambda k: float(d[k])  # noqa: E731
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(io.StringIO(src)))
+h2 = rows[1]
+data = [dict(zip(h2, r)) for r in rows[2:] if len(r) == len(h2)]
+
+
+def g(x):
+    try:
+        return float(x)
+    except ValueError:
+        return 0.0
+
+
+reasons = [c for c in h2 if c.startswith("stall_") and "Not Issued" not in c]
+tot = {r: sum(g(x[r]) for x in data) for r in reasons}
+lsb_bar = lsb_ld = lsb_other = 0.0
+prev = ""
+for x in data:
+    s = x["Source"].strip()
+    v = g(x["stall_long_sb"])
+    if "BRA" in s and "PHASECHK" in prev:
+        lsb_bar += v
+    elif any(t in prev for t in ("LDG", "LDL")) or any(t in s for t in ("LDG", "LDL")):
+        lsb_ld += v
+    else:
+        lsb_other += v
+    prev = s
+opc = collections.Counter()
+for x in data:
+    s = x["Source"].strip()
+    op = (s.split()[1] if s.startswith("@") else s.split()[0]).split(".")[0]
+    opc[op] += g(x["Warp Stall Sampling (All Samples)"])
+res = {
+    "kernel": d.get("Kernel Name"),
+    "source": "ncu --set full --clock-control none --import-source on -k regex:rnsx_kernel --launch-skip 1 -c 1 "
+              "python bench.py --steps 1 --warmup 1 --no-cpu-baseline --admm-iters 0 --cfg4-n 0 --e2e-steps 1 "
+              "(tools/gpu_bench_profile.sh): stage 2 of the split CRT Enc of the p half, (1+mn) u^p mod p^2, 2^20 values",
+    "duration_ms": f("gpu__time_duration.sum"),
+    "dram_bytes_read": f("dram__bytes_read.sum") * 1e9, "dram_bytes_write": f("dram__bytes_write.sum") * 1e9,
+    "traffic_bytes_per_launch": (f("dram__bytes_read.sum") + f("dram__bytes_write.sum")) * 1e9,
+    "algorithmic_io_bytes_per_launch": 1048576 * (32 * 4 + 72 * 4),
+    "l2_hit_rate_pct": f("lts__t_sector_hit_rate.pct"),
+    "pipes": {"issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+              "fma_pipe_pct": f("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+              "alu_pipe_pct": f("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+              "tensor_pipe_pct": f("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+              "shared_pipe_pct": f("sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active"),
+              "sm_clock_ghz": f("sm__cycles_elapsed.avg.per_second")},
+    "stall_samples": {k.replace("stall_", ""): v for k, v in sorted(tot.items(), key=lambda t: -t[1]) if v},
+    "long_scoreboard_attribution": {"mbarrier_wait_loops": lsb_bar, "global/local loads and their first consumers": lsb_ld,
+                                    "other": lsb_other},
+    "samples_by_opcode_top": dict(opc.most_common(12)),
+    "note": "DRAM traffic = the per-thread sliding-window tables (18 entries x 2 tiles x 576 B per element, ~436 MB "
+            "live for the 37,888 resident elements, > the 126 MB L2), re-read on multiply steps at ~0.2 TB/s (3% of "
+            "HBM). Most long-scoreboard samples are the compute warps' mbarrier wait loops (SYNCS.PHASECHK -> BRA) "
+            "on TMEM chunks and A-tile hand-offs; the table loads are a minority.",
+}
+json.dump(res, open(out, "w"), indent=1)
+print(json.dumps({k: res[k] for k in ("duration_ms", "traffic_bytes_per_launch", "pipes", "long_scoreboard_attribution")}, indent=1))
