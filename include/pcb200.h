@@ -226,6 +226,35 @@ pcb_status pcb_decrypt_update_blocks_half(pcb_ctx* ctx, size_t nblocks, const ui
                                           double kappa, double* x, double* z, double* v, int32_t* status,
                                           pcb_stream stream);
 
+/* ---- asynchronous forms for a resident iteration loop --------------------------------------
+ * Same results as the calls above, for DEVICE pointers only and without any host synchronisation
+ * (the round-1 forms synchronised the stream up to three times per call).  Instead of returning
+ * per-element failures they record the first failing element's code in *err_dev (a device int32
+ * the caller zeroes; atomicCAS from 0, so the earliest-arriving failure wins) and the caller checks
+ * it once per iteration.  The call's own return value reports argument / launch errors only. */
+
+/* pcb_quantize without the host round trip: clamps_dev (nullable, device u64[2]) is ACCUMULATED
+ * {low, high}; a non-finite value sets *err_dev = PCB_E_SHAPE. */
+pcb_status pcb_quantize_async(const double* v, size_t count, double z_min, double z_max, double delta,
+                              int fine, uint64_t* q_out, uint64_t* clamps_dev, int32_t* err_dev,
+                              pcb_stream stream);
+
+/* pcb_edge_step_blocks without host synchronisation.  expo_bits: an upper bound of the bit length
+ * of every exponent (the largest Gamma2(B) entry, constant over a session; 0 = compute it, which
+ * synchronises once).  z_j or v_j >= n^2 sets *err_dev = PCB_E_CIPHER_RANGE. */
+pcb_status pcb_edge_step_blocks_async(pcb_ctx* ctx, size_t nblocks, const uint32_t* sizes,
+                                      const uint32_t* alpha, const uint64_t* expo, uint32_t expo_bits,
+                                      const uint32_t* zc, const uint32_t* vc, uint32_t window,
+                                      uint32_t* out, int32_t* err_dev, pcb_stream stream);
+
+/* pcb_decrypt_update_blocks without host synchronisation: rows whose decryption or range gate
+ * fails keep x / z / v and set *err_dev (PCB_E_NOT_UNIT, PCB_E_CIPHER_RANGE, PCB_E_RANGE_UPDATE). */
+pcb_status pcb_decrypt_update_blocks_async(pcb_ctx* ctx, size_t nblocks, const uint32_t* sizes,
+                                           const uint32_t* c, const uint64_t* rowsum,
+                                           const uint64_t* q_z, const uint64_t* q_nv, double z_min,
+                                           double z_max, double delta, double kappa, double* x,
+                                           double* z, double* v, int32_t* err_dev, pcb_stream stream);
+
 /* ---- generic primitive + measurement ------------------------------------------------------ */
 
 /* y_i = x_i^e mod m for an odd modulus m (m_limbs <= 96) and a batch-uniform exponent e —

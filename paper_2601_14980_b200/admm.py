@@ -151,6 +151,11 @@ class ShardedDriver:
     def step_block(self, k: int, t: int) -> int:  # updates x/z/v slices of block k; returns clamps
         raise NotImplementedError
 
+    def check_iteration(self, t: int) -> int:
+        """After the iteration's device work has completed: raise deferred errors, return clamps
+        counted on the device (backends whose steps never synchronise)."""
+        return 0
+
     def setup_all(self) -> int:
         """Setup of every block this rank owns (default: one block at a time)."""
         return sum(self.setup_block(k) for k in self.mine)
@@ -204,6 +209,7 @@ class ShardedDriver:
             res.objective.append(0.5 * float(r @ r) + cfg.lam * float(l1))
             if self.dev != "cpu":
                 torch.cuda.synchronize(self.dev)
+            res.clamps += self.check_iteration(t)
             res.iter_seconds.append(time.perf_counter() - t0)
             if record_trace:
                 res.x_trace.append(self._gather(self.x.clone()))
@@ -274,6 +280,30 @@ class EncryptedSession(ShardedDriver):
                                          L.ptr(q), cl, self._stream()), "quantize")
         return q, cl[0] + cl[1]
 
+    def _quantize_async(self, v, spec):
+        """Gamma2 on the device; clamps accumulate in clamps_dev, failures in err (no host sync)."""
+        import torch
+
+        q = torch.empty((v.shape[0],), dtype=torch.int64, device=v.device)
+        _raise_for(self.lib.pcb_quantize_async(L.ptr(v), v.shape[0], spec[0], spec[1], spec[2], 0, L.ptr(q),
+                                               L.ptr(self.clamps_dev), L.ptr(self.err), self._stream()), "quantize")
+        return q
+
+    def check_iteration(self, t: int) -> int:
+        """One read of the device flags per iteration (the stream is already synchronised by the
+        objective): the reference throws at the first bad element (ProtocolError /
+        invalid_argument / runtime_error, protocol.cpp:20-27, 264-266; paillier.cpp:322-356)."""
+        if self.n_own == 0:
+            return 0
+        code = int(self.err.item())
+        if code:
+            _raise_for(code, f"iteration {t}")
+        if int(self.bad.item()):
+            raise ValueError("encryption argument out of range (crt_encrypt_with_r, paillier.cpp:322-323)")
+        total = int(self.clamps_dev.sum().item())
+        new, self.clamps_seen = total - self.clamps_seen, total
+        return new
+
     def run(self, a, y, factors=None, spec=None, record_trace: bool = True) -> SessionResult:
         import torch
 
@@ -318,6 +348,10 @@ class EncryptedSession(ShardedDriver):
         self.st_pre = [torch.zeros(2 * n_own, dtype=torch.int32, device=self.dev) for _ in range(2)]
         self.st_enc = torch.zeros(2 * n_own, dtype=torch.int32, device=self.dev)
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        # asynchronous iteration (pcb_*_async): first failing element's code, clamps on the device
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.clamps_dev = torch.zeros(2, dtype=torch.int64, device=self.dev)
+        self.clamps_seen = 0
         self.rperm = torch.zeros(0, dtype=torch.int64, device=self.dev)
         if n_own == 0:
             return 0
@@ -328,6 +362,9 @@ class EncryptedSession(ShardedDriver):
             rows.append(q_b[at:at + c * c].reshape(c, c).sum(dim=1))
             at += c * c
         self.expo = q_b
+        # bit length bound of every Gamma2(B) exponent (constant over the session): the edge step
+        # then needs no per-call OR-reduction and read-back
+        self.expo_bits = int(q_b.max().item()).bit_length() if q_b.numel() else 1
         self.rowsum = torch.cat(rows).contiguous()
         r_a = torch.empty((n_own, self.L), dtype=torch.int32, device=self.dev)
         at = 0
@@ -446,7 +483,10 @@ class EncryptedSession(ShardedDriver):
             lo = self.own_lo
             W = 2 * self.L
             vin = torch.cat([self.z[lo:lo + n], -self.v[lo:lo + n]]).contiguous()
-            q, clamps = self._quantize(vin, spec, fine=False)
+            if cfg.variant == "collab":
+                q, clamps = self._quantize(vin, spec, fine=False)
+            else:
+                q = self._quantize_async(vin, spec)
             ct = torch.empty((2 * n, W), dtype=torch.int32, device=self.dev)
             if cfg.variant == "collab":
                 ct = self._collab_encrypt(q, self.rn[slot][:, : self.L].contiguous(), ct)
@@ -463,9 +503,9 @@ class EncryptedSession(ShardedDriver):
         if n:
             upd = torch.empty((n, W), dtype=torch.int32, device=self.dev)
             sz = self.own_sizes
-            _raise_for(self.lib.pcb_edge_step_blocks(self.edge._ctx, len(sz), sz.ctypes.data, L.ptr(self.alpha_hat),
-                                                     L.ptr(self.expo), L.ptr(ct[:n]), L.ptr(ct[n:]), cfg.window,
-                                                     L.ptr(upd), st), "edge step")
+            _raise_for(self.lib.pcb_edge_step_blocks_async(
+                self.edge._ctx, len(sz), sz.ctypes.data, L.ptr(self.alpha_hat), L.ptr(self.expo), self.expo_bits,
+                L.ptr(ct[:n]), L.ptr(ct[n:]), cfg.window, L.ptr(upd), L.ptr(self.err), st), "edge step")
             if cfg.variant == "collab":  # edge: delegated Dec powers; master: decrypt_with_half + update
                 px = self._collab_dec_powers(upd)
                 _raise_for(self.lib.pcb_decrypt_update_blocks_half(
@@ -473,12 +513,8 @@ class EncryptedSession(ShardedDriver):
                     L.ptr(q[:n]), L.ptr(q[n:]), spec[0], spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
                     L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None, st), "master update (collab)")
             else:
-                _raise_for(self.lib.pcb_decrypt_update_blocks(self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd),
-                                                              L.ptr(self.rowsum), L.ptr(q[:n]), L.ptr(q[n:]), spec[0],
-                                                              spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
-                                                              L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None,
-                                                              st), "master update")
-            # the update synchronised the session stream: the encryption statuses are ready
-            if int(self.bad.item()):
-                raise ValueError("encryption argument out of range (crt_encrypt_with_r, paillier.cpp:322-323)")
+                _raise_for(self.lib.pcb_decrypt_update_blocks_async(
+                    self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(self.rowsum), L.ptr(q[:n]),
+                    L.ptr(q[n:]), spec[0], spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
+                    L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), L.ptr(self.err), st), "master update")
         return clamps

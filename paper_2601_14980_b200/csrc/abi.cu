@@ -315,6 +315,9 @@ pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, doub
                            cudaStream_t stream);
 pcb_status launch_onepmn(const uint32_t* m, int ml, const uint32_t* rn, const uint32_t* n_dev, const uint32_t* n2_dev,
                          int L, uint32_t* out, int32_t* st, size_t count, cudaStream_t stream);
+pcb_status launch_quantize(const double* v, size_t count, double zmin, double zmax, double delta, int fine,
+                           uint64_t* q, unsigned long long* clamps, int32_t* err, cudaStream_t stream);
+pcb_status launch_status_flag(const int32_t* st, size_t count, int32_t* err, cudaStream_t stream);
 pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int32_t* st, size_t count,
                            cudaStream_t stream);
 pcb_status launch_update(const uint32_t* m, int L, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
@@ -1700,14 +1703,18 @@ static pcb_status matvec_rnsx(pcb_ctx* x, const uint32_t* alpha, const uint64_t*
   return e;
 }
 
+// bits_hint > 0: an upper bound of every exponent's bit length supplied by the caller (the
+// asynchronous edge step), so the OR-reduction and its host read-back are skipped
 static pcb_status matvec_core(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo_dev, const uint32_t* zv,
-                              size_t nblk, size_t rows_b, size_t cols_b, uint32_t* out, cudaStream_t st) {
+                              size_t nblk, size_t rows_b, size_t cols_b, uint32_t* out, cudaStream_t st,
+                              int bits_hint = 0) {
   const size_t wb = 2 * x->L * 4;
   const size_t rows = nblk * rows_b, cols = nblk * cols_b;
   if (rows == 0) return PCB_OK;
   if (cols_b == 0) return cuda_check(cudaMemcpyAsync(out, alpha, rows * wb, cudaMemcpyDeviceToDevice, st));
-  int maxbits = 0;
-  if (auto e = expo_max_bits(expo_dev, rows * cols_b, st, &maxbits)) return e;
+  int maxbits = bits_hint > 64 ? 64 : bits_hint;
+  if (maxbits <= 0)
+    if (auto e = expo_max_bits(expo_dev, rows * cols_b, st, &maxbits)) return e;
   const int nwin = maxbits ? (maxbits + kMatWin - 1) / kMatWin : 1;
   if (x->use_rx_n2 && nwin <= 15 && nblk * cols_b <= (1u << 20))
     return matvec_rnsx(x, alpha, expo_dev, zv, nblk, rows_b, cols_b, nwin, out, st);
@@ -1786,7 +1793,7 @@ pcb_status pcb_hom_matvec(pcb_ctx* x, const uint32_t* alpha, const uint64_t* exp
 // largest block (zero exponents select the Montgomery one, padded rows are dropped).
 static pcb_status edge_core(pcb_ctx* x, size_t nblk, const uint32_t* sizes, const uint32_t* alpha,
                             const uint64_t* expo, const uint32_t* zc, const uint32_t* vc, uint32_t* out,
-                            cudaStream_t st) {
+                            cudaStream_t st, int bits_hint = 0, int32_t* err_dev = nullptr) {
   const size_t wb = 2 * x->L * 4;
   size_t total = 0, cmax = 0, etotal = 0;
   for (size_t k = 0; k < nblk; k++) {
@@ -1801,12 +1808,16 @@ static pcb_status edge_core(pcb_ctx* x, size_t nblk, const uint32_t* sizes, cons
   pcb_status e = scratch_alloc(2 * total * 4, (void**)&stv, st);
   if (!e) e = launch_dec_prep(zc, x->d_n2, (int)x->L, stv, total, st);
   if (!e) e = launch_dec_prep(vc, x->d_n2, (int)x->L, stv + total, total, st);
-  std::vector<int32_t> hst(2 * total);
-  if (!e) e = cuda_check(cudaMemcpyAsync(hst.data(), stv, 2 * total * 4, cudaMemcpyDeviceToHost, st));
-  if (!e) e = cuda_check(cudaStreamSynchronize(st));
-  if (!e)
-    for (int32_t v : hst)
-      if (v != PCB_OK) e = PCB_E_CIPHER_RANGE;
+  if (err_dev) {  // asynchronous form: the caller reads the flag once per iteration
+    if (!e) e = launch_status_flag(stv, 2 * total, err_dev, st);
+  } else {
+    std::vector<int32_t> hst(2 * total);
+    if (!e) e = cuda_check(cudaMemcpyAsync(hst.data(), stv, 2 * total * 4, cudaMemcpyDeviceToHost, st));
+    if (!e) e = cuda_check(cudaStreamSynchronize(st));
+    if (!e)
+      for (int32_t v : hst)
+        if (v != PCB_OK) e = PCB_E_CIPHER_RANGE;
+  }
   // zv_j = z_j * v_j mod n^2 (hom_add, protocol.cpp:268-269), then the matvec (270-271)
   if (!e) e = scratch_alloc(total * wb, (void**)&zvd, st);
   std::vector<WStep> pa = prog_hom_add();
@@ -1814,7 +1825,7 @@ static pcb_status edge_core(pcb_ctx* x, size_t nblk, const uint32_t* sizes, cons
   bool uniform = true;
   for (size_t k = 0; k < nblk; k++) uniform = uniform && sizes[k] == cmax;
   if (!e && uniform) {
-    e = matvec_core(x, alpha, expo, zvd, nblk, cmax, cmax, out, st);
+    e = matvec_core(x, alpha, expo, zvd, nblk, cmax, cmax, out, st, bits_hint);
   } else if (!e) {
     uint32_t *ap = nullptr, *zp = nullptr, *op = nullptr;
     uint64_t* ep = nullptr;
@@ -1842,7 +1853,7 @@ static pcb_status edge_core(pcb_ctx* x, size_t nblk, const uint32_t* sizes, cons
       off += c;
       eoff += c * c;
     }
-    if (!e) e = matvec_core(x, ap, ep, zp, nblk, cmax, cmax, op, st);
+    if (!e) e = matvec_core(x, ap, ep, zp, nblk, cmax, cmax, op, st, bits_hint);
     off = 0;
     for (size_t k = 0; !e && k < nblk; k++) {
       if (sizes[k])
@@ -1993,6 +2004,75 @@ pcb_status pcb_decrypt_update_blocks(pcb_ctx* x, size_t nblocks, const uint32_t*
                                      double z_max, double delta, double kappa, double* xo, double* zo, double* vo,
                                      int32_t* status, pcb_stream stream) {
   return update_entry(x, nblocks, sizes, c, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, status, stream);
+}
+
+// ---- asynchronous iteration forms (include/pcb200.h): device pointers, no host sync ----------
+pcb_status pcb_edge_step_blocks_async(pcb_ctx* x, size_t nblocks, const uint32_t* sizes, const uint32_t* alpha,
+                                      const uint64_t* expo, uint32_t expo_bits, const uint32_t* zc,
+                                      const uint32_t* vc, uint32_t window, uint32_t* out, int32_t* err_dev,
+                                      pcb_stream stream) {
+  if (!x || (nblocks && !sizes) || !err_dev) return PCB_E_SHAPE;
+  if (window < 1 || window > 8) return PCB_E_SHAPE;
+  size_t total = 0;
+  for (size_t k = 0; k < nblocks; k++) total += sizes[k];
+  if (total == 0) return PCB_OK;
+  if (!alpha || !expo || !zc || !vc || !out) return PCB_E_SHAPE;
+  for (const void* p : {(const void*)alpha, (const void*)expo, (const void*)zc, (const void*)vc, (const void*)out,
+                        (const void*)err_dev})
+    if (!is_device_ptr(p)) return PCB_E_SHAPE;  // the asynchronous form never stages host memory
+  if (auto e = set_device(x)) return e;
+  return edge_core(x, nblocks, sizes, alpha, expo, zc, vc, out, (cudaStream_t)stream, (int)expo_bits, err_dev);
+}
+
+pcb_status pcb_quantize_async(const double* v, size_t count, double z_min, double z_max, double delta, int fine,
+                              uint64_t* q_out, uint64_t* clamps_dev, int32_t* err_dev, pcb_stream stream) {
+  if (count && (!v || !q_out || !err_dev)) return PCB_E_SHAPE;
+  if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
+    return PCB_E_SHAPE;  // check_spec (quantize.cpp:8-15)
+  if (count == 0) return PCB_OK;
+  if (!is_device_ptr(v) || !is_device_ptr(q_out) || !is_device_ptr(err_dev) || (clamps_dev && !is_device_ptr(clamps_dev)))
+    return PCB_E_SHAPE;
+  return launch_quantize(v, count, z_min, z_max, delta, fine, q_out, (unsigned long long*)clamps_dev, err_dev,
+                         (cudaStream_t)stream);
+}
+
+pcb_status pcb_decrypt_update_blocks_async(pcb_ctx* x, size_t nblk, const uint32_t* sizes, const uint32_t* c,
+                                           const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
+                                           double z_min, double z_max, double delta, double kappa, double* xo,
+                                           double* zo, double* vo, int32_t* err_dev, pcb_stream stream) {
+  if (!x || (nblk && !sizes) || !err_dev) return PCB_E_SHAPE;
+  std::vector<long long> seg(nblk + 1, 0);
+  for (size_t k = 0; k < nblk; k++) seg[k + 1] = seg[k] + sizes[k];
+  const size_t count = (size_t)seg[nblk];
+  if (count && (!c || !rowsum || !q_z || !q_nv || !xo || !zo || !vo)) return PCB_E_SHAPE;
+  if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
+    return PCB_E_SHAPE;
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (count == 0) return PCB_OK;
+  if (count > 0x7fffffffu) return PCB_E_SHAPE;
+  for (const void* p : {(const void*)c, (const void*)rowsum, (const void*)q_z, (const void*)q_nv, (const void*)xo,
+                        (const void*)zo, (const void*)vo, (const void*)err_dev})
+    if (!is_device_ptr(p)) return PCB_E_SHAPE;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* m = nullptr;
+  int32_t* stv = nullptr;
+  long long* segd = nullptr;
+  pcb_status e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = scratch_alloc(count * x->L * 4, (void**)&m, st);
+  if (!e) e = scratch_alloc(seg.size() * 8, (void**)&segd, st);
+  // pageable source: the driver stages it before returning, so `seg` may go out of scope
+  if (!e) e = cuda_check(cudaMemcpyAsync(segd, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, st));
+  if (!e) e = dec_core(x, c, count, m, stv, st);
+  if (!e)
+    e = launch_update(m, (int)x->L, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, stv, count, segd,
+                      (int)nblk, st);
+  if (!e) e = launch_status_flag(stv, count, err_dev, st);
+  scratch_free(stv, st);
+  scratch_free(m, st);
+  scratch_free(segd, st);
+  if (!e) x->pow_half += 2 * (uint64_t)count;
+  return e;
 }
 
 pcb_status pcb_decrypt_update_blocks_half(pcb_ctx* x, size_t nblocks, const uint32_t* sizes, const uint32_t* c,

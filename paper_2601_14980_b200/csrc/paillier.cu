@@ -406,6 +406,49 @@ pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, doub
   return cuda_check(cudaGetLastError());
 }
 
+// gamma2_vec / gamma1_vec alone (pcb_quantize_async): no plaintext limbs, no r / n checks; a
+// non-finite value records PCB_E_SHAPE in *err (clamp_in, quantize.cpp:18-19)
+__global__ void quantize_kernel(const double* v, int count, double zmin, double zmax, double delta, int fine,
+                                uint64_t* q, unsigned long long* clamps, int32_t* err) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    const double x = v[i];
+    uint64_t lo = 0, hi = 0;
+    if (!isfinite(x)) {
+      if (err) atomicCAS(err, 0, (int32_t)PCB_E_SHAPE);
+    } else if (fine) {
+      gamma1_dev(x, zmin, zmax, delta, clamps, lo, hi);
+    } else {
+      lo = gamma2_dev(x, zmin, zmax, delta, clamps);
+    }
+    if (fine) {
+      q[2 * (size_t)i] = lo;
+      q[2 * (size_t)i + 1] = hi;
+    } else {
+      q[i] = lo;
+    }
+  }
+}
+
+pcb_status launch_quantize(const double* v, size_t count, double zmin, double zmax, double delta, int fine,
+                           uint64_t* q, unsigned long long* clamps, int32_t* err, cudaStream_t stream) {
+  quantize_kernel<<<small_grid(count), 256, 0, stream>>>(v, (int)count, zmin, zmax, delta, fine, q, clamps, err);
+  count_launch();
+  return cuda_check(cudaGetLastError());
+}
+
+// per-element statuses -> the first failure recorded in *err (the asynchronous ABI forms)
+__global__ void status_flag_kernel(const int32_t* st, int count, int32_t* err) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+    if (st[i] != PCB_OK) atomicCAS(err, 0, st[i]);
+}
+
+pcb_status launch_status_flag(const int32_t* st, size_t count, int32_t* err, cudaStream_t stream) {
+  if (!err || count == 0) return PCB_OK;
+  status_flag_kernel<<<small_grid(count), 256, 0, stream>>>(st, (int)count, err);
+  count_launch();
+  return cuda_check(cudaGetLastError());
+}
+
 // Online half of an offline/online encryption (pcb_encrypt_rn): out = 1 + m n  (2L words, < n^2
 // when m < n), with the checks of crt_encrypt_with_r (paillier.cpp:330-336) applied to m and the
 // precomputed rn = r^n mod n^2 (0 < rn < n^2).  Failed elements get out = 0.

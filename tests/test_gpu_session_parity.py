@@ -233,3 +233,86 @@ def test_null_status_reports_first_failure():
         ph.decrypt_batch(cn)
     with pytest.raises(ValueError):
         ph.encrypt_rn_batch(bad, ph.encrypt_batch(torch.zeros_like(M[:, :1]), r))
+
+
+def test_async_iteration_entries_match_sync_and_flag_errors():
+    """pcb_quantize_async / pcb_edge_step_blocks_async / pcb_decrypt_update_blocks_async (no host
+    sync, errors in a device flag) give the synchronous forms' results, and flag the reference's
+    failures: non-finite value (quantize.cpp:18-19), ciphertext >= n^2 (protocol.cpp:264-266),
+    update above the range cap (protocol.cpp:20-27)."""
+    import torch
+
+    kp = P.keygen(P.Rng(KEY_SEED), 1024)
+    ph, pub = P.Paillier(kp), P.Paillier(P.PublicKey(kp.n, kp.key_bits))
+    lib = L.lib()
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    g = np.random.default_rng(3)
+    spec = (-3.0, 3.0, 1e15)
+    # quantize
+    v = torch.from_numpy(g.uniform(-4, 4, 500)).cuda()
+    q1 = torch.empty(500, dtype=torch.int64, device="cuda")
+    q2 = torch.empty_like(q1)
+    cl = (C.c_uint64 * 2)()
+    assert lib.pcb_quantize(L.ptr(v), 500, *spec, 0, L.ptr(q1), cl, stream) == 0
+    cld = torch.zeros(2, dtype=torch.int64, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    assert lib.pcb_quantize_async(L.ptr(v), 500, *spec, 0, L.ptr(q2), L.ptr(cld), L.ptr(err), stream) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(q1, q2) and cld.tolist() == [cl[0], cl[1]] and int(err.item()) == 0
+    v[17] = float("nan")
+    assert lib.pcb_quantize_async(L.ptr(v), 500, *spec, 0, L.ptr(q2), L.ptr(cld), L.ptr(err), stream) == 0
+    torch.cuda.synchronize()
+    assert int(err.item()) == L.PCB_E_SHAPE
+    # edge step over 2 blocks of 24
+    sizes = np.array([24, 24], np.uint32)
+    n2 = kp.n * kp.n
+    W = 2 * ph.L
+    mk = lambda k: torch.from_numpy(L.ints_to_limbs([int(x) for x in g.integers(1, 2**62, k)], W).view(np.int32)).cuda()  # noqa: E731
+    alpha, zc, vc = mk(48), mk(48), mk(48)
+    expo = torch.from_numpy(g.integers(0, 10**15, 2 * 24 * 24, dtype=np.uint64).view(np.int64)).cuda()
+    o1 = torch.empty((48, W), dtype=torch.int32, device="cuda")
+    o2 = torch.empty_like(o1)
+    assert lib.pcb_edge_step_blocks(pub._ctx, 2, sizes.ctypes.data, L.ptr(alpha), L.ptr(expo), L.ptr(zc), L.ptr(vc),
+                                    6, L.ptr(o1), stream) == 0
+    err.zero_()
+    assert lib.pcb_edge_step_blocks_async(pub._ctx, 2, sizes.ctypes.data, L.ptr(alpha), L.ptr(expo), 50, L.ptr(zc),
+                                          L.ptr(vc), 6, L.ptr(o2), L.ptr(err), stream) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and int(err.item()) == 0
+    zc[30] = torch.from_numpy(L.ints_to_limbs([n2 + 1], W).view(np.int32))[0].cuda()
+    assert lib.pcb_edge_step_blocks_async(pub._ctx, 2, sizes.ctypes.data, L.ptr(alpha), L.ptr(expo), 50, L.ptr(zc),
+                                          L.ptr(vc), 6, L.ptr(o2), L.ptr(err), stream) == 0
+    torch.cuda.synchronize()
+    assert int(err.item()) == L.PCB_E_CIPHER_RANGE
+    # decrypt + update: the range gate
+    cols = 8
+    zmin, zmax, delta = -2.0, 2.0, 1e15
+    cap = delta * delta / (zmax - zmin) + float(cols) * delta * 2.0 * delta
+    lim = int(cap * 1.000001 + 4.0)
+    qs = [0, 12345, lim - (1 << 40), 99, lim + (1 << 50), 7, 1 << 127, 5]
+    r = ph.sample_r_batch(P.Rng(3), cols)
+    c = ph.encrypt_batch(torch.from_numpy(L.ints_to_limbs(qs, ph.L).view(np.int32)).cuda(), r)
+    rowsum = torch.full((cols,), 1000, dtype=torch.int64, device="cuda")
+    qz = torch.full((cols,), 10, dtype=torch.int64, device="cuda")
+    qn = torch.full((cols,), 20, dtype=torch.int64, device="cuda")
+    outs = []
+    for fn in ("sync", "async"):
+        x = torch.full((cols,), 7.0, dtype=torch.float64, device="cuda")
+        z, vv = x.clone(), x.clone()
+        err.zero_()
+        one = np.array([cols], np.uint32)
+        if fn == "sync":
+            st = torch.zeros(cols, dtype=torch.int32, device="cuda")
+            rc = lib.pcb_decrypt_update_blocks(ph._ctx, 1, one.ctypes.data, L.ptr(c), L.ptr(rowsum), L.ptr(qz),
+                                               L.ptr(qn), zmin, zmax, delta, 1.0, L.ptr(x), L.ptr(z), L.ptr(vv),
+                                               L.ptr(st), stream)
+            assert rc == L.PCB_E_RANGE_UPDATE
+        else:
+            rc = lib.pcb_decrypt_update_blocks_async(ph._ctx, 1, one.ctypes.data, L.ptr(c), L.ptr(rowsum), L.ptr(qz),
+                                                     L.ptr(qn), zmin, zmax, delta, 1.0, L.ptr(x), L.ptr(z), L.ptr(vv),
+                                                     L.ptr(err), stream)
+            torch.cuda.synchronize()
+            assert rc == 0 and int(err.item()) == L.PCB_E_RANGE_UPDATE
+        outs.append((x.cpu(), z.cpu(), vv.cpu()))
+    for a_, b_ in zip(*outs):
+        assert torch.equal(a_, b_)
