@@ -518,3 +518,257 @@ class EncryptedSession(ShardedDriver):
                     L.ptr(q[n:]), spec[0], spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
                     L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), L.ptr(self.err), st), "master update")
         return clamps
+
+
+# ---- faithful trust: the private key on rank 0 only (north_star 5) -------------
+
+def rank_slice(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous near-equal slice [offset, offset + count) of `total` items for `rank` (the first
+    total % world ranks take one more): how a job-wide stream of values is sharded."""
+    base, extra = divmod(total, world)
+    count = base + (1 if rank < extra else 0)
+    return rank * base + min(rank, extra), count
+
+
+def fold_partials(part, world: int, group, fold):
+    """Aggregation exchange step: every rank holds its partial product
+    (1 x W int32 limb tensor); all-gather the G partials (G x W x 4 bytes over NVLink with NCCL)
+    and fold them with `fold` (G x W -> 1 x W, e.g. Paillier.aggregate_batch) on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return part.reshape(1, -1)
+    parts = torch.empty((world, part.numel()), dtype=part.dtype, device=part.device)
+    dist.all_gather_into_tensor(parts, part.reshape(1, -1).contiguous(), group=group)
+    return fold(parts).reshape(1, -1)
+
+
+class FaithfulDriver:
+    """Faithful-trust 3P-ADMM-PC2 across ranks: rank 0 is the master and the only holder of the
+    private key; edge k runs on rank floor(k G / K) with the public key.  Per iteration
+    (protocol.cpp:425-511 master, 257-275 edge):
+
+      rank 0      Gamma2 + Enc of [z ; -v] for every block, r from the master stream Rng(seed)
+                  in reference order (block k: c_k draws for z, then c_k for -v)
+      broadcast   the 2N enc_state ciphertexts (protocol.cpp:471-476) from rank 0
+      every rank  the edge step of its own blocks: hom_add + hom_matvec (protocol.cpp:264-271)
+      all-gather  the enc_update ciphertexts (protocol.cpp:273-275), padded per rank, reassembled
+                  in block order on rank 0
+      rank 0      Dec + range gate + inverse quantization + soft threshold (protocol.cpp:488-511)
+
+    Setup: every edge quantizes its own node factor and encrypts Gamma1(alpha) with its own stream
+    Rng(seed ^ mix k) (protocol.cpp:186-212); the Gamma2(B) row sums go to rank 0 (node_share,
+    protocol.cpp:214-218) through one all-gather.  The ciphertext arithmetic is the backend's
+    (FaithfulGpuBackend: the CUDA path; the CPU tests plug a Python-integer backend in), so the
+    exchange logic here is the same for NCCL over NVLink and for gloo.  Rank 0's x / z / v equal
+    the single-process session's bit for bit."""
+
+    def __init__(self, backend, cfg: SessionConfig, rank: int = 0, world: int = 1, group=None):
+        self.B, self.cfg, self.rank, self.world, self.group = backend, cfg, rank, world, group
+
+    def owner(self, k: int) -> int:
+        return k * self.world // self.cfg.nodes
+
+    def _gather_rows(self, rows_own, n_max: int, width: int):
+        """All-gather each rank's rows (n_own x width), padded to n_max, into block order."""
+        import torch
+        import torch.distributed as dist
+
+        if self.world == 1:
+            return rows_own
+        pad = torch.zeros((n_max, width), dtype=rows_own.dtype, device=rows_own.device)
+        pad[: rows_own.shape[0]] = rows_own
+        allr = torch.empty((self.world * n_max, width), dtype=rows_own.dtype, device=rows_own.device)
+        dist.all_gather_into_tensor(allr, pad, group=self.group)
+        out = []
+        for r in range(self.world):
+            n_r = sum(self.sizes[k] for k in range(self.cfg.nodes) if self.owner(k) == r)
+            out.append(allr[r * n_max: r * n_max + n_r])
+        return torch.cat(out)  # ranks own consecutive block ranges: rank order == block order
+
+    def run(self, a, y, factors, spec, record_trace: bool = True) -> SessionResult:
+        import torch
+        import torch.distributed as dist
+
+        cfg = self.cfg
+        n = a.shape[1]
+        self.sizes = split_columns(n, cfg.nodes)
+        self.offs = np.cumsum([0] + self.sizes[:-1]).tolist()
+        self.mine = [k for k in range(cfg.nodes) if self.owner(k) == self.rank]
+        n_max = max(sum(self.sizes[k] for k in range(cfg.nodes) if self.owner(k) == r) for r in range(self.world))
+        B = self.B
+        res = SessionResult(spec=spec)
+        # edge setup of the own blocks; row sums to the master
+        rowsum_own, clamps = B.setup_edges(self.mine, factors, self.sizes, spec, cfg)
+        res.clamps += clamps
+        rowsum = self._gather_rows(rowsum_own.reshape(-1, 1), n_max, 1).reshape(-1)
+        if self.rank == 0:
+            B.setup_master(self.sizes, spec, cfg)
+        dev = B.device
+        x = torch.zeros(n, dtype=torch.float64, device=dev)
+        z = torch.zeros(n, dtype=torch.float64, device=dev)
+        v = torch.zeros(n, dtype=torch.float64, device=dev)
+        W = B.width
+        for t in range(cfg.iters):
+            B.sync()
+            t0 = __import__("time").perf_counter()
+            if self.rank == 0:
+                ct, q = B.master_encrypt(z, v, t)
+            else:
+                ct, q = torch.empty((2 * n, W), dtype=torch.int32, device=dev), None
+            if self.world > 1:
+                dist.broadcast(ct, src=0, group=self.group)
+            upd_own = B.edge_step(self.mine, self.sizes, self.offs, ct)
+            upd = self._gather_rows(upd_own, n_max, W)
+            if self.rank == 0:
+                B.master_update(upd, q, rowsum, self.sizes, spec, cfg, x, z, v)
+                r = (a @ z) - y
+                res.objective.append(0.5 * float(r @ r) + cfg.lam * float(z.abs().sum()))
+                res.clamps += B.check_iteration(t)
+            B.sync()
+            res.iter_seconds.append(__import__("time").perf_counter() - t0)
+            if record_trace and self.rank == 0:
+                res.x_trace.append(x.clone())
+        if self.rank == 0:
+            res.x, res.z, res.v = (t_.cpu().numpy() for t_ in (x, z, v))
+            res.x_trace = [xt.cpu().numpy() for xt in res.x_trace]
+        return res
+
+
+class FaithfulGpuBackend:
+    """The CUDA path under FaithfulDriver: the master's private context lives on rank 0 only; the
+    edges use public contexts.  All calls are the asynchronous ABI forms on device tensors."""
+
+    def __init__(self, keys, rank: int, device: int = 0):
+        import torch
+
+        self.device = torch.device(f"cuda:{device}")
+        self.dev_index = device
+        self.lib = L.lib()
+        self.keys = keys if rank == 0 else None  # the private key never leaves rank 0
+        self.edge = Paillier(PublicKey(keys.n, keys.key_bits), device=device)
+        self.master = Paillier(keys, device=device) if rank == 0 else None
+        self.L = self.edge.L
+        self.width = 2 * self.L
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.clamps_dev = torch.zeros(2, dtype=torch.int64, device=self.device)
+        self.clamps_seen = 0
+
+    def _st(self):
+        import torch
+
+        return C.c_void_p(torch.cuda.current_stream(self.dev_index).cuda_stream)
+
+    def sync(self):
+        import torch
+
+        torch.cuda.synchronize(self.device)
+
+    def setup_edges(self, mine, factors, sizes, spec, cfg):
+        import torch
+
+        st = self._st()
+        n_own = sum(sizes[k] for k in mine)
+        self.n_own = n_own
+        if n_own == 0:
+            return torch.zeros(0, dtype=torch.int64, device=self.device), 0
+        b_all = torch.cat([torch.as_tensor(factors[k][0], dtype=torch.float64, device=self.device).reshape(-1)
+                           for k in mine]).contiguous()
+        q_b = torch.empty(b_all.numel(), dtype=torch.int64, device=self.device)
+        cl = (C.c_uint64 * 2)()
+        _raise_for(self.lib.pcb_quantize(L.ptr(b_all), b_all.numel(), spec[0], spec[1], spec[2], 0, L.ptr(q_b), cl,
+                                         st), "quantize B")
+        rows, at = [], 0
+        for k in mine:
+            c = sizes[k]
+            rows.append(q_b[at:at + c * c].reshape(c, c).sum(dim=1))
+            at += c * c
+        self.expo = q_b
+        self.expo_bits = int(q_b.max().item()).bit_length() or 1
+        r_a = torch.empty((n_own, self.L), dtype=torch.int32, device=self.device)
+        at = 0
+        for k in mine:
+            erng = Rng(cfg.seed ^ ((EDGE_SEED_MIX * (k + 1)) & MASK64))
+            s_ = C.c_uint64(erng.state)
+            _raise_for(self.lib.pcb_sample_r(self.edge._ctx, C.byref(s_), sizes[k], L.ptr(r_a[at:at + sizes[k]]), st),
+                       "sample_r")
+            at += sizes[k]
+        alpha = torch.cat([torch.as_tensor(factors[k][1], dtype=torch.float64, device=self.device)
+                           for k in mine]).contiguous()
+        self.alpha_hat = torch.empty((n_own, self.width), dtype=torch.int32, device=self.device)
+        cla = (C.c_uint64 * 2)()
+        _raise_for(self.lib.pcb_quantize_encrypt(self.edge._ctx, L.ptr(alpha), n_own, spec[0], spec[1], spec[2], 1,
+                                                 L.ptr(r_a), 0, L.ptr(self.alpha_hat), None, cla, st), "alpha")
+        self.own_sizes = np.array([sizes[k] for k in mine], dtype=np.uint32)
+        return torch.cat(rows).contiguous(), int(cl[0] + cl[1] + cla[0] + cla[1])
+
+    def setup_master(self, sizes, spec, cfg):
+        import torch
+
+        n = sum(sizes)
+        self.n = n
+        self.rng_r = Rng(cfg.seed)
+        perm_z, perm_v = [], []
+        offs = np.cumsum([0] + sizes[:-1]).tolist()
+        for k in range(len(sizes)):
+            o, c = offs[k], sizes[k]
+            perm_z.extend(range(2 * o, 2 * o + c))
+            perm_v.extend(range(2 * o + c, 2 * o + 2 * c))
+        self.rperm = torch.tensor(perm_z + perm_v, dtype=torch.int64, device=self.device)
+        self.rall = torch.empty((2 * n, self.L), dtype=torch.int32, device=self.device)
+        self.st_enc = torch.zeros(2 * n, dtype=torch.int32, device=self.device)
+        self.spec = spec
+        self.kappa = cfg.lam / cfg.rho
+
+    def master_encrypt(self, z, v, t):
+        import torch
+
+        st = self._st()
+        spec = self.spec
+        vin = torch.cat([z, -v]).contiguous()
+        q = torch.empty(vin.numel(), dtype=torch.int64, device=self.device)
+        _raise_for(self.lib.pcb_quantize_async(L.ptr(vin), vin.numel(), spec[0], spec[1], spec[2], 0, L.ptr(q),
+                                               L.ptr(self.clamps_dev), L.ptr(self.err), st), "quantize")
+        s_ = C.c_uint64(self.rng_r.state)
+        _raise_for(self.lib.pcb_sample_r(self.master._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
+                   "sample_r")
+        self.rng_r.state = s_.value
+        r = self.rall.index_select(0, self.rperm).contiguous()
+        ct = torch.empty((vin.numel(), self.width), dtype=torch.int32, device=self.device)
+        _raise_for(self.lib.pcb_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(r), vin.numel(), L.ptr(ct), 1,
+                                        L.ptr(self.st_enc), st), "enc_state")
+        return ct, q
+
+    def edge_step(self, mine, sizes, offs, ct):
+        import torch
+
+        if self.n_own == 0:
+            return torch.zeros((0, self.width), dtype=torch.int32, device=self.device)
+        n = ct.shape[0] // 2
+        lo = offs[mine[0]]
+        zc = ct[lo:lo + self.n_own]
+        vc = ct[n + lo:n + lo + self.n_own]
+        upd = torch.empty((self.n_own, self.width), dtype=torch.int32, device=self.device)
+        _raise_for(self.lib.pcb_edge_step_blocks_async(
+            self.edge._ctx, len(self.own_sizes), self.own_sizes.ctypes.data, L.ptr(self.alpha_hat), L.ptr(self.expo),
+            self.expo_bits, L.ptr(zc), L.ptr(vc), 6, L.ptr(upd), L.ptr(self.err), self._st()), "edge step")
+        return upd
+
+    def master_update(self, upd, q, rowsum, sizes, spec, cfg, x, z, v):
+        n = self.n
+        sz = np.array(sizes, dtype=np.uint32)
+        _raise_for(self.lib.pcb_decrypt_update_blocks_async(
+            self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(rowsum), L.ptr(q[:n]), L.ptr(q[n:]),
+            spec[0], spec[1], spec[2], self.kappa, L.ptr(x), L.ptr(z), L.ptr(v), L.ptr(self.err), self._st()),
+            "master update")
+
+    def check_iteration(self, t):
+        code = int(self.err.item())
+        if code:
+            _raise_for(code, f"iteration {t}")
+        if int(self.st_enc.ne(0).any().item()):
+            raise ValueError("encryption argument out of range (crt_encrypt_with_r, paillier.cpp:322-323)")
+        total = int(self.clamps_dev.sum().item())
+        new, self.clamps_seen = total - self.clamps_seen, total
+        return new

@@ -316,3 +316,18 @@ def test_async_iteration_entries_match_sync_and_flag_errors():
         outs.append((x.cpu(), z.cpu(), vv.cpu()))
     for a_, b_ in zip(*outs):
         assert torch.equal(a_, b_)
+
+
+def test_faithful_driver_gpu_backend_bit_exact():
+    """Faithful-trust session (FaithfulDriver + FaithfulGpuBackend: the private context exists on
+    rank 0 only, edges hold public contexts) -- one rank here -- bit-identical to the shadow."""
+    import torch
+
+    iters = 4
+    a, y, sizes, fac, spec = _problem(128, 256, 4, iters)
+    keys = P.keygen(P.Rng(KEY_SEED), 2048)
+    cfg = ADMM.SessionConfig(nodes=4, iters=iters, seed=SEED)
+    drv = ADMM.FaithfulDriver(ADMM.FaithfulGpuBackend(keys, 0, 0), cfg)
+    res = drv.run(torch.as_tensor(a, device="cuda"), torch.as_tensor(y, device="cuda"),
+                  [(torch.as_tensor(b, device="cuda"), torch.as_tensor(al, device="cuda")) for b, al in fac], spec)
+    _assert_trajectory(res, fac, sizes, spec, iters)
