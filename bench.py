@@ -139,6 +139,43 @@ def run_admm(args, rank: int, world: int, local: int):
     return out
 
 
+def run_admm_faithful(args, rank: int, world: int, local: int):
+    """cfg3 in faithful-trust mode (FaithfulDriver): the private key on rank 0 only; rank 0
+    encrypts and decrypts every block, the edge steps run on the block owners, ciphertexts cross
+    ranks by NCCL broadcast / all-gather.  Reported separately: rank 0 serialises
+    the whole master side."""
+    import torch
+    import torch.distributed as dist
+    from paper_2601_14980_b200 import admm as ADMM
+    from paper_2601_14980_b200 import paillier as P
+
+    a, y = gen_problem_fast(512, 4096, 0.1, 1)
+    keys = P.keygen(P.Rng(KEY_SEED), 2048)
+    iters = args.admm_warmup + args.admm_faithful_iters
+    cfg = ADMM.SessionConfig(nodes=8, iters=iters)
+    dev = torch.device(f"cuda:{local}")
+    at = torch.as_tensor(a, device=dev)
+    yt = torch.as_tensor(y, device=dev)
+    sizes = ADMM.split_columns(4096, 8)
+    offs = np.cumsum([0] + sizes[:-1]).tolist()
+    fac = [ADMM.node_factor(at[:, o:o + c], yt, 1.0, 8) for o, c in zip(offs, sizes)]
+    spec = torch.tensor(ADMM.session_bounds(fac, sizes, 1.0, 1.0, iters, 1.5, 1e15), dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.broadcast(spec, src=0)  # the master's QuantSpec (session_init, protocol.cpp:356-371)
+    spec = tuple(float(v) for v in spec.tolist())
+    drv = ADMM.FaithfulDriver(ADMM.FaithfulGpuBackend(keys, rank, local), cfg, rank=rank, world=world,
+                              group=dist.group.WORLD if world > 1 else None)
+    res = drv.run(at, yt, fac, spec, record_trace=False)
+    it = res.iter_seconds[args.admm_warmup:]
+    t = torch.tensor([float(np.mean(it))], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"metric": "3P-ADMM-PC2 sec/iteration (faithful trust: private key on rank 0)", "value": float(t.item()),
+            "unit": "s/iteration", "higher_is_better": False, "iter_seconds": [round(v, 5) for v in res.iter_seconds],
+            "config": {"workload": "cfg3 LASSO N=4096, M=512, K=8 blocks, 2048-bit key; enc_state broadcast + "
+                                   "enc_update all-gather over NCCL", "iterations_timed": len(it)}}
+
+
 def admm_cpu_leg(sess, res) -> dict:
     """cpu_baseline leg of the ADMM sub-line: the reference's CPU cost of one cfg3 iteration on
     this host (1 thread and all threads, admm_cpu_baseline), and the parity gate of the session's
@@ -197,6 +234,12 @@ def run_cfg5(args, rank: int, world: int, local: int):
             "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall}
 
 
+def ADMM_slice(total: int, world: int, rank: int):
+    from paper_2601_14980_b200 import admm as ADMM
+
+    return ADMM.rank_slice(total, world, rank)
+
+
 def run_cfg4(args, rank: int, world: int, local: int):
     """cfg4: Paillier-3072 CRT Enc + Dec of the job's `cfg4_n` values (default 2^22, BASELINE.json
     configs[3]) sliced over the ranks, then the homomorphic aggregation prod c_i mod n^2 (decrypting
@@ -218,14 +261,14 @@ def run_cfg4(args, rank: int, world: int, local: int):
             break
     kp = P.keypair_from_primes(p, q)
     ph = P.Paillier(kp, device=local)
-    n = args.cfg4_n // world
-    vals = splitmix_units(7, n, offset=rank * n) * 12.0 - 6.0
+    off, n = ADMM_slice(args.cfg4_n, world, rank)
+    vals = splitmix_units(7, n, offset=off) * 12.0 - 6.0
     q64 = np.round((vals + 6.0) / 12.0 * 1e15).astype(np.uint64)  # Gamma2-range plaintexts (< 2^50)
     m = torch.zeros((n, ph.L), dtype=torch.int32, device="cuda")
     m[:, 0] = torch.from_numpy((q64 & 0xFFFFFFFF).astype(np.uint32).view(np.int32)).cuda()
     m[:, 1] = torch.from_numpy((q64 >> 32).astype(np.uint32).view(np.int32)).cuda()
     rr = P.Rng(11)
-    ph.skip_r(rr, rank * n)
+    ph.skip_r(rr, off)
     r = ph.sample_r_batch(rr, n)
     torch.cuda.synchronize()
     w = min(n, 1 << 14)
@@ -244,13 +287,11 @@ def run_cfg4(args, rank: int, world: int, local: int):
     t_dec, d = phase(lambda: ph.decrypt_batch(c, True))
     ph.aggregate_batch(c[:w])
 
-    def agg():
-        part = ph.aggregate_batch(c).reshape(1, -1)
-        if world == 1:
-            return part
-        parts = torch.empty((world, part.shape[1]), dtype=part.dtype, device=part.device)
-        dist.all_gather_into_tensor(parts, part)  # G x 768 B over NVLink
-        return ph.aggregate_batch(parts).reshape(1, -1)
+    from paper_2601_14980_b200 import admm as ADMM
+
+    def agg():  # per-rank tree -> all-gather of the G partials (G x 768 B over NVLink) -> fold
+        return ADMM.fold_partials(ph.aggregate_batch(c), world, dist.group.WORLD if world > 1 else None,
+                                  ph.aggregate_batch)
 
     t_agg, tot = phase(agg)
     total = int(sum(int(v) for v in q64))
@@ -265,7 +306,7 @@ def run_cfg4(args, rank: int, world: int, local: int):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_enc, t_dec, t_agg = (float(v) for v in t.tolist())
-    nn = world * n
+    nn = args.cfg4_n
     return {"metric": "Paillier-3072 Enc+Dec pairs/s + aggregation (cfg4)", "value": nn / (t_enc + t_dec),
             "unit": "Enc+Dec pairs/s", "higher_is_better": True, "scaling": "strong",
             "enc_per_s": nn / t_enc, "dec_per_s": nn / t_dec, "aggregate_ciphertexts_per_s": nn / t_agg,
@@ -426,6 +467,7 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--admm-iters", type=int, default=5, help="timed cfg3 ADMM iterations (0 = skip)")
     ap.add_argument("--admm-warmup", type=int, default=2)
+    ap.add_argument("--admm-faithful-iters", type=int, default=3, help="timed faithful-trust cfg3 iterations (0 = skip)")
     ap.add_argument("--cfg4-n", type=int, default=1 << 22, help="cfg4 3072-bit values per job, sliced over ranks (0 = skip)")
     ap.add_argument("--cfg5-iters", type=int, default=0, help="timed cfg5 ADMM iterations (N=65536, 64 blocks; 0 = skip)")
     args = ap.parse_args()
@@ -584,6 +626,7 @@ def main() -> None:
     d2h = N * (2 * ph.L * 4 + ph.L * 4)   # ciphertexts out; plaintexts out
 
     admm = run_admm(args, rank, world, local) if args.admm_iters > 0 else None
+    admm_f = run_admm_faithful(args, rank, world, local) if args.admm_faithful_iters > 0 else None
     cfg4 = run_cfg4(args, rank, world, local) if args.cfg4_n > 0 else None
     cfg5 = run_cfg5(args, rank, world, local) if args.cfg5_iters > 0 else None
 
@@ -626,6 +669,7 @@ def main() -> None:
             "gpu_launches": int(gpu_launches),
             "clocks": clk,
             "admm": admm,
+            "admm_faithful": admm_f,
             "cfg4": cfg4,
             "cfg5": cfg5,
         }
