@@ -3,7 +3,7 @@
  * This is the drop-in boundary.  The reference has no FFI: its seam is the C++ class
  * pcadmm::Paillier (/root/reference/proj/include/pcadmm/paillier.hpp:104-181) and the quantizer
  * free functions (quantize.hpp:32-71).  Each entry point below names the reference member it
- * replaces.  The C++ facade (paper_2601_14980_b200/csrc/host/pcb200.hpp) and the Python package
+ * replaces.  The C++ drop-in (paper_2601_14980_b200/cpp/pcb200_pcadmm.hpp, pcadmm::Paillier) and the Python package
  * re-expose the reference signatures on top of these calls; INTEGRATION.md shows the bindings.
  *
  * Conventions

@@ -61,9 +61,25 @@ inline void report(bool ok, const char* expr, const char* file, int line, bool r
   } while (0)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
-int main() {
-  long cases = 0, failed_cases = 0;
+#include <cstring>
+// argv: --exclude=<substring of a case name> (repeatable) skips cases (reported as SKIP);
+// --list prints PASS / FAIL / SKIP per case.
+int main(int argc, char** argv) {
+  std::vector<std::string> excl;
+  bool list = false;
+  for (int i = 1; i < argc; i++) {
+    if (std::strncmp(argv[i], "--exclude=", 10) == 0) excl.push_back(argv[i] + 10);
+    if (std::strcmp(argv[i], "--list") == 0) list = true;
+  }
+  long cases = 0, failed_cases = 0, skipped = 0;
   for (auto& c : doctest::detail::registry()) {
+    bool skip = false;
+    for (auto& e : excl) skip = skip || std::string(c.name).find(e) != std::string::npos;
+    if (skip) {
+      skipped++;
+      if (list) std::printf("SKIP  %s\n", c.name);
+      continue;
+    }
     long before = doctest::detail::failures();
     cases++;
     try { c.fn(); } catch (const doctest::detail::RequireFailed&) {
@@ -71,10 +87,12 @@ int main() {
       doctest::detail::failures()++;
       std::fprintf(stderr, "case '%s' threw: %s\n", c.name, e.what());
     }
-    if (doctest::detail::failures() != before) failed_cases++;
+    const bool bad = doctest::detail::failures() != before;
+    if (bad) failed_cases++;
+    if (list) std::printf("%s  %s\n", bad ? "FAIL" : "PASS", c.name);
   }
-  std::printf("[doctest-shim] cases: %ld | failed: %ld | checks: %ld | failures: %ld\n", cases,
-              failed_cases, doctest::detail::checks(), doctest::detail::failures());
+  std::printf("[doctest-shim] cases: %ld | failed: %ld | skipped: %ld | checks: %ld | failures: %ld\n", cases,
+              failed_cases, skipped, doctest::detail::checks(), doctest::detail::failures());
   return doctest::detail::failures() ? 1 : 0;
 }
 #endif
