@@ -67,6 +67,13 @@ pcb_status pcb_random_prime(uint64_t* rng_state, uint32_t bits, uint32_t* out);
 pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t n_limbs,
                           const uint32_t* p, const uint32_t* q, uint32_t pq_limbs);
 void pcb_ctx_destroy(pcb_ctx* ctx);
+/* GMode::random_g (paillier.cpp:80-100): sets the generator g (g_limbs words, 1 < g < n^2,
+ * gcd(g, n) = 1, L(g^eps mod n^2) invertible mod n) of a context made by pcb_ctx_create.  The
+ * decryption constants are rebuilt from g (h_p = L_p(g^(p-1) mod p^2)^-1, mu = L(g^eps)^-1), and
+ * pcb_encrypt / pcb_encrypt_rn / pcb_finish_split_encrypt compute g^m mod n^2 on the device from
+ * the 64-bit digit powers g^(2^(64 j)) mod n^2.  g = n + 1 restores the binomial form.  The fused
+ * pcb_quantize_encrypt (the g = n + 1 hot path) returns PCB_E_UNSUPPORTED on a random-g context. */
+pcb_status pcb_ctx_set_generator(pcb_ctx* ctx, const uint32_t* g, uint32_t g_limbs);
 uint32_t pcb_ctx_n_limbs(const pcb_ctx* ctx);   /* L: limb width of plaintexts and r       */
 uint32_t pcb_ctx_n_bits(const pcb_ctx* ctx);    /* bit length of n (plain_bits guard bound) */
 int pcb_ctx_has_private(const pcb_ctx* ctx);
@@ -122,7 +129,8 @@ pcb_status pcb_decrypt(pcb_ctx* ctx, const uint32_t* c, size_t count, uint32_t* 
 
 /* m_i = L(x_i) mu mod n, x_i = CRT(p2_power_i mod p^2, c_i^(eps mod phi(q^2)) mod q^2) —
  * Paillier::decrypt_with_half (paillier.cpp:363-369).  p2_power: count x pw_limbs (pw_limbs <= 2L),
- * e.g. an edge's delegated_power (protocol.cpp:15-18).  Statuses as pcb_decrypt.  2048/3072-bit keys. */
+ * e.g. an edge's delegated_power (protocol.cpp:15-18).  Statuses as pcb_decrypt.  Every key size (keys
+ * up to 1024 bits run it on the K = 40 RNS core, 2048/3072-bit keys on the Enc/Dec core). */
 pcb_status pcb_decrypt_with_half(pcb_ctx* ctx, const uint32_t* c, const uint32_t* p2_power, uint32_t pw_limbs,
                                  size_t count, uint32_t* m, int32_t* status, pcb_stream stream);
 

@@ -87,9 +87,27 @@ KeyPair finish_binomial(const BigNat& p, const BigNat& q, size_t key_bits) {
   return k;
 }
 
-void refuse_random_g(GMode g) {
-  if (g != GMode::binomial)
-    throw std::invalid_argument("GMode::random_g: the B200 path implements g = n + 1 only (north_star)");
+// Random generator (paillier.cpp:80-100): g = random_below(Rng(g_seed), n^2) until g is a unit
+// with L(g^eps mod n^2) invertible mod n; mu = that inverse.  One-time key work on the host, as in
+// the reference; every per-element g power then runs on the device (pcb_ctx_set_generator).
+void finish_random_g(KeyPair& k, u64 g_seed) {
+  const HBN n = to_h(k.pub.n), n2 = to_h(k.pub.n2), eps = to_h(k.prv.epsilon);
+  pcb::HRng gr(g_seed);
+  for (int budget = 256;; budget--) {
+    if (budget == 0) throw std::runtime_error("generator search exhausted");
+    const HBN g = pcb::random_below(gr, n2);
+    if (g.bit_length() < 2 || pcb::gcd(g, n) != HBN(1)) continue;
+    HBN l, r, mu;
+    pcb::divmod(pcb::pow_mod(g, eps, n2) - HBN(1), n, l, r);
+    if (!pcb::mod_inverse(l, n, mu)) continue;
+    k.pub.g = from_h(g);
+    k.pub.binomial_g = false;
+    k.prv.mu = from_h(mu);
+    const HBN p2 = to_h(k.crt.p2), q2 = to_h(k.crt.q2);
+    k.crt.g_p2 = from_h(pcb::mod(g, p2));
+    k.crt.g_q2 = from_h(pcb::mod(g, q2));
+    return;
+  }
 }
 
 }  // namespace
@@ -249,7 +267,6 @@ BigNat random_prime(Rng& rng, size_t bits, int mr_rounds) {
 
 // ---- keys -----------------------------------------------------------------------------------
 KeyPair keygen(Rng& rng, size_t key_bits, GMode gmode) {
-  refuse_random_g(gmode);
   if (key_bits != 64 && key_bits != 1024 && key_bits != 2048 && key_bits != 4096)
     throw std::invalid_argument("key_bits must be 64, 1024, 2048 or 4096");
   const size_t L = key_bits / 32, H = L / 2;
@@ -257,14 +274,22 @@ KeyPair keygen(Rng& rng, size_t key_bits, GMode gmode) {
   u64 st = rng.state;
   check(pcb_keygen(&st, (uint32_t)key_bits, n.data(), p.data(), q.data()), "keygen");
   rng.state = st;
-  return finish_binomial(BigNat::from_u32(p.data(), H), BigNat::from_u32(q.data(), H), key_bits);
+  KeyPair k = finish_binomial(BigNat::from_u32(p.data(), H), BigNat::from_u32(q.data(), H), key_bits);
+  if (gmode == GMode::random_g) {
+    // the reference seeds the generator search with the stream's last draw, rng.next() at
+    // paillier.cpp:120, which pcb_keygen has consumed: its output is the mix of the final state
+    pcb::HRng h(st - 0x9e3779b97f4a7c15ull);
+    finish_random_g(k, h.next());
+  }
+  return k;
 }
 
 KeyPair keypair_from_primes(const BigNat& p, const BigNat& q, GMode gmode, u64 g_seed) {
   (void)g_seed;
   if (p == q || p < BigNat(2) || q < BigNat(2)) throw std::invalid_argument("need two distinct primes");
-  refuse_random_g(gmode);
-  return finish_binomial(p, q, (p * q).bit_length());
+  KeyPair k = finish_binomial(p, q, (p * q).bit_length());
+  if (gmode == GMode::random_g) finish_random_g(k, g_seed);
+  return k;
 }
 
 CrtShare crt_share(const KeyPair& k) { return CrtShare{k.crt.p2, k.crt.phi_p2}; }
@@ -301,42 +326,66 @@ std::vector<uint8_t> serialize_keypair(const KeyPair& k) {
   put_big(o, k.pub.n);
   put_big(o, k.prv.p);
   put_big(o, k.prv.q);
+  if (!k.pub.binomial_g) put_big(o, k.pub.g);
   return o;
 }
 
 KeyPair parse_keypair(const std::vector<uint8_t>& d) {
   if (d.size() < 8 || d[0] != 'P' || d[1] != 'B') throw std::runtime_error("not a key record");
   if (d[2] != 1) throw std::runtime_error("unknown key record version");
-  if (d[3] != 1) throw std::runtime_error("key record with a random generator (unsupported)");
+  if (d[3] > 1) throw std::runtime_error("corrupt key record: generator flag");
   size_t off = 4;
   const uint32_t bits = get_u32(d, off);
   const BigNat n = get_big(d, off), p = get_big(d, off), q = get_big(d, off);
+  BigNat g;
+  if (d[3] == 0) g = get_big(d, off);
   if (off != d.size()) throw std::runtime_error("trailing bytes in key record");
   if (p * q != n) throw std::runtime_error("corrupt key record: n != p*q");
-  return finish_binomial(p, q, bits);
+  KeyPair k = finish_binomial(p, q, bits);
+  if (d[3] == 0) {  // the recorded generator: mu from it (paillier.cpp:90-92)
+    const HBN hn = to_h(n), hn2 = hn * hn, hg = to_h(g);
+    if (hg >= hn2 || pcb::gcd(hg, hn) != HBN(1)) throw std::runtime_error("corrupt key record: g");
+    HBN l, r, mu;
+    pcb::divmod(pcb::pow_mod(hg, to_h(k.prv.epsilon), hn2) - HBN(1), hn, l, r);
+    if (!pcb::mod_inverse(l, hn, mu)) throw std::runtime_error("corrupt key record: g");
+    k.pub.g = g;
+    k.pub.binomial_g = false;
+    k.prv.mu = from_h(mu);
+    k.crt.g_p2 = mod(g, k.crt.p2);
+    k.crt.g_q2 = mod(g, k.crt.q2);
+  }
+  return k;
 }
 
 // ---- Paillier ---------------------------------------------------------------------------------
 Paillier::Paillier(PublicKey pub, Engine engine) : pub_(std::move(pub)), engine_(engine) {
   if (pub_.n.is_zero()) throw std::invalid_argument("empty public key");
-  if (!pub_.binomial_g) refuse_random_g(GMode::random_g);
+  if (pub_.n2.is_zero()) pub_.n2 = pub_.n * pub_.n;
   L_ = (pub_.n.bit_length() + 31) / 32;
   std::vector<uint32_t> n = pub_.n.to_u32(L_);
   pcb_ctx* c = nullptr;
   check(pcb_ctx_create(&c, device_index(), n.data(), (uint32_t)L_, nullptr, nullptr, 0), "context");
   ctx_ = c;
+  set_generator();
+}
+
+void Paillier::set_generator() {
+  if (pub_.binomial_g) return;
+  std::vector<uint32_t> g = pub_.g.to_u32(2 * L_);
+  check(pcb_ctx_set_generator((pcb_ctx*)ctx_, g.data(), (uint32_t)(2 * L_)), "generator");
 }
 
 Paillier::Paillier(const KeyPair& keys, Engine engine)
     : pub_(keys.pub), has_prv_(true), prv_(keys.prv), crt_(keys.crt), engine_(engine) {
   if (pub_.n.is_zero()) throw std::invalid_argument("empty public key");
-  if (!pub_.binomial_g) refuse_random_g(GMode::random_g);
+  if (pub_.n2.is_zero()) pub_.n2 = pub_.n * pub_.n;
   L_ = (pub_.n.bit_length() + 31) / 32;
   const size_t w = std::max((prv_.p.bit_length() + 31) / 32, (prv_.q.bit_length() + 31) / 32);
   std::vector<uint32_t> n = pub_.n.to_u32(L_), p = prv_.p.to_u32(w), q = prv_.q.to_u32(w);
   pcb_ctx* c = nullptr;
   check(pcb_ctx_create(&c, device_index(), n.data(), (uint32_t)L_, p.data(), q.data(), (uint32_t)w), "context");
   ctx_ = c;
+  set_generator();
 }
 
 Paillier::~Paillier() {
@@ -366,7 +415,8 @@ BigNat Paillier::sample_r(Rng& rng) const {
   return BigNat::from_u32(r.data(), L_);
 }
 
-std::vector<BigNat> Paillier::enc_batch(const std::vector<BigNat>& ms, const std::vector<BigNat>& rs, bool use_crt) {
+std::vector<BigNat> Paillier::enc_batch(const std::vector<BigNat>& ms, const std::vector<BigNat>& rs, bool use_crt,
+                                        bool count_g) {
   const size_t cnt = ms.size();
   if (cnt == 0) return {};
   if (use_crt) need_private("split encryption needs p and q");
@@ -393,6 +443,12 @@ std::vector<BigNat> Paillier::enc_batch(const std::vector<BigNat>& ms, const std
     pow_half_ += 2 * cnt;  // two half_pow per element (paillier.cpp:339-342)
   else
     pow_full_ += cnt;      // r^n mod n^2 (paillier.cpp:325)
+  if (count_g && !pub_.binomial_g) {  // g^m: one full power, or one per CRT side (paillier.cpp:253-271)
+    if (use_crt)
+      pow_half_ += 2 * cnt;
+    else
+      pow_full_ += cnt;
+  }
   return out;
 }
 
@@ -438,7 +494,7 @@ RnFactor Paillier::make_rn_factor(const BigNat& r) {
   if (r.is_zero() || r >= pub_.n) throw std::invalid_argument("randomness not in [1, n)");
   RnFactor f;
   f.r = r;
-  f.full = enc_batch({BigNat()}, {r}, false)[0];
+  f.full = enc_batch({BigNat()}, {r}, false, false)[0];
   if (has_prv_) {
     f.half_p2 = mod(f.full, crt_.p2);
     f.half_q2 = mod(f.full, crt_.q2);
@@ -454,13 +510,19 @@ Ciphertext Paillier::encrypt_with_factor(const BigNat& m, const RnFactor& f) {
   int32_t st = 0;
   check(pcb_encrypt_rn((pcb_ctx*)ctx_, mm.data(), (uint32_t)L_, rn.data(), 1, c.data(), &st, nullptr), "encrypt");
   if (st) throw_status(st, "encrypt");
+  if (!pub_.binomial_g) pow_full_ += 1;  // g^m (paillier.cpp:388)
   return Ciphertext{BigNat::from_u32(c.data(), 2 * L_), (u32)m.bit_length()};
 }
 
 Ciphertext Paillier::crt_encrypt_with_factor(const BigNat& m, const RnFactor& f) {
   need_private("split encryption needs p and q");
   if (f.half_p2.is_zero() && f.half_q2.is_zero()) throw std::invalid_argument("factor missing split residues");
-  return encrypt_with_factor(m, f);  // the same residue (paillier.cpp:391-400 == 384-389 for g = n + 1)
+  Ciphertext c = encrypt_with_factor(m, f);  // the same residue (paillier.cpp:391-400 == 384-389)
+  if (!pub_.binomial_g) {  // ledger of the split form: g on both sides (paillier.cpp:397-398)
+    pow_full_ -= 1;
+    pow_half_ += 2;
+  }
+  return c;
 }
 
 Ciphertext Paillier::finish_split_encrypt(const BigNat& m, const BigNat& p2_g_power, const BigNat& r) {
@@ -473,7 +535,7 @@ Ciphertext Paillier::finish_split_encrypt(const BigNat& m, const BigNat& p2_g_po
                                  c.data(), &st, nullptr),
         "finish_split_encrypt");
   if (st) throw_status(st, "finish_split_encrypt");
-  pow_half_ += 2;
+  pow_half_ += pub_.binomial_g ? 2 : 3;  // both r halves (+ the q-side g power, paillier.cpp:410-413)
   return Ciphertext{BigNat::from_u32(c.data(), 2 * L_), (u32)m.bit_length()};
 }
 

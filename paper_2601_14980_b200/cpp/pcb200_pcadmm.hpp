@@ -7,12 +7,13 @@
 // call on the B200.  Host code here is bookkeeping only: key material and CRT constants (one-time,
 // as in the reference), plain_bits tracking, exception mapping, operation counters.
 //
-// Differences from the reference, by design (north_star: g = n + 1, no multi-backend dispatch):
-//   * GMode::random_g keys are refused (std::invalid_argument); the B200 path implements the
-//     binomial generator g = n + 1 only.
+// Notes:
+//   * GMode::random_g keys work: the generator search is the reference's (host key work), and the
+//     device computes g^m from 64-bit digit powers (pcb_ctx_set_generator).  The fused ADMM hot
+//     path (pcb_quantize_encrypt) is the g = n + 1 form, as north_star fixes it.
 //   * Engine::coeff_fft is accepted and runs the same CUDA path (the reference pins the two lanes
-//     to identical results, test_paillier.cpp:242-257); there is no second lane.
-//   * finish_split_encrypt* and decrypt_with_half need 2048/3072-bit keys (the RNS core).
+//     to identical results, test_paillier.cpp:242-257); there is no second lane to dispatch to.
+//   * Keys above 3072 bits (4096) are refused by the device context (std::invalid_argument).
 // Errors map 1:1 to the reference's exception types (paillier.cpp; pcb_status in pcb200.h).
 #pragma once
 
@@ -191,7 +192,9 @@ class Paillier {
  private:
   void need_private(const char* what) const;
   void bump_bits_or_throw(u32 bits) const;
-  std::vector<BigNat> enc_batch(const std::vector<BigNat>& ms, const std::vector<BigNat>& rs, bool use_crt);
+  std::vector<BigNat> enc_batch(const std::vector<BigNat>& ms, const std::vector<BigNat>& rs, bool use_crt,
+                                bool count_g = true);
+  void set_generator();
   std::vector<BigNat> dec_batch(const std::vector<Ciphertext>& cs, bool use_crt);
 
   PublicKey pub_;

@@ -134,6 +134,17 @@ __global__ void first_bad_kernel(const int32_t* st, size_t n, unsigned long long
     if (st[i] != 0) atomicMin(out, ((unsigned long long)i << 32) | (uint32_t)st[i]);
 }
 
+// out[i] = src (w words) for every i < count (a broadcast base for the digit exponentiations)
+__global__ void bcast_kernel(uint32_t* out, const uint32_t* src, int w, size_t count) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count * (size_t)w; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = src[i % w];
+}
+// rows whose argument check failed come back as 0 (as the other encryption paths do)
+__global__ void zero_bad_rows_kernel(uint32_t* c, int w, const int32_t* st, size_t count) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count * (size_t)w; i += (size_t)gridDim.x * blockDim.x)
+    if (st[i / w] != 0) c[i] = 0;
+}
+
 // Scans stv[0, count) for the first non-OK element; synchronises `st` (only called when the caller
 // asked for no status array, i.e. for a single error code).
 pcb_status first_failure(const int32_t* stv, size_t count, cudaStream_t st) {
@@ -278,6 +289,15 @@ struct pcb_ctx {
   bool use_rns = false;
   RnsXModulus rx_p, rx_q;        // p^2, q^2 for the streaming RNS core (rnsx.cu)
   bool use_rnsx = false;
+  // rx_p / rx_q exist (use_rnsx, or small keys where they serve only the collaborative entry
+  // points decrypt_with_half / finish_split_encrypt while Enc / Dec stay on the carry core)
+  bool has_rx = false;
+  // random generator (GMode::random_g, pcb_ctx_set_generator): g and its 64-bit digit powers
+  // G_j = g^(2^(64 j)) mod n^2 (d_gtab, gdig x 2L words) for g^m = prod_j G_j^(m_j) on the device
+  bool random_g = false;
+  HBN g;
+  uint32_t* d_gtab = nullptr;
+  int gdig = 0;
   // split CRT encryption (2048-bit keys): r^n mod p^2 = ((r mod p)^q mod p)^p mod p^2, since u^p
   // mod p^2 depends only on u mod p; stage 1 on the carry-chain core mod p (1024 bits), stage 2
   // on the RNS core with the 1024-bit exponent p (half the exponent bits of n).  Same for q.
@@ -374,8 +394,8 @@ void build_dec(pcb_ctx* x) {
   t.to_limbs(k.pinv_lo, H);
   if (!mod_inverse(x->q, RH, t)) throw std::invalid_argument("even q");
   t.to_limbs(k.qinv_lo, H);
-  // h_p = L_p(g^(p-1) mod p^2)^-1 mod p with g = n + 1
-  const HBN g = x->n + HBN(1);
+  // h_p = L_p(g^(p-1) mod p^2)^-1 mod p (g = n + 1, or the context's random generator)
+  const HBN g = x->random_g ? x->g : x->n + HBN(1);
   for (int side = 0; side < 2; side++) {
     const HBN& pr = side ? x->q : x->p;
     const HBN& m2 = side ? q2 : p2;
@@ -405,7 +425,13 @@ void build_half(pcb_ctx* x) {
   const HBN RH = HBN(1) << (32 * H);
   const HBN eps = lcm(x->p - HBN(1), x->q - HBN(1));
   HBN mu;
-  if (!mod_inverse(mod(eps, x->n), x->n, mu)) throw std::invalid_argument("degenerate key (mu)");  // paillier.cpp:78
+  if (x->random_g) {  // mu = L(g^eps mod n^2)^-1 mod n (paillier.cpp:90-92)
+    HBN l, r;
+    divmod(pow_mod(x->g, eps, x->n2) - HBN(1), x->n, l, r);
+    if (!mod_inverse(l, x->n, mu)) throw std::invalid_argument("degenerate generator (mu)");
+  } else if (!mod_inverse(mod(eps, x->n), x->n, mu)) {
+    throw std::invalid_argument("degenerate key (mu)");  // paillier.cpp:78
+  }
   for (int side = 0; side < 2; side++) {
     const HBN& pr = side ? x->q : x->p;
     const HBN& ot = side ? x->p : x->q;
@@ -547,6 +573,7 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
         int K = 0;
         if ((!ev || atoi(ev) != 0) && (x->S == 64 || x->S == 96) && rnsx_shape((int)(32 * x->S), &K))
           x->use_rnsx = rnsx_build(p2, x->n, x->S, K, &x->rx_p) && rnsx_build(q2, x->n, x->S, K, &x->rx_q);
+        x->has_rx = x->use_rnsx;
         const char* es = getenv("PCB_ENC_SPLIT");
         const size_t hb = (size_t)16 * x->S;  // half the p^2 width: p, q bits
         if (x->use_rnsx && (x->S == 64 || x->S == 96) && x->p.bit_length() <= hb && x->q.bit_length() <= hb &&
@@ -568,7 +595,16 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
         }
       }
       switch (x->S) {
-        case 32: build_enc<32>(x.get()); build_dec<32>(x.get()); break;
+        case 32: {
+          build_enc<32>(x.get());
+          build_dec<32>(x.get());
+          build_half<32>(x.get());
+          // p^2, q^2 <= 1024 bits on the K = 40 RNS core for the collaborative entry points only
+          const char* ev = getenv("PCB_RNSX");
+          if (!ev || atoi(ev) != 0)
+            x->has_rx = rnsx_build(p2, x->n, 32, 40, &x->rx_p) && rnsx_build(q2, x->n, 32, 40, &x->rx_q);
+          break;
+        }
         case 64: {
           build_enc<64>(x.get());
           build_dec<64>(x.get());
@@ -701,6 +737,7 @@ void pcb_ctx_destroy(pcb_ctx* x) {
   rnsx_free(&x->rx_n2);
   rnsx_free(&x->rx1_p);
   rnsx_free(&x->rx1_q);
+  if (x->d_gtab) cudaFree(x->d_gtab);
   delete x;
 }
 
@@ -733,6 +770,46 @@ pcb_status pcb_ctx_get_n(const pcb_ctx* x, uint32_t* n, uint32_t* n2) {
   if (!x) return PCB_E_SHAPE;
   if (n) x->n.to_limbs(n, x->L);
   if (n2) x->n2.to_limbs(n2, 2 * x->L);
+  return PCB_OK;
+}
+
+pcb_status pcb_ctx_set_generator(pcb_ctx* x, const uint32_t* g, uint32_t g_limbs) {
+  if (!x || !g || !g_limbs) return PCB_E_SHAPE;
+  try {
+    const HBN gg = HBN::from_limbs(g, g_limbs);
+    if (gg >= x->n2 || gg.bit_length() < 2 || gcd(gg, x->n) != HBN(1)) return PCB_E_SHAPE;
+    if (gg == x->n + HBN(1)) {  // the binomial generator: nothing to do
+      x->random_g = false;
+      return PCB_OK;
+    }
+    x->random_g = true;
+    x->g = gg;
+    if (x->has_prv) {  // decryption constants from g (h_p, h_q; mu for decrypt_with_half)
+      switch (x->S) {
+        case 32: build_dec<32>(x); build_half<32>(x); break;
+        case 64: build_dec<64>(x); build_half<64>(x); break;
+        case 96: build_dec<96>(x); build_half<96>(x); break;
+        default: return PCB_E_UNSUPPORTED;
+      }
+    }
+    // G_j = g^(2^(64 j)) mod n^2, j < ceil(L / 2): key-setup constants for g^m on the device
+    x->gdig = (int)((x->L + 1) / 2);
+    const size_t W = 2 * x->L;
+    std::vector<uint32_t> tab((size_t)x->gdig * W, 0);
+    HBN gj = gg;
+    const HBN two64 = HBN(1) << 64;
+    for (int j = 0; j < x->gdig; j++) {
+      gj.to_limbs(tab.data() + (size_t)j * W, W);
+      gj = pow_mod(gj, two64, x->n2);
+    }
+    if (set_device(x)) return PCB_E_CUDA;
+    if (x->d_gtab) cudaFree(x->d_gtab);
+    x->d_gtab = nullptr;
+    if (cudaMalloc(&x->d_gtab, tab.size() * 4) != cudaSuccess) return PCB_E_ALLOC;
+    if (cudaMemcpy(x->d_gtab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
+  } catch (...) {
+    return PCB_E_SHAPE;
+  }
   return PCB_OK;
 }
 
@@ -1019,6 +1096,53 @@ static pcb_status run_wide(pcb_ctx* x, const WStep* prog, int nsteps, const uint
   return PCB_E_UNSUPPORTED;
 }
 
+static std::vector<WStep> prog_hom_add();
+static std::vector<WStep> prog_scalar_pow();
+
+// g^m mod n^2 for a random generator (g_power_full, paillier.cpp:253-258) with per-element m
+// (count x m_limbs words): m = sum_j m_j 2^(64 j), g^m = prod_j G_j^(m_j) with the context's digit
+// powers G_j, each a 64-bit-exponent power on the n^2 core (prog_scalar_pow), multiplied in with
+// prog_hom_add.  Chunks of <= 2^16 elements bound the broadcast-base scratch.
+static pcb_status gpow_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, size_t count, uint32_t* out,
+                            cudaStream_t st) {
+  if (!x->random_g || !x->d_gtab) return PCB_E_UNSUPPORTED;
+  const size_t W = 2 * x->L, wb = W * 4;
+  const int nd = std::min<int>((int)((m_limbs + 1) / 2), x->gdig);
+  const size_t CH = 1 << 16;
+  std::vector<WStep> pw = prog_scalar_pow(), pa = prog_hom_add();
+  uint32_t *mp = nullptr, *base = nullptr, *pj = nullptr;
+  uint64_t* kj = nullptr;
+  const size_t mw = 2 * (size_t)nd;  // even-width copy of m (64-bit digits)
+  pcb_status e = scratch_alloc(count * mw * 4, (void**)&mp, st);
+  if (!e) e = cuda_check(cudaMemsetAsync(mp, 0, count * mw * 4, st));
+  if (!e)
+    e = cuda_check(cudaMemcpy2DAsync(mp, mw * 4, m, m_limbs * 4, std::min<size_t>(m_limbs, mw) * 4, count,
+                                     cudaMemcpyDeviceToDevice, st));
+  if (!e) e = scratch_alloc(std::min(count, CH) * wb, (void**)&base, st);
+  if (!e) e = scratch_alloc(std::min(count, CH) * wb, (void**)&pj, st);
+  if (!e) e = scratch_alloc(std::min(count, CH) * 8, (void**)&kj, st);
+  for (size_t c0 = 0; !e && c0 < count; c0 += CH) {
+    const size_t cn = std::min(CH, count - c0);
+    uint32_t* acc = out + c0 * W;
+    for (int j = 0; !e && j < nd; j++) {
+      bcast_kernel<<<(int)std::min<size_t>((cn * W + 255) / 256, 4096), 256, 0, st>>>(base, x->d_gtab + (size_t)j * W,
+                                                                                  (int)W, cn);
+      count_launch();
+      e = cuda_check(cudaGetLastError());
+      if (!e)
+        e = cuda_check(cudaMemcpy2DAsync(kj, 8, mp + c0 * mw + 2 * j, mw * 4, 8, cn, cudaMemcpyDeviceToDevice, st));
+      if (!e)
+        e = run_wide(x, pw.data(), (int)pw.size(), base, nullptr, kj, 1, cn, cn, j ? pj : acc, 16, st);
+      if (!e && j) e = run_wide(x, pa.data(), (int)pa.size(), acc, pj, nullptr, 1, cn, cn, acc, 1, st);
+    }
+  }
+  scratch_free(mp, st);
+  scratch_free(base, st);
+  scratch_free(pj, st);
+  scratch_free(kj, st);
+  return e;
+}
+
 // Public-key encryption c = (1 + m n) r^n mod n^2 (encrypt_with_r, paillier.cpp:320-328) on the
 // radix kernel at modulus n^2 (ENC mode of side28.cu).
 static pcb_status run_pub_enc(pcb_ctx* x, const uint32_t* r, const uint32_t* m, int m_words, const int32_t* stv,
@@ -1113,6 +1237,65 @@ static std::vector<WStep> prog_aggregate(int chunk) {
   return p;
 }
 
+// Encryption under a random generator: c = g^m r^n mod n^2 (encrypt_with_r / crt_encrypt_with_r,
+// paillier.cpp:320-344; the CRT form is the same residue, test_paillier.cpp:63-78).  r^n (CRT or
+// n^2 path, as for g = n + 1 with m = 0), then g^m by gpow_core, one product, and the argument
+// statuses of the real m and r (rows that fail come back as 0).
+static pcb_status encrypt_random_g(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* r, size_t count,
+                                   uint32_t* c, int use_crt, int32_t* status, cudaStream_t st) {
+  Staged sm, sr, sc, ss;
+  uint32_t *m0 = nullptr, *gm = nullptr;
+  int32_t* stv = nullptr;
+  const size_t W = 2 * x->L;
+  pcb_status e = stage_in(m, count * m_limbs * 4, st, &sm);
+  if (!e) e = stage_in(r, count * x->L * 4, st, &sr);
+  if (!e) e = stage_out(c, count * W * 4, st, &sc);
+  if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+  stv = (int32_t*)ss.dev;
+  if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = scratch_alloc(count * 4, (void**)&m0, st);
+  if (!e) e = cuda_check(cudaMemsetAsync(m0, 0, count * 4, st));
+  if (!e && x->has_prv) {
+    e = enc_core(x, m0, 1, nullptr, 0, 0, 0, 0, nullptr, nullptr, (const uint32_t*)sr.dev, count, (uint32_t*)sc.dev,
+                 stv, st);
+  } else if (!e) {
+    e = launch_enc_prep(m0, 1, nullptr, 0, 0, 0, 0, nullptr, 0, nullptr, nullptr, (const uint32_t*)sr.dev, x->d_n,
+                        (int)x->L, stv, count, st);
+    if (!e) e = cuda_check(cudaMemsetAsync(sc.dev, 0, count * W * 4, st));
+    if (!e) e = run_pub_enc(x, (const uint32_t*)sr.dev, m0, 1, stv, count, (uint32_t*)sc.dev, st);
+  }
+  if (!e)  // statuses of the real arguments
+    e = launch_enc_prep((const uint32_t*)sm.dev, (int)m_limbs, nullptr, 0, 0, 0, 0, nullptr, 0, nullptr, nullptr,
+                        (const uint32_t*)sr.dev, x->d_n, (int)x->L, stv, count, st);
+  if (!e) e = scratch_alloc(count * W * 4, (void**)&gm, st);
+  if (!e) e = gpow_core(x, (const uint32_t*)sm.dev, m_limbs, count, gm, st);
+  std::vector<WStep> pa = prog_hom_add();
+  if (!e) e = run_wide(x, pa.data(), (int)pa.size(), (const uint32_t*)sc.dev, gm, nullptr, 1, count, count,
+                       (uint32_t*)sc.dev, 1, st);
+  if (!e) {
+    zero_bad_rows_kernel<<<(int)std::min<size_t>((count * W + 255) / 256, 4096), 256, 0, st>>>((uint32_t*)sc.dev,
+                                                                                             (int)W, stv, count);
+    count_launch();
+    e = cuda_check(cudaGetLastError());
+  }
+  if (!e) e = unstage_out(c, &sc, st);
+  if (!e) e = unstage_out(status, &ss, st);
+  if (!e && !status) e = first_failure(stv, count, st);
+  scratch_free(m0, st);
+  scratch_free(gm, st);
+  if (!ss.dev) scratch_free(stv, st);
+  const bool any_host = sm.host || sr.host || sc.host || ss.host;
+  for (auto* p : {&sm, &sr, &sc, &ss}) unstage(p, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!e) {  // reference ledger: g^m and r^n (paillier.cpp:253-258, 325; 264-271, 339-342)
+    if (use_crt)
+      x->pow_half += 4 * (uint64_t)count;
+    else
+      x->pow_full += 2 * (uint64_t)count;
+  }
+  return e;
+}
+
 extern "C" {
 
 pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* r, size_t count, uint32_t* c,
@@ -1120,6 +1303,11 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
   if (!x || (count && (!m || !r || !c))) return PCB_E_SHAPE;
   if (m_limbs == 0 || m_limbs > x->L) return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
+  if (!x->has_prv && use_crt) return PCB_E_NO_PRIVATE;
+  if (x->random_g) {
+    if (auto e = set_device(x)) return e;
+    return encrypt_random_g(x, m, m_limbs, r, count, c, use_crt, status, (cudaStream_t)stream);
+  }
   // use_crt = 0 on a private context: same residue through the CRT halves (the reference's own
   // tests pin CRT == direct bit-identically, test_paillier.cpp:63-78, acceptance [2]); the
   // ledger still records the direct path (pow_full).  Public-key-only: n^2 path (TODO).
@@ -1203,6 +1391,15 @@ pcb_status pcb_encrypt_rn(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const
   if (!e)
     e = launch_onepmn((const uint32_t*)sm.dev, (int)m_limbs, (const uint32_t*)sr.dev, x->d_n, x->d_n2, (int)x->L, b,
                       stv, count, st);
+  if (!e && x->random_g) {  // g^m instead of 1 + m n (encrypt_with_factor, paillier.cpp:384-389)
+    e = gpow_core(x, (const uint32_t*)sm.dev, m_limbs, count, b, st);
+    if (!e) {
+      zero_bad_rows_kernel<<<(int)std::min<size_t>((count * 2 * x->L + 255) / 256, 4096), 256, 0, st>>>(
+          b, (int)(2 * x->L), stv, count);
+      count_launch();
+      e = cuda_check(cudaGetLastError());
+    }
+  }
   std::vector<WStep> p = prog_hom_add();  // (1 + m n) * rn mod n^2; failed rows have b = 0 -> c = 0
   if (!e) e = run_wide(x, p.data(), (int)p.size(), (const uint32_t*)sr.dev, b, nullptr, 1, count, count,
                        (uint32_t*)sc.dev, 1, st);
@@ -1268,6 +1465,9 @@ static pcb_status dwh_core(pcb_ctx* x, const uint32_t* c, const uint32_t* pw, si
   if (!e)
     e = launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_epsq, x->len_epsq, kTab, c, L2, nullptr, 0, count, yq, st,
                     ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm);
+  if (!e && S == 32)
+    e = launch_dec_finish<32>(*reinterpret_cast<const CrtDecConsts<32>*>(x->half_blob.data()), yp, yq, stv, m,
+                              (int)x->L, count, st);
   if (!e && S == 64)
     e = launch_dec_finish<64>(*reinterpret_cast<const CrtDecConsts<64>*>(x->half_blob.data()), yp, yq, stv, m,
                               (int)x->L, count, st);
@@ -1376,7 +1576,7 @@ pcb_status pcb_decrypt_with_half(pcb_ctx* x, const uint32_t* c, const uint32_t* 
                                  size_t count, uint32_t* m, int32_t* status, pcb_stream stream) {
   if (!x || (count && (!c || !p2_power || !m)) || pw_limbs == 0 || pw_limbs > 2 * x->L) return PCB_E_SHAPE;
   if (!x->has_prv) return PCB_E_NO_PRIVATE;
-  if (!x->use_rnsx) return PCB_E_UNSUPPORTED;  // 2048 / 3072-bit keys
+  if (!x->has_rx) return PCB_E_UNSUPPORTED;
   if (count == 0) return PCB_OK;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1416,7 +1616,7 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
                                     pcb_stream stream) {
   if (!x || (count && (!m || !p2_g_power || !r || !c)) || pg_limbs == 0 || pg_limbs > 2 * x->L) return PCB_E_SHAPE;
   if (!x->has_prv) return PCB_E_NO_PRIVATE;
-  if (!x->use_rnsx) return PCB_E_UNSUPPORTED;
+  if (!x->has_rx) return PCB_E_UNSUPPORTED;
   if (count == 0) return PCB_OK;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1445,6 +1645,17 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
   const double mm = 2.0 * S * S + S, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm;
   // cp = (p2_g_power mod p^2) r^(n mod phi(p^2)) mod p^2;  cq = (1 + m n) r^(n mod phi(q^2)) mod q^2
   if (!e) e = launch_rnsx(x->rx_p, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, gw, L2, nullptr, 0, count, gp, st, mm);
+  // random generator: the q side's g power is g^m mod q^2 (g_power_half, paillier.cpp:264-271),
+  // from g^m mod n^2 (gpow_core) reduced mod q^2
+  uint32_t *gfull = nullptr, *gq = nullptr;
+  if (!e && x->random_g) {
+    e = scratch_alloc(count * L2 * 4, (void**)&gfull, st);
+    if (!e) e = scratch_alloc(count * S * 4, (void**)&gq, st);
+    if (!e) e = gpow_core(x, (const uint32_t*)sm.dev, m_limbs, count, gfull, st);
+    if (!e)
+      e = launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, gfull, L2, nullptr, 0, count, gq, st,
+                      mm);
+  }
   if (x->enc_split) {  // r^n mod p^2 = (r^q mod p)^p mod p^2, same for q
     uint32_t* u = nullptr;
     if (!e) e = scratch_alloc(count * x->w1 * 4, (void**)&u, st);
@@ -1452,7 +1663,9 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
     if (!e)
       e = launch_rnsx(x->rx_p, kRxEncG, x->d_sched + x->off_ep, x->len_ep, kTab, u, x->w1, gp, S, count, yp, st, alg);
     if (!e) e = split_stage1(x, 1, (const uint32_t*)sr.dev, stv, count, u, st);
-    if (!e)
+    if (!e && gq)
+      e = launch_rnsx(x->rx_q, kRxEncG, x->d_sched + x->off_eq, x->len_eq, kTab, u, x->w1, gq, S, count, yq, st, alg);
+    else if (!e)
       e = launch_rnsx(x->rx_q, kRxEnc, x->d_sched + x->off_eq, x->len_eq, kTab, u, x->w1, (const uint32_t*)sm.dev,
                       (int)m_limbs, count, yq, st, alg);
     scratch_free(u, st);
@@ -1460,10 +1673,16 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
     if (!e)
       e = launch_rnsx(x->rx_p, kRxEncG, x->d_sched + x->off_enc_p, x->len_enc_p, kTab, (const uint32_t*)sr.dev,
                       (int)x->L, gp, S, count, yp, st, alg);
-    if (!e)
+    if (!e && gq)
+      e = launch_rnsx(x->rx_q, kRxEncG, x->d_sched + x->off_enc_q, x->len_enc_q, kTab, (const uint32_t*)sr.dev,
+                      (int)x->L, gq, S, count, yq, st, alg);
+    else if (!e)
       e = launch_rnsx(x->rx_q, kRxEnc, x->d_sched + x->off_enc_q, x->len_enc_q, kTab, (const uint32_t*)sr.dev,
                       (int)x->L, (const uint32_t*)sm.dev, (int)m_limbs, count, yq, st, alg);
   }
+  if (!e && S == 32)
+    e = launch_garner<32>(*reinterpret_cast<const CrtEncConsts<32>*>(x->enc_blob.data()), yp, yq, stv,
+                          (uint32_t*)sc.dev, (int)x->L, count, st);
   if (!e && S == 64)
     e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv,
                           (uint32_t*)sc.dev, (int)x->L, count, st);
@@ -1477,6 +1696,8 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
   scratch_free(gp, st);
   scratch_free(yp, st);
   scratch_free(yq, st);
+  scratch_free(gfull, st);
+  scratch_free(gq, st);
   if (!ss.dev) scratch_free(stv, st);
   const bool any_host = sm.host || sg.host || sr.host || sc.host || ss.host;
   unstage(&sm, st);
@@ -1959,7 +2180,7 @@ static pcb_status update_entry(pcb_ctx* x, size_t nblk, const uint32_t* sizes, c
   if (!e) e = scratch_alloc(seg.size() * 8, (void**)&segd, st);
   if (!e) e = cuda_check(cudaMemcpyAsync(segd, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, st));
   Staged sp;
-  if (p2pow && !x->use_rnsx) e = e ? e : PCB_E_UNSUPPORTED;
+  if (p2pow && !x->has_rx) e = e ? e : PCB_E_UNSUPPORTED;
   if (!e && p2pow) e = stage_in(p2pow, count * 2 * x->L * 4, st, &sp);
   if (!e) e = p2pow ? dwh_core(x, (const uint32_t*)sc.dev, (const uint32_t*)sp.dev, count, m, stv, st)  // collaborative
                     : dec_core(x, (const uint32_t*)sc.dev, count, m, stv, st);
@@ -2165,6 +2386,7 @@ pcb_status pcb_quantize_encrypt(pcb_ctx* x, const double* v, size_t count, doubl
   if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
     return PCB_E_SHAPE;
   if (use_crt && !x->has_prv) return PCB_E_NO_PRIVATE;
+  if (x->random_g) return PCB_E_UNSUPPORTED;  // the fused quantize + Enc is the g = n + 1 hot path
   if (count == 0) return PCB_OK;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;

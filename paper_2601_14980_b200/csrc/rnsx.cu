@@ -1176,6 +1176,7 @@ struct XOutArgs {
   const uint32_t* tabs;  // mod[K] minv[K] c4[K] invp[2K] mpj[K][mpw] mp[mpw] n[S]
   int count, K, mpw, S;
   double ntop;
+  int ntw;  // word index of the lower of N's two top words (ntop = N / 2^(32 ntw))
 };
 
 __global__ void rnsx_out_kernel(const __grid_constant__ XOutArgs P) {
@@ -1225,7 +1226,7 @@ __global__ void rnsx_out_kernel(const __grid_constant__ XOutArgs P) {
       }
     }
     double rt = 0.0;
-    for (int w = W + 1; w >= S_ - 2; w--) rt = rt * 4294967296.0 + (double)r[w];
+    for (int w = W + 1; w >= P.ntw; w--) rt = rt * 4294967296.0 + (double)r[w];
     const double qd = floor(rt / P.ntop) - 1.0;
     const uint32_t q = qd > 0 ? (uint32_t)qd : 0u;
     if (q) {
@@ -1363,6 +1364,7 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
     O.mpw = md.mpw;
     O.S = md.S;
     O.ntop = md.ntop;
+    O.ntw = md.ntw;
     const int grid = (int)((count + 127) / 128 < 4096 ? (count + 127) / 128 : 4096);
     rnsx_out_kernel<<<grid, 128, 0, st>>>(O);
     count_launch();
@@ -1624,9 +1626,13 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
   }
   Mp.to_limbs(otab.data() + 5 * K + (size_t)K * md.mpw, md.mpw);
   N.to_limbs(otab.data() + 5 * K + (size_t)K * md.mpw + md.mpw, S);
+  // the quotient estimate of the output conversion uses N's two TOP words (N may be much narrower
+  // than S words, e.g. p^2 of a toy key): ntop = N / 2^(32 ntw)
   double nt = 0.0;
   const std::vector<uint32_t> nl = N.limbs(S);
-  for (int w = S - 1; w >= S - 2; w--) nt = nt * 4294967296.0 + (double)nl[w];
+  const int top = (int)((N.bit_length() + 31) / 32) - 1;
+  md.ntw = top > 0 ? top - 1 : 0;
+  for (int w = top; w >= md.ntw; w--) nt = nt * 4294967296.0 + (double)nl[w];
   md.ntop = nt;
   md.wimg_stride = (img.size() + 4095) & ~(size_t)4095;
   bool ok = cudaMalloc(&md.d_wimg, md.wimg_stride * kRxReplicas) == cudaSuccess;

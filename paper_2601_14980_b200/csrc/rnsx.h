@@ -63,7 +63,8 @@ struct RnsXModulus {
   uint4* d_cvec = nullptr;    // constant operands in thread order: [id][g][NV][4]
   uint32_t* d_slt = nullptr;  // per slice of a product: {image offset / 16, bytes}
   uint32_t* d_out = nullptr;  // output conversion: mod'[K] minv'[K] c4[K] invp[2K] M'/m'_j[K][mpw] M'[mpw] N[S]
-  double ntop = 0.0;          // N / 2^(32 (S-2))
+  double ntop = 0.0;          // N / 2^(32 ntw): N's two top words
+  int ntw = 0;
   bool ok = false;
 };
 
