@@ -234,6 +234,18 @@ pcb_status pcb_decrypt_update_blocks_half(pcb_ctx* ctx, size_t nblocks, const ui
                                           double kappa, double* x, double* z, double* v, int32_t* status,
                                           pcb_stream stream);
 
+/* combined_quantized_update (quantize.cpp:66-82) on the device: out_i = q_alpha_i +
+ * sum_j q_b[i][j] (q_z_j + q_nv_j) in u128 (wrapping as the reference).  q_alpha / out: rows (lo, hi)
+ * u64 pairs, q_b: rows x cols row-major.  The plaintext oracle of the encrypted edge step. */
+pcb_status pcb_combined_update(const uint64_t* q_alpha, const uint64_t* q_b, const uint64_t* q_z,
+                               const uint64_t* q_nv, size_t rows, size_t cols, uint64_t* out, pcb_stream stream);
+
+/* inverse_quantize_x (quantize.cpp:84-112) on the device, FP64 in the reference's operation order
+ * (no contraction; the sequential sum over columns in one thread).  q: rows (lo, hi) u64 pairs. */
+pcb_status pcb_inverse_quantize_x(const uint64_t* q, const uint64_t* rowsum, const uint64_t* q_z,
+                                  const uint64_t* q_nv, size_t rows, size_t cols, double z_min, double z_max,
+                                  double delta, double* x, pcb_stream stream);
+
 /* ---- asynchronous forms for a resident iteration loop --------------------------------------
  * Same results as the calls above, for DEVICE pointers only and without any host synchronisation
  * (the round-1 forms synchronised the stream up to three times per call).  Instead of returning

@@ -338,6 +338,11 @@ pcb_status launch_onepmn(const uint32_t* m, int ml, const uint32_t* rn, const ui
 pcb_status launch_quantize(const double* v, size_t count, double zmin, double zmax, double delta, int fine,
                            uint64_t* q, unsigned long long* clamps, int32_t* err, cudaStream_t stream);
 pcb_status launch_status_flag(const int32_t* st, size_t count, int32_t* err, cudaStream_t stream);
+pcb_status launch_combined_update(const uint64_t* qa, const uint64_t* qb, const uint64_t* qz, const uint64_t* qnv,
+                                  size_t rows, size_t cols, uint64_t* out, cudaStream_t stream);
+pcb_status launch_inverse_x(const uint64_t* q, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
+                            size_t rows, size_t cols, double zmin, double zmax, double delta, double* x,
+                            cudaStream_t stream);
 pcb_status launch_dec_prep(const uint32_t* c, const uint32_t* n2_dev, int L, int32_t* st, size_t count,
                            cudaStream_t stream);
 pcb_status launch_update(const uint32_t* m, int L, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
@@ -2225,6 +2230,51 @@ pcb_status pcb_decrypt_update_blocks(pcb_ctx* x, size_t nblocks, const uint32_t*
                                      double z_max, double delta, double kappa, double* xo, double* zo, double* vo,
                                      int32_t* status, pcb_stream stream) {
   return update_entry(x, nblocks, sizes, c, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, status, stream);
+}
+
+pcb_status pcb_combined_update(const uint64_t* q_alpha, const uint64_t* q_b, const uint64_t* q_z,
+                               const uint64_t* q_nv, size_t rows, size_t cols, uint64_t* out, pcb_stream stream) {
+  if (rows && (!q_alpha || !out || (cols && (!q_b || !q_z || !q_nv)))) return PCB_E_SHAPE;
+  if (rows == 0) return PCB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Staged sa, sb, sz, sn, so;
+  pcb_status e = stage_in(q_alpha, rows * 16, st, &sa);
+  if (!e) e = stage_in(q_b, rows * cols * 8, st, &sb);
+  if (!e) e = stage_in(q_z, cols * 8, st, &sz);
+  if (!e) e = stage_in(q_nv, cols * 8, st, &sn);
+  if (!e) e = stage_out(out, rows * 16, st, &so);
+  if (!e)
+    e = launch_combined_update((const uint64_t*)sa.dev, (const uint64_t*)sb.dev, (const uint64_t*)sz.dev,
+                               (const uint64_t*)sn.dev, rows, cols, (uint64_t*)so.dev, st);
+  if (!e) e = unstage_out(out, &so, st);
+  const bool any_host = sa.host || sb.host || sz.host || sn.host || so.host;
+  for (auto* p : {&sa, &sb, &sz, &sn, &so}) unstage(p, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  return e;
+}
+
+pcb_status pcb_inverse_quantize_x(const uint64_t* q, const uint64_t* rowsum, const uint64_t* q_z,
+                                  const uint64_t* q_nv, size_t rows, size_t cols, double z_min, double z_max,
+                                  double delta, double* x, pcb_stream stream) {
+  if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
+    return PCB_E_SHAPE;  // check_spec (quantize.cpp:8-15)
+  if (rows && (!q || !rowsum || !x || (cols && (!q_z || !q_nv)))) return PCB_E_SHAPE;
+  if (rows == 0) return PCB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Staged sq, sr, sz, sn, sx;
+  std::vector<uint64_t> zero(2, 0);
+  pcb_status e = stage_in(q, rows * 16, st, &sq);
+  if (!e) e = stage_in(rowsum, rows * 8, st, &sr);
+  if (!e) e = stage_in(cols ? (const void*)q_z : (const void*)zero.data(), std::max<size_t>(cols, 1) * 8, st, &sz);
+  if (!e) e = stage_in(cols ? (const void*)q_nv : (const void*)zero.data(), std::max<size_t>(cols, 1) * 8, st, &sn);
+  if (!e) e = stage_out(x, rows * 8, st, &sx);
+  if (!e)
+    e = launch_inverse_x((const uint64_t*)sq.dev, (const uint64_t*)sr.dev, (const uint64_t*)sz.dev,
+                         (const uint64_t*)sn.dev, rows, cols, z_min, z_max, delta, (double*)sx.dev, st);
+  if (!e) e = unstage_out(x, &sx, st);
+  for (auto* p : {&sq, &sr, &sz, &sn, &sx}) unstage(p, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  return e;
 }
 
 // ---- asynchronous iteration forms (include/pcb200.h): device pointers, no host sync ----------

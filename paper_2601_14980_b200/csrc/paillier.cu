@@ -326,6 +326,15 @@ __global__ void sumzv_kernel(const uint64_t* q_z, const uint64_t* q_nv, const lo
   out[b] = s;
 }
 
+// inverse_quantize_x for one row (quantize.cpp:105-110): the reference's operation order, no FMA
+__device__ __forceinline__ double inverse_x_row(uint64_t lo, uint64_t hi, uint64_t rowsum, double cols, double szv,
+                                                double zmin, double step, double step2) {
+  const double rowsum_b = __dadd_rn(__dmul_rn(cols, zmin), __dmul_rn(step, __ull2double_rn(rowsum)));
+  return __dsub_rn(__dadd_rn(__dmul_rn(u128_to_double_rn(lo, hi), step2),
+                             __dmul_rn(zmin, __dadd_rn(__dadd_rn(1.0, __dmul_rn(2.0, rowsum_b)), szv))),
+                   __dmul_rn(__dmul_rn(__dmul_rn(2.0, zmin), zmin), cols));
+}
+
 __global__ void update_kernel(const __grid_constant__ UpdateArgs P) {
   const double range = __dsub_rn(P.zmax, P.zmin);
   const double step = __ddiv_rn(range, P.delta);
@@ -352,12 +361,7 @@ __global__ void update_kernel(const __grid_constant__ UpdateArgs P) {
       P.st[i] = PCB_E_RANGE_UPDATE;
       continue;
     }
-    // inverse_quantize_x (quantize.cpp:105-110)
-    const double rowsum_b = __dadd_rn(__dmul_rn(cols, P.zmin), __dmul_rn(step, __ull2double_rn(P.rowsum[i])));
-    const double xi = __dsub_rn(
-        __dadd_rn(__dmul_rn(u128_to_double_rn(lo, hi), step2),
-                  __dmul_rn(P.zmin, __dadd_rn(__dadd_rn(1.0, __dmul_rn(2.0, rowsum_b)), szv))),
-        __dmul_rn(__dmul_rn(__dmul_rn(2.0, P.zmin), P.zmin), cols));
+    const double xi = inverse_x_row(lo, hi, P.rowsum[i], cols, szv, P.zmin, step, step2);
     // protocol.cpp:504-511 + soft_threshold (admm.cpp:18-22)
     const double xv = __dadd_rn(xi, P.v[i]);
     double zz;
@@ -572,6 +576,59 @@ pcb_status launch_dec_finish(const CrtDecConsts<S>& k, const uint32_t* xp, const
   dec_finish_kernel<S><<<blocks, kThreadsPerBlock, smem, stream>>>(P);
   count_launch();
   return cuda_check(cudaGetLastError());
+}
+
+// combined_quantized_update (quantize.cpp:66-82) on the device: q_i = qa_i + sum_j qb_ij (qz_j + qnv_j)
+// in u128 (wrapping like the reference's u128 arithmetic), one row per thread
+__global__ void combined_update_kernel(const uint64_t* qa, const uint64_t* qb, const uint64_t* qz, const uint64_t* qnv,
+                                       size_t rows, size_t cols, uint64_t* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < rows; i += (size_t)gridDim.x * blockDim.x) {
+    unsigned __int128 acc = ((unsigned __int128)qa[2 * i + 1] << 64) | qa[2 * i];
+    const uint64_t* row = qb + i * cols;
+    for (size_t j = 0; j < cols; j++)
+      acc += (unsigned __int128)row[j] * ((unsigned __int128)qz[j] + (unsigned __int128)qnv[j]);
+    out[2 * i] = (uint64_t)acc;
+    out[2 * i + 1] = (uint64_t)(acc >> 64);
+  }
+}
+
+pcb_status launch_combined_update(const uint64_t* qa, const uint64_t* qb, const uint64_t* qz, const uint64_t* qnv,
+                                  size_t rows, size_t cols, uint64_t* out, cudaStream_t stream) {
+  combined_update_kernel<<<small_grid(rows), 256, 0, stream>>>(qa, qb, qz, qnv, rows, cols, out);
+  count_launch();
+  return cuda_check(cudaGetLastError());
+}
+
+// inverse_quantize_x (quantize.cpp:84-112) alone: sum_zv in the reference's sequential order
+// (sumzv_kernel, one block), then one row per thread
+__global__ void inverse_x_kernel(const uint64_t* q, const uint64_t* rowsum, const double* szv, size_t rows,
+                                 double cols, double zmin, double zmax, double delta, double* x) {
+  const double step = __ddiv_rn(__dsub_rn(zmax, zmin), delta);
+  const double step2 = __dmul_rn(step, step);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < rows; i += (size_t)gridDim.x * blockDim.x)
+    x[i] = inverse_x_row(q[2 * i], q[2 * i + 1], rowsum[i], cols, szv[0], zmin, step, step2);
+}
+
+pcb_status launch_inverse_x(const uint64_t* q, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
+                            size_t rows, size_t cols, double zmin, double zmax, double delta, double* x,
+                            cudaStream_t stream) {
+  double* szv = nullptr;
+  long long* seg = nullptr;
+  pcb_status e = scratch_alloc(8, (void**)&szv, stream);
+  if (!e) e = scratch_alloc(16, (void**)&seg, stream);
+  const long long hseg[2] = {0, (long long)cols};
+  if (!e) e = cuda_check(cudaMemcpyAsync(seg, hseg, 16, cudaMemcpyHostToDevice, stream));
+  if (!e) {
+    sumzv_kernel<<<1, 128, 0, stream>>>(q_z, q_nv, seg, 1, zmin, zmax, delta, szv);
+    count_launch();
+    inverse_x_kernel<<<small_grid(rows), 256, 0, stream>>>(q, rowsum, szv, rows, (double)cols, zmin, zmax, delta, x);
+    count_launch();
+    e = cuda_check(cudaGetLastError());
+  }
+  if (!e) e = cuda_check(cudaStreamSynchronize(stream));  // hseg is a host temporary
+  scratch_free(szv, stream);
+  scratch_free(seg, stream);
+  return e;
 }
 
 #define PCB_INSTANTIATE(S)                                                                                         \

@@ -31,3 +31,17 @@ def test_facade_library_exports_the_reference_api():
     out = subprocess.run(["nm", "-D", "--defined-only", str(lib)], capture_output=True, text=True).stdout
     for sym in ("_ZN6pcadmm8Paillier18crt_encrypt_with_rERKNS_6BigNatES3_", "_ZN6pcadmm6keygenERNS_3RngEmNS_5GModeE"):
         assert sym in out, sym
+
+
+@pytest.mark.gpu
+def test_reference_test_quantize_through_the_facade():
+    """The reference's tests/test_quantize.cpp against the B200 quantizer API (gamma2 / gamma1,
+    combined integer update and its inverse on the device): 10 cases, the reference's 24,057
+    checks."""
+    qbin = BIN.parent / "test_quantize_b200"
+    if not qbin.exists():
+        pytest.skip("facade test binary not built (needs /root/reference at build time)")
+    r = subprocess.run([str(qbin), "--list"], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "cases: 10 | failed: 0 | skipped: 0 | checks: 24057 | failures: 0" in r.stdout
