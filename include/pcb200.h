@@ -145,6 +145,13 @@ void pcb_share_destroy(pcb_share* share);
 pcb_status pcb_delegated_power(pcb_share* share, const uint32_t* base, uint32_t base_limbs, const uint32_t* obf,
                                uint32_t obf_limbs, size_t count, uint32_t* out, pcb_stream stream);
 
+/* out_i = value_i + mask_i * n_eps — obfuscate_exponent (protocol.cpp:11-13), the master's masked
+ * exponents for the edges' delegated powers.  value: count x value_limbs, mask: count u64 (draw_mask,
+ * protocol.cpp:86-93), n_eps: ne_limbs (n * eps), out: count x out_limbs (>= ne_limbs + 3). */
+pcb_status pcb_obfuscate_exponent(const uint32_t* value, uint32_t value_limbs, const uint64_t* mask,
+                                  const uint32_t* n_eps, uint32_t ne_limbs, size_t count, uint32_t* out,
+                                  uint32_t out_limbs, pcb_stream stream);
+
 /* c_i = CRT((p2_g_power_i mod p^2) r_i^(n mod phi(p^2)) mod p^2, (1 + m_i n) r_i^(n mod phi(q^2)) mod q^2)
  * — Paillier::finish_split_encrypt (paillier.cpp:402-414).  Statuses as pcb_encrypt. */
 pcb_status pcb_finish_split_encrypt(pcb_ctx* ctx, const uint32_t* m, uint32_t m_limbs, const uint32_t* p2_g_power,

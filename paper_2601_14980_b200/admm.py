@@ -73,6 +73,33 @@ class SessionResult:
     iter_seconds: list = field(default_factory=list)
 
 
+def draw_mask(rng: Rng, bits: int = 64) -> int:
+    """draw_mask (protocol.cpp:86-93): a non-zero mask of `bits` bits (0 = masking off)."""
+    if bits == 0:
+        return 0
+    if bits > 64:
+        raise ValueError("mask width above 64")
+    while True:
+        m = rng.next() if bits == 64 else rng.next() >> (64 - bits)
+        if m:
+            return m
+
+
+def draw_masks(rng: Rng, count: int) -> np.ndarray:
+    """count x draw_mask(rng, 64) as a u64 array: the counter form of splitmix64, with the
+    serial retry on a (probability 2^-64) zero draw kept exact."""
+    GAMMA = 0x9E3779B97F4A7C15
+    with np.errstate(over="ignore"):
+        z = np.uint64(rng.state) + np.arange(1, count + 1, dtype=np.uint64) * np.uint64(GAMMA)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    if count and not (z == 0).any():
+        rng.state = (rng.state + count * GAMMA) & MASK64
+        return z
+    return np.array([draw_mask(rng) for _ in range(count)], dtype=np.uint64)
+
+
 def split_columns(cols: int, k: int) -> list[int]:
     """admm.cpp:77-83."""
     if cols < 1 or k < 1 or k > cols:
@@ -253,18 +280,22 @@ class EncryptedSession(ShardedDriver):
         _raise_for(self.lib.pcb_ctx_set_priority(self.master._ctx, 1), "priority")
         _raise_for(self.lib.pcb_ctx_set_priority(self.edge._ctx, 1), "priority")
         _raise_for(self.lib.pcb_ctx_set_priority(self.pre._ctx, 0), "priority")
+        self.delegated_pows = 0  # RoleStats.delegated_pows of this rank's edges (protocol.hpp:43-46)
         if cfg.variant == "collab":
-            # the edges' CrtShare {p^2, phi(p^2)} (paillier.hpp:64-66); n eps and the masks of
-            # obfuscate_exponent (protocol.cpp:11-13, 335-356): any mask gives the same powers
+            # the edges' CrtShare {p^2, phi(p^2)} (paillier.hpp:64-66), n eps, and the mask stream
+            # Rng(seed ^ "maskmask") of protocol.cpp:334: first one draw_mask per edge for its
+            # decryption exponent obf_dec (session_init, 352-353), then per iteration and block c_k
+            # masks for z and c_k for -v (440-446).  Every rank walks the whole stream.
+            import math
+
             from .paillier import crt_share
 
             self.share = crt_share(keys, device)
-            import math
-
             lam = (keys.p - 1) * (keys.q - 1) // math.gcd(keys.p - 1, keys.q - 1)
             self.n_eps = keys.n * int(lam)
             self.eps = int(lam)
-            self.mask_rng = Rng(cfg.seed ^ 0x636F6C6C61622121)
+            self.mask_rng = Rng(cfg.seed ^ 0x6D61736B6D61736B)
+            self.obf_dec = [self.eps + draw_mask(self.mask_rng) * self.n_eps for _ in range(cfg.nodes)]
 
     def _stream(self):
         import torch
@@ -415,42 +446,63 @@ class EncryptedSession(ShardedDriver):
                            "offline encryption")
             self.rn_ready[slot].record(ps)
 
-    def _masks(self, count: int) -> list[int]:
-        return [self.mask_rng.next() for _ in range(count)]
+    def _collab_setup(self):
+        """Device-resident constants of the collaborative variant for this rank's blocks."""
+        import torch
+
+        n = self.n_own
+        S = self.share.S
+        self.ne_words = (self.n_eps.bit_length() + 31) // 32
+        self.ow = self.ne_words + 3  # value (< 2^64) + mask (< 2^64) * n_eps
+        self.neps_dev = torch.from_numpy(L.int_to_limbs(self.n_eps, self.ne_words).view(np.int32)).to(self.dev)
+        g = L.int_to_limbs(self.master.n + 1, 2 * S).view(np.int32)
+        self.gbase = torch.from_numpy(np.tile(g, (2 * n, 1))).to(self.dev)  # g for every delegated g power
+        rows = []
+        for k in self.mine:  # each edge's obf_dec, repeated over its block's rows
+            rows.append(np.tile(L.int_to_limbs(self.obf_dec[k], self.ow), (self.sizes[k], 1)))
+        self.obf_dec_rows = torch.from_numpy(np.concatenate(rows).view(np.int32)).to(self.dev) if rows else None
+        self.obf_buf = torch.empty((2 * n, self.ow), dtype=torch.int32, device=self.dev)
+
+    def _iteration_masks(self):
+        """This iteration's masks for all blocks in reference order (block k: c_k for z, then c_k
+        for -v), this rank's draws gathered into batch order [z_own ; -v_own] (like the r stream)."""
+        import torch
+
+        m = draw_masks(self.mask_rng, 2 * sum(self.sizes))
+        idx = self.rperm.cpu().numpy()
+        return torch.from_numpy(m[idx].view(np.int64)).to(self.dev)
 
     def _collab_encrypt(self, q, r, ct):
-        """Alg. 3 encryption: the edge returns g^(obf(q) mod phi(p^2)) mod p^2 (delegated_power,
-        protocol.cpp:248-249), the master finishes with finish_split_encrypt (paillier.cpp:402-414)."""
-        import torch
-
-        qs = q.cpu().numpy().view(np.uint64).reshape(-1).tolist()
-        obf = [int(v) + k * self.n_eps for v, k in zip(qs, self._masks(len(qs)))]
-        ow = max(1, max(o.bit_length() for o in obf) // 32 + 1)
-        g = np.zeros((len(qs), 2 * self.share.S), np.uint32)
-        g[:] = L.int_to_limbs(self.master.n + 1, 2 * self.share.S)
-        gp = self.share.delegated_power_batch(g, L.ints_to_limbs(obf, ow))
-        G = torch.from_numpy(gp.view(np.int32)).to(self.dev)
-        st = np.zeros(len(qs), np.int32)
-        out = torch.empty_like(ct)
-        torch.cuda.current_stream(self.device).synchronize()
-        _raise_for(self.lib.pcb_finish_split_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(G), gp.shape[1], L.ptr(r),
-                                                     len(qs), L.ptr(out), L.ptr(st), None),
-                   "finish_split_encrypt")
-        return out
+        """Alg. 3 encryption, device-resident: obfuscate_exponent(q, n eps, mask) on the master
+        (protocol.cpp:11-13, 440-446), the edge's delegated g powers (protocol.cpp:244-249), then the
+        master's finish_split_encrypt (paillier.cpp:402-414) with the same r stream as the basic
+        variant (protocol.cpp:285-288)."""
+        st = self._stream()
+        n2 = q.shape[0]
+        if not hasattr(self, "gbase"):
+            self._collab_setup()
+        mask = self._iteration_masks()
+        _raise_for(self.lib.pcb_obfuscate_exponent(L.ptr(q), 2, L.ptr(mask), L.ptr(self.neps_dev), self.ne_words, n2,
+                                                   L.ptr(self.obf_buf), self.ow, st), "obfuscate_exponent")
+        gp = self.share.delegated_power_tensor(self.gbase, self.obf_buf, st)
+        self.delegated_pows += n2
+        _raise_for(self.lib.pcb_finish_split_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(gp), gp.shape[1], L.ptr(r),
+                                                     n2, L.ptr(ct), L.ptr(self.st_enc), st), "finish_split_encrypt")
+        if self.capture is not None:
+            self.capture.setdefault("obf", []).append(self.obf_buf.clone())
+        return ct
 
     def _collab_dec_powers(self, upd):
-        """Edge side of Alg. 3 decryption: upd^(obf_dec mod phi(p^2)) mod p^2 (protocol.cpp:226, 492)."""
+        """Edge side of Alg. 3 decryption, device-resident: upd^(obf_dec_k mod phi(p^2)) mod p^2
+        with the edge's own obf_dec (protocol.cpp:226-227, 288-291)."""
         import torch
 
-        torch.cuda.current_stream(self.device).synchronize()
         n = upd.shape[0]
-        obf_dec = [self.eps + k * self.n_eps for k in self._masks(n)]
-        ow = max(1, max(o.bit_length() for o in obf_dec) // 32 + 1)
-        px = self.share.delegated_power_batch(upd.cpu().numpy().view(np.uint32), L.ints_to_limbs(obf_dec, ow))
-        W = 2 * self.L
-        full = np.zeros((n, W), np.uint32)
+        px = self.share.delegated_power_tensor(upd, self.obf_dec_rows, self._stream())
+        self.delegated_pows += n
+        full = torch.zeros((n, 2 * self.L), dtype=torch.int32, device=self.dev)
         full[:, : px.shape[1]] = px
-        return torch.from_numpy(full.view(np.int32)).to(self.dev)
+        return full
 
     def step_all(self, t: int) -> int:
         """The iteration on the high-priority session stream, joined back to the caller's stream."""
@@ -490,6 +542,7 @@ class EncryptedSession(ShardedDriver):
             ct = torch.empty((2 * n, W), dtype=torch.int32, device=self.dev)
             if cfg.variant == "collab":
                 ct = self._collab_encrypt(q, self.rn[slot][:, : self.L].contiguous(), ct)
+                self.bad |= self.st_enc.ne(0).any().to(torch.int32)
             else:
                 _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(self.rn[slot]), 2 * n,
                                                    L.ptr(ct), L.ptr(self.st_enc), st), "Enc z, -v")
@@ -497,6 +550,8 @@ class EncryptedSession(ShardedDriver):
             if self.capture is not None and t < self.capture.get("iters", 0):
                 self.capture.setdefault("q", []).append(q.clone())
                 self.capture.setdefault("ct", []).append(ct.clone())
+        if not n and cfg.variant == "collab":
+            draw_masks(self.mask_rng, 2 * sum(self.sizes))  # keep the shared mask stream in step
         self.enc_done.record(cur)
         if t + 1 < cfg.iters:
             self._precompute(1 - slot)

@@ -338,6 +338,10 @@ pcb_status launch_onepmn(const uint32_t* m, int ml, const uint32_t* rn, const ui
 pcb_status launch_quantize(const double* v, size_t count, double zmin, double zmax, double delta, int fine,
                            uint64_t* q, unsigned long long* clamps, int32_t* err, cudaStream_t stream);
 pcb_status launch_status_flag(const int32_t* st, size_t count, int32_t* err, cudaStream_t stream);
+pcb_status launch_obfuscate(const uint32_t* value, int vw, const uint64_t* mask, const uint32_t* neps, int nw,
+                            size_t count, uint32_t* out, int ow, cudaStream_t stream);
+pcb_status launch_mod_words(const uint32_t* a, int aw, size_t count, const uint32_t* v_norm, int s, int shift,
+                            uint32_t* out, cudaStream_t stream);
 pcb_status launch_combined_update(const uint64_t* qa, const uint64_t* qb, const uint64_t* qz, const uint64_t* qnv,
                                   size_t rows, size_t cols, uint64_t* out, cudaStream_t stream);
 pcb_status launch_inverse_x(const uint64_t* q, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
@@ -1488,6 +1492,8 @@ struct pcb_share {  // an edge's CrtShare (paillier.hpp:64-66): p^2 and phi(p^2)
   HBN p2, phi;
   int S = 0;
   RnsXModulus md;
+  uint32_t* d_phi = nullptr;  // phi(p^2) normalised for the device long division (exponent reduction)
+  int phi_words = 0, phi_shift = 0;
 };
 extern "C" {
 
@@ -1507,6 +1513,12 @@ pcb_status pcb_share_create(pcb_share** out, int device, const uint32_t* p2, uin
     if (!rnsx_shape(32 * sh->S, &K) || sh->p2.bit_length() <= 1024) return PCB_E_UNSUPPORTED;  // 2048/3072-bit keys
     if (cudaSetDevice(device) != cudaSuccess) return PCB_E_CUDA;
     if (!rnsx_build(sh->p2, sh->p2, sh->S, K, &sh->md)) return PCB_E_UNSUPPORTED;
+    // phi(p^2) shifted so its top word has the top bit set (Knuth D divisor)
+    sh->phi_words = (int)((sh->phi.bit_length() + 31) / 32);
+    sh->phi_shift = (int)(32 * sh->phi_words - sh->phi.bit_length());
+    const std::vector<uint32_t> vn = (sh->phi << (size_t)sh->phi_shift).limbs(sh->phi_words);
+    if (cudaMalloc(&sh->d_phi, vn.size() * 4) != cudaSuccess) return PCB_E_ALLOC;
+    if (cudaMemcpy(sh->d_phi, vn.data(), vn.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
   } catch (const std::bad_alloc&) {
     return PCB_E_ALLOC;
   } catch (...) {
@@ -1520,11 +1532,12 @@ void pcb_share_destroy(pcb_share* sh) {
   if (!sh) return;
   cudaSetDevice(sh->device);
   rnsx_free(&sh->md);
+  if (sh->d_phi) cudaFree(sh->d_phi);
   delete sh;
 }
 
 // delegated_power (protocol.cpp:15-18): out_i = (base_i mod p^2)^(obf_i mod phi(p^2)) mod p^2.
-// The exponent reduction is host work (big-integer mod per element); the powers run on the RNS
+// The exponent reduction runs on the device (mod_words_kernel); the powers run on the RNS
 // core with a per-element 4-bit window table.
 pcb_status pcb_delegated_power(pcb_share* sh, const uint32_t* base, uint32_t base_limbs, const uint32_t* obf,
                                uint32_t obf_limbs, size_t count, uint32_t* out, pcb_stream stream) {
@@ -1533,47 +1546,35 @@ pcb_status pcb_delegated_power(pcb_share* sh, const uint32_t* base, uint32_t bas
   if (count == 0) return PCB_OK;
   if (cudaSetDevice(sh->device) != cudaSuccess) return PCB_E_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
-  const int S = sh->S, W = 2 * S;
-  // exponents: obf mod phi(p^2) (host), S words each
-  std::vector<uint32_t> ob((size_t)count * obf_limbs), ex((size_t)count * S, 0);
-  if (is_device_ptr(obf)) {
-    if (cudaMemcpyAsync(ob.data(), obf, ob.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess)
-      return PCB_E_CUDA;
-  } else {
-    std::memcpy(ob.data(), obf, ob.size() * 4);
-  }
-  size_t maxbits = 0;
-  try {
-    for (size_t i = 0; i < count; i++) {
-      const HBN e = mod(HBN::from_limbs(ob.data() + i * obf_limbs, obf_limbs), sh->phi);
-      maxbits = std::max(maxbits, e.bit_length());
-      e.to_limbs(ex.data() + i * S, S);
-    }
-  } catch (...) {
-    return PCB_E_SHAPE;
-  }
-  const int nwin = maxbits ? (int)((maxbits + 3) / 4) : 1;
-  Staged sb, so;
-  uint32_t *bw = nullptr, *ed = nullptr;
+  const int S = sh->S, W = 2 * S, PW = sh->phi_words;
+  Staged sb, so, sx;
+  uint32_t *bw = nullptr, *ed = nullptr, *er = nullptr;
   pcb_status e = stage_in(base, count * base_limbs * 4, st, &sb);
+  if (!e) e = stage_in(obf, count * obf_limbs * 4, st, &sx);
   if (!e) e = stage_out(out, count * S * 4, st, &so);
   if (!e) e = scratch_alloc(count * W * 4, (void**)&bw, st);
   if (!e) e = scratch_alloc(count * S * 4, (void**)&ed, st);
+  if (!e) e = scratch_alloc(count * PW * 4, (void**)&er, st);
   if (!e) e = cuda_check(cudaMemset2DAsync(bw, W * 4, 0, W * 4, count, st));
   if (!e) e = cuda_check(cudaMemcpy2DAsync(bw, W * 4, sb.dev, base_limbs * 4, base_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
-  if (!e) e = cuda_check(cudaMemcpyAsync(ed, ex.data(), ex.size() * 4, cudaMemcpyHostToDevice, st));
+  // exponents obf mod phi(p^2) on the device (mod(obf, phi_p2), protocol.cpp:17), S words each
+  if (!e) e = launch_mod_words((const uint32_t*)sx.dev, (int)obf_limbs, count, sh->d_phi, PW, sh->phi_shift, er, st);
+  if (!e) e = cuda_check(cudaMemset2DAsync(ed, S * 4, 0, S * 4, count, st));
+  if (!e) e = cuda_check(cudaMemcpy2DAsync(ed, S * 4, er, PW * 4, std::min(PW, S) * 4, count, cudaMemcpyDeviceToDevice, st));
+  // windows of the reduced exponents: < phi(p^2), so ceil(bits(phi) / 4) 4-bit windows
+  const int nwin = (int)((sh->phi.bit_length() + 3) / 4);
   const double mm = 2.0 * S * S + S;
   if (!e) e = launch_rnsx(sh->md, kRxPowVar, nullptr, nwin, 16, bw, W, ed, S, count, (uint32_t*)so.dev, st,
                           (4.0 * nwin + nwin + 14.0) * mm);
   if (!e) e = unstage_out(out, &so, st);
   scratch_free(bw, st);
   scratch_free(ed, st);
-  const bool any_host = sb.host || so.host;
+  scratch_free(er, st);
+  const bool any_host = sb.host || so.host || sx.host;
   unstage(&sb, st);
+  unstage(&sx, st);
   unstage(&so, st);
-  (void)any_host;
-  if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;  // ex (host) must outlive its copy
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
   return e;
 }
 
@@ -2274,6 +2275,28 @@ pcb_status pcb_inverse_quantize_x(const uint64_t* q, const uint64_t* rowsum, con
   if (!e) e = unstage_out(x, &sx, st);
   for (auto* p : {&sq, &sr, &sz, &sn, &sx}) unstage(p, st);
   if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  return e;
+}
+
+pcb_status pcb_obfuscate_exponent(const uint32_t* value, uint32_t value_limbs, const uint64_t* mask,
+                                  const uint32_t* n_eps, uint32_t ne_limbs, size_t count, uint32_t* out,
+                                  uint32_t out_limbs, pcb_stream stream) {
+  if (count && (!value || !mask || !n_eps || !out)) return PCB_E_SHAPE;
+  if (!value_limbs || !ne_limbs || out_limbs < ne_limbs + 3 || out_limbs < value_limbs) return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Staged sv, sm, sn, so;
+  pcb_status e = stage_in(value, count * value_limbs * 4, st, &sv);
+  if (!e) e = stage_in(mask, count * 8, st, &sm);
+  if (!e) e = stage_in(n_eps, ne_limbs * 4, st, &sn);
+  if (!e) e = stage_out(out, count * out_limbs * 4, st, &so);
+  if (!e)
+    e = launch_obfuscate((const uint32_t*)sv.dev, (int)value_limbs, (const uint64_t*)sm.dev, (const uint32_t*)sn.dev,
+                         (int)ne_limbs, count, (uint32_t*)so.dev, (int)out_limbs, st);
+  if (!e) e = unstage_out(out, &so, st);
+  const bool any_host = sv.host || sm.host || sn.host || so.host;
+  for (auto* p : {&sv, &sm, &sn, &so}) unstage(p, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
   return e;
 }
 

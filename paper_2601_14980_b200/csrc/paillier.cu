@@ -631,6 +631,102 @@ pcb_status launch_inverse_x(const uint64_t* q, const uint64_t* rowsum, const uin
   return e;
 }
 
+// r = a mod v per element (Knuth algorithm D, remainder only, 32-bit digits): a is count x aw words,
+// v (s >= 2 words) arrives normalised (shifted left by `shift` so its top bit is set); out is
+// count x s words.  One element per thread, the dividend window in local memory.  Used for the edge's
+// exponent reduction obf mod phi(p^2) (delegated_power, protocol.cpp:15-18), which the reference
+// does per element before its modexp.
+constexpr int kModMaxWords = 260;
+__global__ void mod_words_kernel(const uint32_t* a, int aw, int count, const uint32_t* v, int s, int shift,
+                                 uint32_t* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    uint32_t u[kModMaxWords + 2];
+    const uint32_t* ai = a + (size_t)i * aw;
+    const int n = aw > s ? aw : s;  // dividend digits (zero-extended to at least s)
+    // u = a << shift, n + 1 words
+    uint32_t carry = 0;
+    for (int k = 0; k < n; k++) {
+      const uint32_t w = k < aw ? ai[k] : 0u;
+      u[k] = shift ? (w << shift) | carry : w;
+      carry = shift ? w >> (32 - shift) : 0u;
+    }
+    u[n] = carry;
+    const uint64_t vt = v[s - 1], vt2 = v[s - 2];
+    for (int j = n - s; j >= 0; j--) {
+      const uint64_t num = ((uint64_t)u[j + s] << 32) | u[j + s - 1];
+      uint64_t qh = num / vt, rh = num % vt;
+      while (qh >= (1ull << 32) || qh * vt2 > ((rh << 32) | u[j + s - 2])) {
+        qh--;
+        rh += vt;
+        if (rh >= (1ull << 32)) break;
+      }
+      // u[j .. j+s] -= qh * v
+      int64_t borrow = 0;
+      uint64_t mc = 0;
+      for (int k = 0; k < s; k++) {
+        const uint64_t p = qh * v[k] + mc;
+        mc = p >> 32;
+        const int64_t t = (int64_t)u[j + k] - (int64_t)(uint32_t)p + borrow;
+        u[j + k] = (uint32_t)t;
+        borrow = t >> 32;
+      }
+      const int64_t t = (int64_t)u[j + s] - (int64_t)mc + borrow;
+      u[j + s] = (uint32_t)t;
+      if (t < 0) {  // qh was one too large: add v back
+        uint64_t c2 = 0;
+        for (int k = 0; k < s; k++) {
+          const uint64_t t2 = (uint64_t)u[j + k] + v[k] + c2;
+          u[j + k] = (uint32_t)t2;
+          c2 = t2 >> 32;
+        }
+        u[j + s] += (uint32_t)c2;
+      }
+    }
+    uint32_t* o = out + (size_t)i * s;  // remainder = u[0 .. s) >> shift
+    for (int k = 0; k < s; k++)
+      o[k] = shift ? (u[k] >> shift) | (u[k + 1] << (32 - shift)) : u[k];
+  }
+}
+
+pcb_status launch_mod_words(const uint32_t* a, int aw, size_t count, const uint32_t* v_norm, int s, int shift,
+                            uint32_t* out, cudaStream_t stream) {
+  if (s < 2 || aw + 1 > kModMaxWords || s + 1 > kModMaxWords) return PCB_E_UNSUPPORTED;
+  mod_words_kernel<<<small_grid(count), 128, 0, stream>>>(a, aw, (int)count, v_norm, s, shift, out);
+  count_launch();
+  return cuda_check(cudaGetLastError());
+}
+
+// obfuscate_exponent (protocol.cpp:11-13): out = value + mask * n_eps, per element (value: vw words,
+// mask: u64, n_eps: nw words shared, out: ow words, ow >= nw + 3)
+__global__ void obfuscate_kernel(const uint32_t* value, int vw, const uint64_t* mask, const uint32_t* neps, int nw,
+                                 int count, uint32_t* out, int ow) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    const uint64_t mk = mask[i];
+    const uint32_t m0 = (uint32_t)mk, m1 = (uint32_t)(mk >> 32);
+    const uint32_t* v = value + (size_t)i * vw;
+    uint32_t* o = out + (size_t)i * ow;
+    // o = v + m0 * neps + (m1 * neps << 32): column k takes lo(m0 N[k]) + lo(m1 N[k-1]) and the
+    // high halves of the previous column's two products
+    uint64_t carry = 0;
+    uint32_t hb = 0;  // hi(m1 N[k-2]) for column k
+    for (int k = 0; k < ow; k++) {
+      const uint64_t a = k < nw ? (uint64_t)m0 * neps[k] : 0ull;
+      const uint64_t b = (k >= 1 && k - 1 < nw) ? (uint64_t)m1 * neps[k - 1] : 0ull;
+      const uint64_t t = (uint64_t)(k < vw ? v[k] : 0u) + (uint32_t)a + (uint32_t)b + carry + hb;
+      o[k] = (uint32_t)t;
+      carry = (t >> 32) + (a >> 32);
+      hb = (uint32_t)(b >> 32);
+    }
+  }
+}
+
+pcb_status launch_obfuscate(const uint32_t* value, int vw, const uint64_t* mask, const uint32_t* neps, int nw,
+                            size_t count, uint32_t* out, int ow, cudaStream_t stream) {
+  obfuscate_kernel<<<small_grid(count), 256, 0, stream>>>(value, vw, mask, neps, nw, (int)count, out, ow);
+  count_launch();
+  return cuda_check(cudaGetLastError());
+}
+
 #define PCB_INSTANTIATE(S)                                                                                         \
   template pcb_status launch_garner<S>(const CrtEncConsts<S>&, const uint32_t*, const uint32_t*, const int32_t*,  \
                                        uint32_t*, int, size_t, cudaStream_t);                                      \

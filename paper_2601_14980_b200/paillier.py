@@ -491,6 +491,15 @@ class CrtShare:
             L._lib.pcb_share_destroy(h)
             self._h = None
 
+    def delegated_power_tensor(self, base, obf, stream=None):
+        """Device tensors (int32 limb views): base (count, <= 2S), obf (count, k) -> (count, S)
+        tensor of (base mod p^2)^(obf mod phi(p^2)) mod p^2, exponent reduction on the device."""
+        torch = _torch()
+        out = torch.empty((base.shape[0], self.S), dtype=torch.int32, device=base.device)
+        _raise_for(L.lib().pcb_delegated_power(self._h, L.ptr(base), base.shape[1], L.ptr(obf), obf.shape[1],
+                                               base.shape[0], L.ptr(out), stream), "delegated_power")
+        return out
+
     def delegated_power_batch(self, base, obf):
         """base: (count, <= 2S) limbs, obf: (count, k) limbs -> (count, S) limbs of
         (base mod p^2)^(obf mod phi(p^2)) mod p^2."""

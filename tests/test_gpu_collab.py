@@ -138,3 +138,56 @@ def test_collab_session_equals_basic():
     for t in range(3):
         assert collab.x_trace[t].tolist() == basic.x_trace[t].tolist(), t
     assert collab.z.tolist() == basic.z.tolist() and collab.v.tolist() == basic.v.tolist()
+
+
+def test_collab_session_masks_exponents_and_ledger():
+    """Reference fidelity of the collaborative session: the mask stream is Rng(seed ^ "maskmask")
+    (protocol.cpp:334) -- one draw_mask per edge for obf_dec at session init (352-353), then per
+    iteration and block c_k masks for z and c_k for -v (440-446) -- and the obfuscated exponents
+    the edges receive are q + mask * n eps (protocol.cpp:11-13), computed on the device.  Ledger
+    (test_protocol.cpp:179-195, binomial g): the master pays 5 half-exponentiations per element
+    and iteration (2 x 2 r halves + 1 decrypt_with_half; basic: 6), the edges 3 delegated powers."""
+    import math
+
+    import torch
+
+    import admm_oracle as AO
+    from paper_2601_14980_b200 import admm as ADMM
+
+    iters, seed = 2, 7
+    a, y, _ = AO.gen_gaussian_problem(24, 40, 0.1, 4)
+    sizes = AO.split_columns(40, 2)
+    fac, at = [], 0
+    for c in sizes:
+        fac.append(AO.node_factor(a[:, at:at + c], y, 1.0, 2))
+        at += c
+    spec = AO.session_bounds(a, y, 1.0, 1.0, iters, sizes, 1.5, 1e15, fac)
+    keys = P.keygen(P.Rng(1 ^ 0x6B657967656E2E2E), 2048)
+    sess = ADMM.EncryptedSession(keys, ADMM.SessionConfig(nodes=2, iters=iters, variant="collab", seed=seed))
+    sess.capture = {"iters": iters}
+    sess.master.reset_counters()
+    res = sess.run(a, y, factors=fac, spec=spec)
+    n_tot = sum(sizes)
+    # the exponents: replay the reference's mask stream with Python integers
+    eps = (keys.p - 1) * (keys.q - 1) // math.gcd(keys.p - 1, keys.q - 1)
+    n_eps = keys.n * eps
+    rng = P.Rng(seed ^ 0x6D61736B6D61736B)
+    obf_dec = [eps + ADMM.draw_mask(rng) * n_eps for _ in range(2)]
+    assert obf_dec == sess.obf_dec
+    for t in range(iters):
+        q = sess.capture["q"][t].cpu().numpy().view(np.uint64)
+        obf = L.limbs_to_ints(sess.capture["obf"][t].cpu().numpy().view(np.uint32))
+        masks = [ADMM.draw_mask(rng) for _ in range(2 * n_tot)]
+        o = 0
+        for c in sizes:  # block: c masks for z, then c for -v; batch rows [z_all ; -v_all]
+            for i in range(c):
+                assert obf[o + i] == int(q[o + i]) + masks[2 * o + i] * n_eps
+                assert obf[n_tot + o + i] == int(q[n_tot + o + i]) + masks[2 * o + c + i] * n_eps
+            o += c
+    # ledger
+    full, half = sess.master.counters()
+    assert half == 5 * n_tot * iters and sess.delegated_pows == 3 * n_tot * iters
+    basic = ADMM.EncryptedSession(keys, ADMM.SessionConfig(nodes=2, iters=iters, seed=seed)).run(
+        a, y, factors=fac, spec=spec)
+    for t in range(iters):
+        assert res.x_trace[t].tolist() == basic.x_trace[t].tolist()
