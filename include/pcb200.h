@@ -282,6 +282,26 @@ pcb_status pcb_decrypt_update_blocks_async(pcb_ctx* ctx, size_t nblocks, const u
                                            double z_max, double delta, double kappa, double* x,
                                            double* z, double* v, int32_t* err_dev, pcb_stream stream);
 
+/* ---- wire format (interop with the reference's SimCarrier / TcpCarrier sessions) ---------- */
+
+/* put_cipher_vec (wire.cpp:125-132) on the device: u32 BE count, then per element u32 BE byte
+ * length, the minimal big-endian magnitude of c_i (bignat.cpp:414-418) and u32 BE plain_bits_i.
+ * c: count x W LE u32 limbs, plain_bits: count u32 (nullable -> 0).  *out_len gets the byte count;
+ * out = NULL only queries it.  PCB_E_SHAPE if out_cap is too small. */
+pcb_status pcb_wire_put_cipher_vec(const uint32_t* c, uint32_t W, const uint32_t* plain_bits, size_t count,
+                                   uint8_t* out, size_t out_cap, size_t* out_len, pcb_stream stream);
+/* get_cipher_vec (wire.cpp:134-146): parses the vector at byte *off of in (in_len bytes) into c
+ * (count x W limbs, zero-extended) and plain_bits (nullable); *count_out = count, *off advances.
+ * PCB_E_SHAPE on truncation (runtime_error), more than max_count elements or a magnitude wider
+ * than W limbs. */
+pcb_status pcb_wire_get_cipher_vec(const uint8_t* in, size_t in_len, size_t* off, uint32_t W, size_t max_count,
+                                   size_t* count_out, uint32_t* c, uint32_t* plain_bits, pcb_stream stream);
+/* encode_envelope (wire.cpp:148-159): u32 BE (7 + payload_len), type (1..7, wire.hpp:16-24), u16 BE
+ * session, u32 BE iteration, payload.  PCB_E_SHAPE past kFrameCap (length_error).  out = NULL
+ * queries *out_len. */
+pcb_status pcb_encode_envelope(uint8_t type, uint16_t session, uint32_t iteration, const uint8_t* payload,
+                               size_t payload_len, uint8_t* out, size_t out_cap, size_t* out_len, pcb_stream stream);
+
 /* ---- generic primitive + measurement ------------------------------------------------------ */
 
 /* y_i = x_i^e mod m for an odd modulus m (m_limbs <= 96) and a batch-uniform exponent e —

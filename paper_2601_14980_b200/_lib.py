@@ -87,6 +87,12 @@ SIGNATURES = {
                                             C.c_double, C.c_double, _vp, _vp, _vp, _vp, _vp]),
     "pcb_decrypt_update_blocks_half": (C.c_int, [_vp, C.c_size_t, _vp, _vp, _vp, _vp, _vp, _vp, C.c_double,
                                                  C.c_double, C.c_double, C.c_double, _vp, _vp, _vp, _vp, _vp]),
+    "pcb_wire_put_cipher_vec": (C.c_int, [_vp, C.c_uint32, _vp, C.c_size_t, _vp, C.c_size_t,
+                                          C.POINTER(C.c_size_t), _vp]),
+    "pcb_wire_get_cipher_vec": (C.c_int, [_vp, C.c_size_t, C.POINTER(C.c_size_t), C.c_uint32, C.c_size_t,
+                                          C.POINTER(C.c_size_t), _vp, _vp, _vp]),
+    "pcb_encode_envelope": (C.c_int, [C.c_uint8, C.c_uint16, C.c_uint32, _vp, C.c_size_t, _vp, C.c_size_t,
+                                      C.POINTER(C.c_size_t), _vp]),
     "pcb_obfuscate_exponent": (C.c_int, [_vp, C.c_uint32, _vp, _vp, C.c_uint32, C.c_size_t, _vp, C.c_uint32, _vp]),
     "pcb_combined_update": (C.c_int, [_vp, _vp, _vp, _vp, C.c_size_t, C.c_size_t, _vp, _vp]),
     "pcb_inverse_quantize_x": (C.c_int, [_vp, _vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_double, C.c_double,

@@ -40,6 +40,7 @@ SOURCES = [
     "imad_peak.cu",
     "rns.cu",
     "rnsx.cu",
+    "wire.cu",
     "host/hbn.cpp",
 ]
 
