@@ -20,6 +20,9 @@ Algorithm (Bajard-Imbert RNS Montgomery; approximate first base extension, exact
        V'_j = sum_i xi_i W1'_ji = qh'_j C3_j 2^32 (mod m'_j), and r~'_j = REDC(t~'_j C2_j + V'_j)
        in one REDC (t~' C2 + V' < 2 m'^2 + 2^49, so the result stays < 2m')
     5. xi'_j = REDC(r~'_j C4_j), C4 = M'_j^-1;  beta = floor(sum_j xi'_j / m'_j + 2^-20)
+       (rnsx.cu, round 2: S is an FP32 over-estimate -- terms f32(2^23 + (xi' >> 8)) * f32(2^8 / m'),
+       the 2^23 parts subtracted once -- plus 2^-8: S_true lies in [beta, beta + 2^-24) and the FP32
+       error is ~2^-12.5, so any estimate in [S_true, S_true + 1 - 2^-24) floors to beta)
     6. r~_i = REDC(sum_j xi'_j W2_ij + beta W2_ik),  W2_ij = M'_j 2^64 mod m_i,
        W2_ik = -M' 2^64 mod m_i                                       (GEMM 2, exact)
   The GEMMs run on int8 tensor cores: each 32-bit operand is split into 4 bytes on both sides,
@@ -150,8 +153,20 @@ class RnsCtx:
             r1 = self.redc(tb * self.C2, mBp, self.minvBp) + self.redc(qh * self.C3, mBp, self.minvBp)
             r1 = np.where(r1 >= 2 * mBp, r1 - 2 * mBp, r1)
         xip = self.redc(r1 * self.C4, mBp, self.minvBp)
-        S = float(np.sum(xip.astype(np.float64) * self.invBp))
-        beta = int(np.floor(S + 2.0 ** -20))
+        if self.fused:  # rnsx.cu rx_e1: FP32 over-estimate, 2^-8 bias (one-sided bound, see module doc)
+            f = ((xip >> np.uint64(8)) | np.uint64(0x4B000000)).astype(np.uint32).view(np.float32)
+            inv8 = (256.0 / self.mBp.astype(np.float64)).astype(np.float32)
+            sp = np.float32(0.0)
+            for a, b in zip(f, inv8):
+                sp = np.float32(sp + np.float32(a * b))
+            cthr = np.float32(0.0)
+            for b in inv8:
+                cthr = np.float32(cthr + np.float32(np.float32(8388608.0) * b))
+            beta = int(np.floor(np.float32(np.float32(sp - cthr) + np.float32(0.00390625))))
+        else:
+            S = float(np.sum(xip.astype(np.float64) * self.invBp))
+            beta = int(np.floor(S + 2.0 ** -20))
+        assert beta == int(sum(int(a) * ((self.Mp // int(m)) % self.Mp) for a, m in zip(xip, self.mBp)) // self.Mp)
         xiext = np.concatenate([xip, np.array([beta], np.uint64)])
         ra = self.redc(self.gemm_bytes(xiext, self.W2, mB), mB, self.minvB)
         for v, m in ((ra, mB), (r1, mBp)):

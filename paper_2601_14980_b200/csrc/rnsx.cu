@@ -207,6 +207,7 @@ struct Thr {
   uint32_t dbi, dph;
   bool nowait;
   uint32_t rank;  // CTA rank in the pair (cta_group::2): rank 1 signals the leader's barriers
+  float cthr;     // sum over this thread's primes of 2^23 (2^8 / m'): the bias of the beta terms
   uint64_t *dfull, *dfree, *a1, *a2;
 };
 
@@ -308,10 +309,15 @@ __device__ __forceinline__ void rx_s1(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::
 }
 
 template <class C>
-__device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t* A2, double* sS, uint64_t* a2) {
+__device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t* A2, float* sS, uint64_t* a2) {
   constexpr int NC = C::NC;
   // ---- 2. GEMM-1 epilogue per chunk: qh', r' (new B'), xi' -> A2, partial beta ------------------
-  double sp = 0.0;
+  // beta = floor(S), S = sum_j xi'_j / m'_j = beta + r'/M' with r'/M' < 2^-24 (M' > 2^24 (2K+2) N).
+  // An over-estimate within [S, S + 1 - 2^-24) gives the same floor, so FP32 suffices: each term is
+  // f(xi' >> 8) * (2^8 / m') with f(u) = the float 2^23 + u (bit trick, no conversion instruction),
+  // the 2^23 parts (T.cthr) subtracted once, and a bias of 2^-8 above the total error bound
+  // (~2^-12.5: truncated low bytes, FP32 roundings of 72 terms at magnitude < 2^6).
+  float sp = 0.0f;
 #pragma unroll
   for (int c = 0; c < NC; c++) {
     const int ptc = C::ptc(c), nq = (ptc + 3) / 4;
@@ -331,18 +337,18 @@ __device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t
         const uint32_t r = redc((uint64_t)XQ[w] * rq.z + V, rq.x, rq.y);
         XQ[w] = r;
         xp[t] = mulr(r, rr.x, rq.x, rq.y);
-        sp = __fma_rn((double)xp[t], __hiloint2double((int)rr.z, (int)rr.y), sp);  // beta needs 2^-20 only
+        sp = __fmaf_rn(__uint_as_float((xp[t] >> 8) | 0x4B000000u), __uint_as_float(rr.y), sp);
       }
       uint8_t* dst = A2 + umma::kmajor_off(T.e, 4 * (C::cp0(c) + C::slot(c, T.g, j)), C::TILE);
       if (QT == 4) stq<4>(dst, xp); else stq<2>(dst, xp);
     }
   }
-  sS[T.g * C::TILE + T.e] = sp;
+  sS[T.g * C::TILE + T.e] = __fsub_rn(sp, T.cthr);
   umma::fence_async_smem();
   umma::named_sync(1, C::NCT);
   if (T.g == 0) {
-    const double S = sS[T.e] + sS[C::TILE + T.e] + sS[2 * C::TILE + T.e] + sS[3 * C::TILE + T.e];
-    const uint32_t beta = (uint32_t)floor(S + 9.5367431640625e-07);  // + 2^-20
+    const float S = sS[T.e] + sS[C::TILE + T.e] + sS[2 * C::TILE + T.e] + sS[3 * C::TILE + T.e];
+    const uint32_t beta = (uint32_t)floorf(S + 0.00390625f);  // + 2^-8 (see above)
     *reinterpret_cast<uint4*>(A2 + umma::kmajor_off(T.e, 4 * C::K, C::TILE)) = make_uint4(beta, 0, 0, 0);
     umma::fence_async_smem();
   }
@@ -378,7 +384,7 @@ template <class C>
 __device__ __forceinline__ void rx_mm(uint32_t (&XB)[C::RPT], uint32_t (&XQ)[C::RPT], bool sq, const uint32_t* ybase,
                                       int yvs, Thr<C>& T) {
   rx_s1<C>(XB, XQ, sq, ybase, yvs, T, T.sm + C::OFF_A1, T.a1);
-  rx_e1<C>(XQ, T, T.sm + C::OFF_A2, reinterpret_cast<double*>(T.sm + C::OFF_S), T.a2);
+  rx_e1<C>(XQ, T, T.sm + C::OFF_A2, reinterpret_cast<float*>(T.sm + C::OFF_S), T.a2);
   rx_e2<C>(XB, T);
 }
 
@@ -648,8 +654,8 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
     uint8_t* A2a = T.sm + C::OFF_A2;
     uint8_t* A1b = A1a + C::ABLK;
     uint8_t* A2b = A2a + C::ABLK;
-    double* sSa = reinterpret_cast<double*>(T.sm + C::OFF_S);
-    double* sSb = sSa + C::G * C::TILE;
+    float* sSa = reinterpret_cast<float*>(T.sm + C::OFF_S);
+    float* sSb = sSa + C::G * C::TILE;
     const int npairs = (ntiles + 1) / 2;
     (void)npairs;
 #pragma unroll 1
@@ -689,7 +695,7 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
   if constexpr (C::NT == 3) {
     // Three tiles in flight (small K): the same rotation as above over tiles 0, 1, 2.
     constexpr int NT = C::NT;
-    double* sS0 = reinterpret_cast<double*>(T.sm + C::OFF_S);
+    float* sS0 = reinterpret_cast<float*>(T.sm + C::OFF_S);
 #pragma unroll 1
     for (int k = 0; k < mine; k++) {
       const int pr = blockIdx.x + k * gridDim.x;
@@ -1145,6 +1151,8 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     T.e = qd * 32 + lane;
     T.tl = tm + ((uint32_t)(qd * 32) << 16);
     T.rc = reinterpret_cast<const uint4*>(sm + C::OFF_CONS) + T.g * C::RPT * 3;
+    T.cthr = 0.0f;
+    for (int w = 0; w < C::RPT; w++) T.cthr = __fmaf_rn(8388608.0f, __uint_as_float(T.rc[w * 3 + 2].y), T.cthr);
     T.NT = gridDim.x * C::NCT;
     T.gt = blockIdx.x * C::NCT + tid;
     T.dbi = 0;
@@ -1497,15 +1505,15 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
     c4[j] = inv_mod(mprod_mod(Bp, j, m), m);
     invp[j] = 1.0 / (double)m;
   }
-  // constant records per (g, w): {m, minv, c1, q64} {m', minv', c2, c3} {c4, invp lo, invp hi, q64'}
+  // constant records per (g, w): {m, minv, c1, q64} {m', minv', c2, c3} {c4, f32(2^8 / m'), 0, q64'}
   std::vector<uint32_t> cons((size_t)G * RPT * 12);
   for (int g = 0; g < G; g++)
     for (int w = 0; w < RPT; w++) {
       const int i = prime_of(g, w);
-      uint64_t ib;
-      memcpy(&ib, &invp[i], 8);
-      const uint32_t rec[12] = {B[i],  minv[i], c1[i], q64[i], Bp[i], minv[K + i], c2[i], c3[i],
-                                c4[i], (uint32_t)ib, (uint32_t)(ib >> 32), q64[K + i]};
+      const float inv8 = (float)(256.0 / (double)Bp[i]);
+      uint32_t fb;
+      memcpy(&fb, &inv8, 4);
+      const uint32_t rec[12] = {B[i], minv[i], c1[i], q64[i], Bp[i], minv[K + i], c2[i], c3[i], c4[i], fb, 0u, q64[K + i]};
       memcpy(&cons[((size_t)g * RPT + w) * 12], rec, sizeof rec);
     }
   // constant operand vectors in thread order: [id][g][v][4]

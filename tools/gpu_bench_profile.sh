@@ -9,3 +9,4 @@ ncu --set full --clock-control none --import-source on -k regex:rnsx_kernel --la
     -o gpurun_out/r02_rnsx72_bench python bench.py --steps 1 --warmup 1 --no-cpu-baseline --admm-iters 0 \
     --cfg4-n 0 --e2e-steps 1 > gpurun_out/r02_ncu_bench.log 2>&1
 ls -la gpurun_out
+bash tools/gpu_admm_profile.sh
