@@ -12,7 +12,10 @@ rep, out = sys.argv[1], sys.argv[2]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 d = dict(zip(rows[0], rows[2]))
+units = dict(zip(rows[0], rows[1]))
 f = lambda k: float(d[k])  # noqa: E731
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+fb = lambda k: float(d[k]) * SCALE[units[k]]  # noqa: E731  (bytes, whatever unit ncu printed)
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
@@ -52,8 +55,8 @@ res = {
               "python bench.py --steps 1 --warmup 1 --no-cpu-baseline --admm-iters 0 --cfg4-n 0 --e2e-steps 1 "
               "(tools/gpu_bench_profile.sh): stage 2 of the split CRT Enc of the p half, (1+mn) u^p mod p^2, 2^20 values",
     "duration_ms": f("gpu__time_duration.sum"),
-    "dram_bytes_read": f("dram__bytes_read.sum") * 1e9, "dram_bytes_write": f("dram__bytes_write.sum") * 1e9,
-    "traffic_bytes_per_launch": (f("dram__bytes_read.sum") + f("dram__bytes_write.sum")) * 1e9,
+    "dram_bytes_read": fb("dram__bytes_read.sum"), "dram_bytes_write": fb("dram__bytes_write.sum"),
+    "traffic_bytes_per_launch": fb("dram__bytes_read.sum") + fb("dram__bytes_write.sum"),
     "algorithmic_io_bytes_per_launch": 1048576 * (32 * 4 + 72 * 4),
     "l2_hit_rate_pct": f("lts__t_sector_hit_rate.pct"),
     "pipes": {"issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
