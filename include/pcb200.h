@@ -158,6 +158,14 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* ctx, const uint32_t* m, uint32_t m_
                                     uint32_t pg_limbs, const uint32_t* r, size_t count, uint32_t* c,
                                     int32_t* status, pcb_stream stream);
 
+/* The pooled form — Paillier::finish_split_encrypt_with_factor (paillier.cpp:416-426): rn = the
+ * factor's r^n mod n^2 (RnFactor.full, whose residues mod p^2 / q^2 are half_p2 / half_q2), count x 2L
+ * limbs; c_i = CRT(p2_g_power_i mod p^2, (1 + m_i n) mod q^2) rn_i mod n^2, no exponentiation with r.
+ * rn_i = 0 or >= n^2 fails that element with PCB_E_RANDOMNESS_RANGE.  Statuses as pcb_encrypt. */
+pcb_status pcb_finish_split_encrypt_rn(pcb_ctx* ctx, const uint32_t* m, uint32_t m_limbs, const uint32_t* p2_g_power,
+                                       uint32_t pg_limbs, const uint32_t* rn, size_t count, uint32_t* c,
+                                       int32_t* status, pcb_stream stream);
+
 /* ---- homomorphic operations (public key suffices) ----------------------------------------- */
 
 /* out_i = a_i * b_i mod n^2 — Paillier::hom_add (paillier.cpp:428-432).  plain_bits tracking

@@ -72,6 +72,7 @@ SIGNATURES = {
     "pcb_share_destroy": (None, [_vp]),
     "pcb_delegated_power": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_uint32, C.c_size_t, _vp, _vp]),
     "pcb_finish_split_encrypt": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp, _vp]),
+    "pcb_finish_split_encrypt_rn": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp, _vp]),
     "pcb_hom_add": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
     "pcb_hom_scalar_mul": (C.c_int, [_vp, _vp, _vp, C.c_size_t, _vp, _vp]),
     "pcb_hom_matvec": (C.c_int, [_vp, _vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_uint32, _vp, _vp]),

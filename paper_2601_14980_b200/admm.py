@@ -59,6 +59,37 @@ class SessionConfig:
     seed: int = 1
     over_k: bool = False  # YScaling::full
     variant: str = "basic"  # "collab": paper Alg. 3, the p^2 side of every Enc/Dec delegated to the edges
+    # RandomnessMode (protocol.hpp:17-22): "fresh" draws r per encryption from Rng(seed); "pooled"
+    # draws pool_size r once, precomputes their r^n and cycles them (pool[pool_at++ % pool_size],
+    # protocol.cpp:382-391) -- ciphertexts change, plaintexts and the trajectory do not
+    r_mode: str = "fresh"
+    pool_size: int = 16
+    mask_bits: int = 64  # exponent mask width of the collaborative variant; 0 sends exponents bare
+    use_crt: bool = True  # master arithmetic of the basic variant (the collaborative one is always split)
+    engine: str = "packed"  # Engine::packed | coeff_fft: one CUDA lane; the reference pins both to equal results
+
+    def validate(self) -> None:
+        """The argument errors run_session raises (protocol.cpp:384, 86-88; protocol.hpp:24-41)."""
+        if self.variant not in ("basic", "collab"):
+            raise ValueError(f"unknown protocol variant {self.variant!r}")
+        if self.r_mode not in ("fresh", "pooled"):
+            raise ValueError(f"unknown randomness mode {self.r_mode!r}")
+        if self.r_mode == "pooled" and self.pool_size < 1:
+            raise ValueError("pool size below 1")
+        if self.mask_bits > 64 or self.mask_bits < 0:
+            raise ValueError("mask width above 64")
+        if self.engine not in ("packed", "coeff_fft"):
+            raise ValueError(f"unknown engine {self.engine!r}")
+
+
+@dataclass
+class RoleStats:
+    """pcadmm::RoleStats (protocol.hpp:43-46): the exponentiation ledger of one protocol role under
+    the reference's booking rules (paillier.cpp OpCount), and the edge-side delegated powers."""
+
+    pow_full: int = 0
+    pow_half: int = 0
+    delegated_pows: int = 0
 
 
 @dataclass
@@ -71,6 +102,16 @@ class SessionResult:
     clamps: int = 0
     spec: tuple = None
     iter_seconds: list = field(default_factory=list)
+    # master-side phase accounting (protocol.hpp:58-64, protocol.cpp:316-329, 392, 515-525): t_pre_s
+    # from loop entry through setup and the randomness pool; each iteration splits into the time the
+    # master waits on the edges / the exchange (t_comm_s) and the local remainder (t_loc_s);
+    # t_pre_s + sum(t_loc_s + t_comm_s) == t_master_s up to the loop's own bookkeeping
+    t_pre_s: float = 0.0
+    t_loc_s: list = field(default_factory=list)
+    t_comm_s: list = field(default_factory=list)
+    t_master_s: float = 0.0
+    master: RoleStats = None
+    edges: RoleStats = None  # this rank's edges together
 
 
 def draw_mask(rng: Rng, bits: int = 64) -> int:
@@ -85,19 +126,25 @@ def draw_mask(rng: Rng, bits: int = 64) -> int:
             return m
 
 
-def draw_masks(rng: Rng, count: int) -> np.ndarray:
-    """count x draw_mask(rng, 64) as a u64 array: the counter form of splitmix64, with the
-    serial retry on a (probability 2^-64) zero draw kept exact."""
+def draw_masks(rng: Rng, count: int, bits: int = 64) -> np.ndarray:
+    """count x draw_mask(rng, bits) as a u64 array: the counter form of splitmix64, with the
+    serial retry on a zero draw (probability 2^-bits) kept exact; bits = 0 draws nothing."""
+    if bits == 0:
+        return np.zeros(count, dtype=np.uint64)
+    if bits > 64:
+        raise ValueError("mask width above 64")
     GAMMA = 0x9E3779B97F4A7C15
     with np.errstate(over="ignore"):
         z = np.uint64(rng.state) + np.arange(1, count + 1, dtype=np.uint64) * np.uint64(GAMMA)
         z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         z = z ^ (z >> np.uint64(31))
+        if bits < 64:
+            z = z >> np.uint64(64 - bits)
     if count and not (z == 0).any():
         rng.state = (rng.state + count * GAMMA) & MASK64
         return z
-    return np.array([draw_mask(rng) for _ in range(count)], dtype=np.uint64)
+    return np.array([draw_mask(rng, bits) for _ in range(count)], dtype=np.uint64)
 
 
 def split_columns(cols: int, k: int) -> list[int]:
@@ -183,6 +230,15 @@ class ShardedDriver:
         counted on the device (backends whose steps never synchronise)."""
         return 0
 
+    def iteration_wait(self, t: int) -> float:
+        """Seconds of iteration t the master spent waiting on edge work (the reference's
+        carrier-blocked time covers the edges' compute, protocol.cpp:319-329); read after the
+        iteration's device work has completed.  Collectives are timed by the driver itself."""
+        return 0.0
+
+    def role_stats(self, res: SessionResult) -> None:
+        """Fill res.master / res.edges (backends that keep a ledger)."""
+
     def setup_all(self) -> int:
         """Setup of every block this rank owns (default: one block at a time)."""
         return sum(self.setup_block(k) for k in self.mine)
@@ -205,6 +261,9 @@ class ShardedDriver:
         import torch
 
         cfg = self.cfg
+        cfg.validate()
+        sync = (lambda: torch.cuda.synchronize(self.dev)) if self.dev != "cpu" else (lambda: None)
+        m0 = time.perf_counter()
         n = a.shape[1]
         self.sizes = split_columns(n, cfg.nodes)
         self.offs = np.cumsum([0] + self.sizes[:-1]).tolist()
@@ -215,10 +274,12 @@ class ShardedDriver:
         self.z = torch.zeros(n, dtype=torch.float64, device=self.dev)
         self.v = torch.zeros(n, dtype=torch.float64, device=self.dev)
         res.clamps += self.setup_all()
+        sync()
+        res.t_pre_s = time.perf_counter() - m0
         for t in range(cfg.iters):
-            if self.dev != "cpu":
-                torch.cuda.synchronize(self.dev)
+            it0 = time.perf_counter()
             t0 = time.perf_counter()
+            comm = 0.0
             res.clamps += self.step_all(t)
             # objective on z (admm.cpp:31-34): A z partial sums over this rank's blocks
             az = torch.zeros(a.shape[0], dtype=torch.float64, device=self.dev)
@@ -230,16 +291,28 @@ class ShardedDriver:
             if self.world > 1:
                 import torch.distributed as dist
 
+                sync()
+                c0 = time.perf_counter()
                 dist.all_reduce(az, group=self.group)
                 dist.all_reduce(l1, group=self.group)
+                sync()
+                comm += time.perf_counter() - c0
             r = az - y
             res.objective.append(0.5 * float(r @ r) + cfg.lam * float(l1))
-            if self.dev != "cpu":
-                torch.cuda.synchronize(self.dev)
+            sync()
             res.clamps += self.check_iteration(t)
             res.iter_seconds.append(time.perf_counter() - t0)
+            comm += self.iteration_wait(t)
             if record_trace:
-                res.x_trace.append(self._gather(self.x.clone()))
+                c0 = time.perf_counter()
+                xt = self._gather(self.x.clone())
+                if self.world > 1:
+                    comm += time.perf_counter() - c0
+                res.x_trace.append(xt)
+            res.t_comm_s.append(comm)
+            res.t_loc_s.append(time.perf_counter() - it0 - comm)
+        res.t_master_s = time.perf_counter() - m0
+        self.role_stats(res)
         res.x, res.z, res.v = (self._gather(t_).cpu().numpy() for t_ in (self.x, self.z, self.v))
         res.x_trace = [xt.cpu().numpy() for xt in res.x_trace]
         return res
@@ -281,6 +354,8 @@ class EncryptedSession(ShardedDriver):
         _raise_for(self.lib.pcb_ctx_set_priority(self.edge._ctx, 1), "priority")
         _raise_for(self.lib.pcb_ctx_set_priority(self.pre._ctx, 0), "priority")
         self.delegated_pows = 0  # RoleStats.delegated_pows of this rank's edges (protocol.hpp:43-46)
+        self.adj_full = self.adj_half = 0  # ledger bookings the device path does not do itself (role_stats)
+        cfg.validate()
         if cfg.variant == "collab":
             # the edges' CrtShare {p^2, phi(p^2)} (paillier.hpp:64-66), n eps, and the mask stream
             # Rng(seed ^ "maskmask") of protocol.cpp:334: first one draw_mask per edge for its
@@ -295,7 +370,7 @@ class EncryptedSession(ShardedDriver):
             self.n_eps = keys.n * int(lam)
             self.eps = int(lam)
             self.mask_rng = Rng(cfg.seed ^ 0x6D61736B6D61736B)
-            self.obf_dec = [self.eps + draw_mask(self.mask_rng) * self.n_eps for _ in range(cfg.nodes)]
+            self.obf_dec = [self.eps + draw_mask(self.mask_rng, cfg.mask_bits) * self.n_eps for _ in range(cfg.nodes)]
 
     def _stream(self):
         import torch
@@ -384,6 +459,8 @@ class EncryptedSession(ShardedDriver):
         self.clamps_dev = torch.zeros(2, dtype=torch.int64, device=self.dev)
         self.clamps_seen = 0
         self.rperm = torch.zeros(0, dtype=torch.int64, device=self.dev)
+        self.ev_wait = []  # (start, end) events around edge work the master waits on, this iteration
+        self._build_pool()
         if n_own == 0:
             return 0
         b_all = torch.cat([self.factors[k][0].reshape(-1) for k in own]).contiguous()
@@ -423,6 +500,32 @@ class EncryptedSession(ShardedDriver):
         return cl_b + cla[0] + cla[1]
 
 
+    def _build_pool(self) -> None:
+        """Pooled randomness (protocol.cpp:382-388): pool_size r from the master stream Rng(seed),
+        each made into an RnFactor once -- r^n mod n^2 (= Enc(0; r)) on the device.  Every rank
+        builds the same pool (it is pool_size elements); the ledger books it once, on rank 0, as
+        make_rn_factor does (1 full + 2 halves per factor, paillier.cpp:371-383)."""
+        import torch
+
+        cfg = self.cfg
+        if cfg.r_mode != "pooled":
+            return
+        P, st = cfg.pool_size, self._stream()
+        self.pool_r = torch.empty((P, self.L), dtype=torch.int32, device=self.dev)
+        s_ = C.c_uint64(self.rng_r.state)
+        _raise_for(self.lib.pcb_sample_r(self.master._ctx, C.byref(s_), P, L.ptr(self.pool_r), st), "sample_r")
+        self.rng_r.state = s_.value
+        self.pool_rn = torch.empty((P, 2 * self.L), dtype=torch.int32, device=self.dev)
+        m0 = torch.zeros((P, 1), dtype=torch.int32, device=self.dev)
+        _raise_for(self.lib.pcb_encrypt(self.master._ctx, L.ptr(m0), 1, L.ptr(self.pool_r), P, L.ptr(self.pool_rn), 1,
+                                        None, st), "make_rn_factor")
+        # pcb_encrypt(use_crt) booked 2 halves per factor; make_rn_factor also books its full
+        if self.rank == 0:
+            self.adj_full += P
+        else:
+            self.adj_half -= 2 * P
+        self.pool_at = 0
+
     def _precompute(self, slot: int) -> None:
         """Offline half of the next iteration's encryptions on the side stream: draw the master r
         stream for ALL blocks (reference order), keep this rank's draws in batch order, and
@@ -433,6 +536,15 @@ class EncryptedSession(ShardedDriver):
         ps.wait_event(self.enc_done)  # the slot was last read by an earlier online encryption
         with torch.cuda.stream(ps):
             st = C.c_void_p(ps.cuda_stream)
+            if self.cfg.r_mode == "pooled":
+                # next_factor() in reference order: this iteration's draws sit at stream positions
+                # pool_at + [0, 2N); block k's z draws at 2 off_k + i, its -v draws after them
+                if self.n_own:
+                    idx = torch.remainder(self.rperm + self.pool_at, self.cfg.pool_size)
+                    torch.index_select(self.pool_rn, 0, idx, out=self.rn[slot])
+                self.pool_at += self.rall.shape[0]
+                self.rn_ready[slot].record(ps)
+                return
             s_ = C.c_uint64(self.rng_r.state)
             _raise_for(self.lib.pcb_sample_r(self.pre._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
                        "sample_r")
@@ -442,8 +554,8 @@ class EncryptedSession(ShardedDriver):
             elif self.n_own:
                 r_in = self.rall.index_select(0, self.rperm).contiguous()
                 _raise_for(self.lib.pcb_encrypt(self.pre._ctx, L.ptr(self.m0), 1, L.ptr(r_in), r_in.shape[0],
-                                                L.ptr(self.rn[slot]), 1, L.ptr(self.st_pre[slot]), st),
-                           "offline encryption")
+                                                L.ptr(self.rn[slot]), 1 if self.cfg.use_crt else 0,
+                                                L.ptr(self.st_pre[slot]), st), "offline encryption")
             self.rn_ready[slot].record(ps)
 
     def _collab_setup(self):
@@ -468,7 +580,7 @@ class EncryptedSession(ShardedDriver):
         for -v), this rank's draws gathered into batch order [z_own ; -v_own] (like the r stream)."""
         import torch
 
-        m = draw_masks(self.mask_rng, 2 * sum(self.sizes))
+        m = draw_masks(self.mask_rng, 2 * sum(self.sizes), self.cfg.mask_bits)
         idx = self.rperm.cpu().numpy()
         return torch.from_numpy(m[idx].view(np.int64)).to(self.dev)
 
@@ -484,13 +596,52 @@ class EncryptedSession(ShardedDriver):
         mask = self._iteration_masks()
         _raise_for(self.lib.pcb_obfuscate_exponent(L.ptr(q), 2, L.ptr(mask), L.ptr(self.neps_dev), self.ne_words, n2,
                                                    L.ptr(self.obf_buf), self.ow, st), "obfuscate_exponent")
+        ev = self._wait_begin()
         gp = self.share.delegated_power_tensor(self.gbase, self.obf_buf, st)
+        self._wait_end(ev)
         self.delegated_pows += n2
-        _raise_for(self.lib.pcb_finish_split_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(gp), gp.shape[1], L.ptr(r),
-                                                     n2, L.ptr(ct), L.ptr(self.st_enc), st), "finish_split_encrypt")
+        if self.cfg.r_mode == "pooled":  # finish_split_encrypt_with_factor (protocol.cpp:401-403)
+            _raise_for(self.lib.pcb_finish_split_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(gp), gp.shape[1],
+                                                            L.ptr(r), n2, L.ptr(ct), L.ptr(self.st_enc), st),
+                       "finish_split_encrypt_with_factor")
+        else:
+            _raise_for(self.lib.pcb_finish_split_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(gp), gp.shape[1],
+                                                         L.ptr(r), n2, L.ptr(ct), L.ptr(self.st_enc), st),
+                       "finish_split_encrypt")
         if self.capture is not None:
             self.capture.setdefault("obf", []).append(self.obf_buf.clone())
         return ct
+
+    def _wait_begin(self):
+        import torch
+
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(torch.cuda.current_stream(self.device))
+        return ev
+
+    def _wait_end(self, ev0) -> None:
+        import torch
+
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(torch.cuda.current_stream(self.device))
+        self.ev_wait.append((ev0, ev))
+
+    def iteration_wait(self, t: int) -> float:
+        """Device time of the edge work the master waited on this iteration: the edge step and,
+        collaborative, the delegated g powers and Dec powers (events on the session stream)."""
+        w = sum(a.elapsed_time(b) for a, b in self.ev_wait) / 1e3
+        self.ev_wait = []
+        return w
+
+    def role_stats(self, res: SessionResult) -> None:
+        """The master's ledger = the master and offline-precompute contexts' counters plus the
+        bookings the device path does not do itself (pool build; decrypt_vec(use_crt = false) is
+        one full per element, paillier.cpp:345-350, where the device always runs the CRT form)."""
+        f1, h1 = self.master.counters()
+        f2, h2 = self.pre.counters()
+        res.master = RoleStats(f1 + f2 + self.adj_full, h1 + h2 + self.adj_half, 0)
+        fe, he = self.edge.counters()
+        res.edges = RoleStats(fe, he, self.delegated_pows)
 
     def _collab_dec_powers(self, upd):
         """Edge side of Alg. 3 decryption, device-resident: upd^(obf_dec_k mod phi(p^2)) mod p^2
@@ -529,7 +680,7 @@ class EncryptedSession(ShardedDriver):
         cur.wait_event(self.rn_ready[slot])
         n = self.n_own
         clamps = 0
-        if n and cfg.variant != "collab":
+        if n and cfg.variant != "collab" and cfg.r_mode == "fresh":
             self.bad |= self.st_pre[slot].ne(0).any().to(torch.int32)
         if n:
             lo = self.own_lo
@@ -541,7 +692,8 @@ class EncryptedSession(ShardedDriver):
                 q = self._quantize_async(vin, spec)
             ct = torch.empty((2 * n, W), dtype=torch.int32, device=self.dev)
             if cfg.variant == "collab":
-                ct = self._collab_encrypt(q, self.rn[slot][:, : self.L].contiguous(), ct)
+                rr = self.rn[slot] if cfg.r_mode == "pooled" else self.rn[slot][:, : self.L].contiguous()
+                ct = self._collab_encrypt(q, rr, ct)
                 self.bad |= self.st_enc.ne(0).any().to(torch.int32)
             else:
                 _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(self.rn[slot]), 2 * n,
@@ -551,23 +703,29 @@ class EncryptedSession(ShardedDriver):
                 self.capture.setdefault("q", []).append(q.clone())
                 self.capture.setdefault("ct", []).append(ct.clone())
         if not n and cfg.variant == "collab":
-            draw_masks(self.mask_rng, 2 * sum(self.sizes))  # keep the shared mask stream in step
+            draw_masks(self.mask_rng, 2 * sum(self.sizes), cfg.mask_bits)  # keep the shared mask stream in step
         self.enc_done.record(cur)
         if t + 1 < cfg.iters:
             self._precompute(1 - slot)
         if n:
             upd = torch.empty((n, W), dtype=torch.int32, device=self.dev)
             sz = self.own_sizes
+            ev = self._wait_begin()
             _raise_for(self.lib.pcb_edge_step_blocks_async(
                 self.edge._ctx, len(sz), sz.ctypes.data, L.ptr(self.alpha_hat), L.ptr(self.expo), self.expo_bits,
                 L.ptr(ct[:n]), L.ptr(ct[n:]), cfg.window, L.ptr(upd), L.ptr(self.err), st), "edge step")
             if cfg.variant == "collab":  # edge: delegated Dec powers; master: decrypt_with_half + update
                 px = self._collab_dec_powers(upd)
+                self._wait_end(ev)
                 _raise_for(self.lib.pcb_decrypt_update_blocks_half(
                     self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(px), L.ptr(self.rowsum),
                     L.ptr(q[:n]), L.ptr(q[n:]), spec[0], spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
                     L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None, st), "master update (collab)")
             else:
+                self._wait_end(ev)
+                if not cfg.use_crt:  # decrypt_vec(use_crt = false): one full each (paillier.cpp:345-350)
+                    self.adj_full += n
+                    self.adj_half -= 2 * n
                 _raise_for(self.lib.pcb_decrypt_update_blocks_async(
                     self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(self.rowsum), L.ptr(q[:n]),
                     L.ptr(q[n:]), spec[0], spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
@@ -646,7 +804,13 @@ class FaithfulDriver:
         import torch
         import torch.distributed as dist
 
+        import time
+
         cfg = self.cfg
+        cfg.validate()
+        if cfg.variant != "basic":
+            raise ValueError("the faithful-trust driver runs the basic variant")
+        m0 = time.perf_counter()
         n = a.shape[1]
         self.sizes = split_columns(n, cfg.nodes)
         self.offs = np.cumsum([0] + self.sizes[:-1]).tolist()
@@ -665,26 +829,39 @@ class FaithfulDriver:
         z = torch.zeros(n, dtype=torch.float64, device=dev)
         v = torch.zeros(n, dtype=torch.float64, device=dev)
         W = B.width
+        B.sync()
+        res.t_pre_s = time.perf_counter() - m0
         for t in range(cfg.iters):
             B.sync()
-            t0 = __import__("time").perf_counter()
+            t0 = time.perf_counter()
             if self.rank == 0:
                 ct, q = B.master_encrypt(z, v, t)
             else:
                 ct, q = torch.empty((2 * n, W), dtype=torch.int32, device=dev), None
+            # the master waits from handing the enc_state frames over to holding every enc_update
+            # (timed_send / timed_recv, protocol.cpp:319-329): broadcast, the edge steps, all-gather
+            B.sync()
+            c0 = time.perf_counter()
             if self.world > 1:
                 dist.broadcast(ct, src=0, group=self.group)
             upd_own = B.edge_step(self.mine, self.sizes, self.offs, ct)
             upd = self._gather_rows(upd_own, n_max, W)
+            B.sync()
+            comm = time.perf_counter() - c0
             if self.rank == 0:
                 B.master_update(upd, q, rowsum, self.sizes, spec, cfg, x, z, v)
                 r = (a @ z) - y
                 res.objective.append(0.5 * float(r @ r) + cfg.lam * float(z.abs().sum()))
                 res.clamps += B.check_iteration(t)
             B.sync()
-            res.iter_seconds.append(__import__("time").perf_counter() - t0)
+            res.iter_seconds.append(time.perf_counter() - t0)
             if record_trace and self.rank == 0:
                 res.x_trace.append(x.clone())
+            res.t_comm_s.append(comm)
+            res.t_loc_s.append(time.perf_counter() - t0 - comm)
+        res.t_master_s = time.perf_counter() - m0
+        if hasattr(B, "role_stats"):
+            B.role_stats(res, self.rank)
         if self.rank == 0:
             res.x, res.z, res.v = (t_.cpu().numpy() for t_ in (x, z, v))
             res.x_trace = [xt.cpu().numpy() for xt in res.x_trace]
@@ -775,6 +952,20 @@ class FaithfulGpuBackend:
         self.st_enc = torch.zeros(2 * n, dtype=torch.int32, device=self.device)
         self.spec = spec
         self.kappa = cfg.lam / cfg.rho
+        self.cfg = cfg
+        self.adj_full = self.adj_half = 0
+        if cfg.r_mode == "pooled":  # protocol.cpp:382-388, as EncryptedSession._build_pool
+            P, st = cfg.pool_size, self._st()
+            pool_r = torch.empty((P, self.L), dtype=torch.int32, device=self.device)
+            s_ = C.c_uint64(self.rng_r.state)
+            _raise_for(self.lib.pcb_sample_r(self.master._ctx, C.byref(s_), P, L.ptr(pool_r), st), "sample_r")
+            self.rng_r.state = s_.value
+            self.pool_rn = torch.empty((P, self.width), dtype=torch.int32, device=self.device)
+            m0 = torch.zeros((P, 1), dtype=torch.int32, device=self.device)
+            _raise_for(self.lib.pcb_encrypt(self.master._ctx, L.ptr(m0), 1, L.ptr(pool_r), P, L.ptr(self.pool_rn), 1,
+                                            None, st), "make_rn_factor")
+            self.adj_full += P  # make_rn_factor's full (paillier.cpp:376)
+            self.pool_at = 0
 
     def master_encrypt(self, z, v, t):
         import torch
@@ -785,14 +976,20 @@ class FaithfulGpuBackend:
         q = torch.empty(vin.numel(), dtype=torch.int64, device=self.device)
         _raise_for(self.lib.pcb_quantize_async(L.ptr(vin), vin.numel(), spec[0], spec[1], spec[2], 0, L.ptr(q),
                                                L.ptr(self.clamps_dev), L.ptr(self.err), st), "quantize")
-        s_ = C.c_uint64(self.rng_r.state)
-        _raise_for(self.lib.pcb_sample_r(self.master._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
-                   "sample_r")
-        self.rng_r.state = s_.value
-        r = self.rall.index_select(0, self.rperm).contiguous()
         ct = torch.empty((vin.numel(), self.width), dtype=torch.int32, device=self.device)
-        _raise_for(self.lib.pcb_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(r), vin.numel(), L.ptr(ct), 1,
-                                        L.ptr(self.st_enc), st), "enc_state")
+        if self.cfg.r_mode == "pooled":  # crt_encrypt_with_factor / encrypt_with_factor (protocol.cpp:411-415)
+            rn = self.pool_rn.index_select(0, torch.remainder(self.rperm + self.pool_at, self.cfg.pool_size))
+            self.pool_at += vin.numel()
+            _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(rn), vin.numel(), L.ptr(ct),
+                                               L.ptr(self.st_enc), st), "enc_state")
+        else:
+            s_ = C.c_uint64(self.rng_r.state)
+            _raise_for(self.lib.pcb_sample_r(self.master._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
+                       "sample_r")
+            self.rng_r.state = s_.value
+            r = self.rall.index_select(0, self.rperm).contiguous()
+            _raise_for(self.lib.pcb_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(r), vin.numel(), L.ptr(ct),
+                                            1 if self.cfg.use_crt else 0, L.ptr(self.st_enc), st), "enc_state")
         return ct, q
 
     def edge_step(self, mine, sizes, offs, ct):
@@ -810,8 +1007,19 @@ class FaithfulGpuBackend:
             self.expo_bits, L.ptr(zc), L.ptr(vc), 6, L.ptr(upd), L.ptr(self.err), self._st()), "edge step")
         return upd
 
+    def role_stats(self, res, rank: int) -> None:
+        """Ledgers as EncryptedSession.role_stats: the master's on rank 0, each rank's edges."""
+        if rank == 0:
+            f, h = self.master.counters()
+            res.master = RoleStats(f + self.adj_full, h + self.adj_half, 0)
+        fe, he = self.edge.counters()
+        res.edges = RoleStats(fe, he, 0)
+
     def master_update(self, upd, q, rowsum, sizes, spec, cfg, x, z, v):
         n = self.n
+        if not cfg.use_crt:  # decrypt_vec(use_crt = false): one full each (paillier.cpp:345-350)
+            self.adj_full += n
+            self.adj_half -= 2 * n
         sz = np.array(sizes, dtype=np.uint32)
         _raise_for(self.lib.pcb_decrypt_update_blocks_async(
             self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(rowsum), L.ptr(q[:n]), L.ptr(q[n:]),

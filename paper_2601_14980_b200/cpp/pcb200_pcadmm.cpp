@@ -541,9 +541,22 @@ Ciphertext Paillier::finish_split_encrypt(const BigNat& m, const BigNat& p2_g_po
 
 Ciphertext Paillier::finish_split_encrypt_with_factor(const BigNat& m, const BigNat& p2_g_power, const RnFactor& f) {
   if (f.half_p2.is_zero() && f.half_q2.is_zero()) throw std::invalid_argument("factor missing split residues");
-  Ciphertext c = finish_split_encrypt(m, p2_g_power, f.r);
-  pow_half_ -= 2;  // the factor's r^n halves are reused (paillier.cpp:416-426)
-  return c;
+  need_private("split encryption needs p and q");
+  if (f.full.is_zero()) {  // a factor carrying only its halves: recompute from r
+    Ciphertext c = finish_split_encrypt(m, p2_g_power, f.r);
+    pow_half_ -= 2;  // the factor's r^n halves are reused (paillier.cpp:416-426)
+    return c;
+  }
+  if (m >= pub_.n) throw std::invalid_argument("plaintext not below n");
+  std::vector<uint32_t> mm = m.to_u32(L_), g = mod(p2_g_power, pub_.n2).to_u32(2 * L_), rn = f.full.to_u32(2 * L_),
+                        c(2 * L_);
+  int32_t st = 0;
+  check(pcb_finish_split_encrypt_rn((pcb_ctx*)ctx_, mm.data(), (uint32_t)L_, g.data(), (uint32_t)(2 * L_), rn.data(), 1,
+                                    c.data(), &st, nullptr),
+        "finish_split_encrypt_with_factor");
+  if (st) throw_status(st, "finish_split_encrypt_with_factor");
+  if (!pub_.binomial_g) pow_half_ += 1;  // the q-side g power (paillier.cpp:424)
+  return Ciphertext{BigNat::from_u32(c.data(), 2 * L_), (u32)m.bit_length()};
 }
 
 BigNat Paillier::decrypt_with_half(const Ciphertext& c, const BigNat& p2_power) {

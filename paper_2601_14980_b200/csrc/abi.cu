@@ -1716,6 +1716,87 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
   return e;
 }
 
+// finish_split_encrypt_with_factor (paillier.cpp:416-426) with the pooled factor's rn = r^n mod n^2
+// (RnFactor.full; its residues mod p^2 / q^2 are the factor's half_p2 / half_q2):
+//   c = CRT(p2_g_power mod p^2, g_q(m) mod q^2) * rn mod n^2,  g_q(m) = 1 + m n (g^m for random g)
+// -- two plain reductions, one Garner recombination and one multiply mod n^2; no exponentiation
+// with r (that is what the pool buys).
+pcb_status pcb_finish_split_encrypt_rn(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* p2_g_power,
+                                       uint32_t pg_limbs, const uint32_t* rn, size_t count, uint32_t* c,
+                                       int32_t* status, pcb_stream stream) {
+  if (!x || (count && (!m || !p2_g_power || !rn || !c)) || pg_limbs == 0 || pg_limbs > 2 * x->L) return PCB_E_SHAPE;
+  if (m_limbs == 0 || m_limbs > x->L) return PCB_E_SHAPE;
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (!x->has_rx) return PCB_E_UNSUPPORTED;
+  if (count == 0) return PCB_OK;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = x->S, L2 = 2 * (int)x->L;
+  Staged sm, sg, sr, sc, ss;
+  uint32_t *gw = nullptr, *u = nullptr, *yp = nullptr, *yq = nullptr, *c1 = nullptr;
+  int32_t* stv = nullptr;
+  pcb_status e = stage_in(m, count * m_limbs * 4, st, &sm);
+  if (!e) e = stage_in(p2_g_power, count * pg_limbs * 4, st, &sg);
+  if (!e) e = stage_in(rn, count * L2 * 4, st, &sr);
+  if (!e) e = stage_out(c, count * L2 * 4, st, &sc);
+  if (!e) e = stage_out(status, status ? count * 4 : 0, st, &ss);
+  stv = (int32_t*)ss.dev;
+  if (!e && !stv) e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = scratch_alloc(count * L2 * 4, (void**)&gw, st);
+  if (!e) e = scratch_alloc(count * L2 * 4, (void**)&u, st);
+  if (!e) e = scratch_alloc(count * L2 * 4, (void**)&c1, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yp, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&yq, st);
+  // m < n, rn in [1, n^2) ("factor missing split residues" for rn = 0); u = 1 + m n
+  if (!e)
+    e = launch_onepmn((const uint32_t*)sm.dev, (int)m_limbs, (const uint32_t*)sr.dev, x->d_n, x->d_n2, (int)x->L, u,
+                      stv, count, st);
+  if (!e && x->random_g) {  // g_power_half(m, false) of a random generator (paillier.cpp:259-267)
+    e = gpow_core(x, (const uint32_t*)sm.dev, m_limbs, count, u, st);
+    if (!e) {
+      zero_bad_rows_kernel<<<(int)std::min<size_t>((count * L2 + 255) / 256, 4096), 256, 0, st>>>(u, L2, stv, count);
+      count_launch();
+      e = cuda_check(cudaGetLastError());
+    }
+  }
+  if (!e) e = cuda_check(cudaMemset2DAsync(gw, L2 * 4, 0, L2 * 4, count, st));
+  if (!e)
+    e = cuda_check(cudaMemcpy2DAsync(gw, L2 * 4, sg.dev, pg_limbs * 4, pg_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
+  const double mm = 2.0 * S * S + S;
+  if (!e) e = launch_rnsx(x->rx_p, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, gw, L2, nullptr, 0, count, yp, st, mm);
+  if (!e) e = launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, u, L2, nullptr, 0, count, yq, st, mm);
+  if (!e && S == 32)
+    e = launch_garner<32>(*reinterpret_cast<const CrtEncConsts<32>*>(x->enc_blob.data()), yp, yq, stv, c1, (int)x->L,
+                          count, st);
+  if (!e && S == 64)
+    e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv, c1, (int)x->L,
+                          count, st);
+  if (!e && S == 96)
+    e = launch_garner<96>(*reinterpret_cast<const CrtEncConsts<96>*>(x->enc_blob.data()), yp, yq, stv, c1, (int)x->L,
+                          count, st);
+  std::vector<WStep> p = prog_hom_add();  // CRT(...) * rn mod n^2; failed rows have c1 = 0 -> c = 0
+  if (!e) e = run_wide(x, p.data(), (int)p.size(), (const uint32_t*)sr.dev, c1, nullptr, 1, count, count,
+                       (uint32_t*)sc.dev, 1, st);
+  if (!e) e = unstage_out(c, &sc, st);
+  if (!e) e = unstage_out(status, &ss, st);
+  if (!e && !status) e = first_failure(stv, count, st);
+  scratch_free(gw, st);
+  scratch_free(u, st);
+  scratch_free(c1, st);
+  scratch_free(yp, st);
+  scratch_free(yq, st);
+  if (!ss.dev) scratch_free(stv, st);
+  const bool any_host = sm.host || sg.host || sr.host || sc.host || ss.host;
+  unstage(&sm, st);
+  unstage(&sg, st);
+  unstage(&sr, st);
+  unstage(&sc, st);
+  unstage(&ss, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  if (!e && x->random_g) x->pow_half += (uint64_t)count;  // g_power_half on the q side (paillier.cpp:424)
+  return e;
+}
+
 pcb_status pcb_hom_add(pcb_ctx* x, const uint32_t* a, const uint32_t* b, size_t count, uint32_t* out,
                        pcb_stream stream) {
   if (!x || (count && (!a || !b || !out))) return PCB_E_SHAPE;

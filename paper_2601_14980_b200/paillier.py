@@ -225,6 +225,20 @@ class Paillier:
                                           self._stream() if dev else None), "encrypt_rn")
         return c
 
+    def finish_split_encrypt_rn_batch(self, m, p2_g_power, rn, status=None):
+        """Paillier::finish_split_encrypt_with_factor (paillier.cpp:416-426) with the factor's
+        rn = r^n mod n^2: c = CRT(p2_g_power mod p^2, (1 + m n) mod q^2) rn mod n^2."""
+        torch = _torch()
+        self._need_prv()
+        count, ml = m.shape
+        dev = m.is_cuda if hasattr(m, "is_cuda") else False
+        c = torch.empty((count, 2 * self.L), dtype=torch.int32, device=m.device) if dev else \
+            np.zeros((count, 2 * self.L), np.uint32)
+        _raise_for(L.lib().pcb_finish_split_encrypt_rn(self._ctx, L.ptr(m), ml, L.ptr(p2_g_power), p2_g_power.shape[1],
+                                                       L.ptr(rn), count, L.ptr(c), L.ptr(status),
+                                                       self._stream() if dev else None), "finish_split_encrypt_rn")
+        return c
+
     def decrypt_batch(self, c, use_crt: bool = True, status=None):
         torch = _torch()
         self._need_prv()

@@ -1,0 +1,42 @@
+"""Host logic of the session surface (CPU): SessionConfig defaults and argument errors
+(protocol.hpp:24-41, protocol.cpp:86-88, 384) and the vectorised mask stream at every width
+against the serial draw_mask (protocol.cpp:86-93)."""
+import pytest
+
+from paper_2601_14980_b200 import admm as ADMM
+from paper_2601_14980_b200.paillier import Rng
+
+
+def test_defaults_follow_the_reference():
+    c = ADMM.SessionConfig()
+    assert (c.nodes, c.iters, c.rho, c.lam, c.seed, c.window) == (3, 100, 1.0, 1.0, 1, 6)
+    assert (c.r_mode, c.pool_size, c.mask_bits, c.use_crt, c.engine) == ("fresh", 16, 64, True, "packed")
+    c.validate()
+
+
+@pytest.mark.parametrize("kw,msg", [({"r_mode": "pooled", "pool_size": 0}, "pool size below 1"),
+                                    ({"mask_bits": 65}, "mask width above 64"),
+                                    ({"engine": "x"}, "unknown engine"),
+                                    ({"variant": "x"}, "unknown protocol variant"),
+                                    ({"r_mode": "x"}, "unknown randomness mode")])
+def test_argument_errors(kw, msg):
+    with pytest.raises(ValueError, match=msg):
+        ADMM.SessionConfig(**kw).validate()
+    ADMM.SessionConfig(r_mode="fresh", pool_size=0).validate()  # the pool size only matters pooled
+
+
+@pytest.mark.parametrize("bits", [64, 63, 32, 16, 8, 3, 1])
+def test_draw_masks_equals_serial_draw_mask(bits):
+    r1, r2 = Rng(0xABCDEF), Rng(0xABCDEF)
+    v = ADMM.draw_masks(r1, 4000, bits)
+    s = [ADMM.draw_mask(r2, bits) for _ in range(4000)]
+    assert [int(x) for x in v] == s and r1.state == r2.state
+    assert all(0 < x < (1 << bits) for x in s)
+
+
+def test_mask_width_zero_draws_nothing():
+    r = Rng(5)
+    assert ADMM.draw_mask(r, 0) == 0 and r.state == 5
+    assert not ADMM.draw_masks(r, 10, 0).any() and r.state == 5
+    with pytest.raises(ValueError, match="mask width above 64"):
+        ADMM.draw_mask(r, 65)
