@@ -133,7 +133,9 @@ def run_admm(args, rank: int, world: int, local: int):
                       "iterations_timed": args.admm_iters, "warmup_iterations": args.admm_warmup,
                       "blocks_per_gpu": 8 // world if 8 % world == 0 else None},
            "iter_seconds": [round(v, 5) for v in res.iter_seconds],
-           "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall}
+           "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall, "node_factors_s": t_fac,
+           "phases": {"t_pre_s": res.t_pre_s, "t_master_s": res.t_master_s,
+                      "t_loc_s": [round(v, 4) for v in res.t_loc_s], "t_comm_s": [round(v, 4) for v in res.t_comm_s]}}
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = admm_cpu_leg(sess, res)
     return out
@@ -246,7 +248,15 @@ def run_cfg5(args, rank: int, world: int, local: int):
     group = dist.group.WORLD if world > 1 else None
     sess = ADMM.EncryptedSession(keys, cfg, device=local, rank=rank, world=world, group=group)
     t0 = time.perf_counter()
-    res = sess.run(a, y, record_trace=True)  # x gathered after each iteration's timed part
+    # the 64 node factors on the device (pcb_node_factors: FP64 Gram + blocked Cholesky +
+    # triangular inverse on DMMA), timed on their own
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fac = ADMM.node_factors(a, y, ADMM.split_columns(65536, 64), cfg.rho, 64)
+    e1.record()
+    torch.cuda.synchronize()
+    t_fac = e0.elapsed_time(e1) / 1e3
+    res = sess.run(a, y, factors=fac, record_trace=True)  # x gathered after each iteration's timed part
     wall = time.perf_counter() - t0
     it = res.iter_seconds[args.admm_warmup:args.admm_warmup + args.cfg5_iters]
     t = torch.tensor([float(np.mean(it))], device="cuda")

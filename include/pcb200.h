@@ -166,6 +166,20 @@ pcb_status pcb_finish_split_encrypt_rn(pcb_ctx* ctx, const uint32_t* m, uint32_t
                                        uint32_t pg_limbs, const uint32_t* rn, size_t count, uint32_t* c,
                                        int32_t* status, pcb_stream stream);
 
+/* ---- edge setup: node factors ---------------------------------------- */
+
+/* pcadmm::node_factor (admm.cpp:63-75) for every block of a column split at once:
+ * normal_k = A_k^T A_k + rho I,  b_bar_k = rho normal_k^-1,  alpha_k = normal_k^-1 A_k^T y_s,
+ * y_s = y / k_total when over_k (YScaling::over_k) else y.  a: rows x cols FP64 row-major with row
+ * stride lda; block k = the sizes[k] consecutive columns after blocks 0..k-1 (sum sizes = cols).
+ * b_bar: the blocks' sizes[k]^2 row-major matrices back to back; alpha: cols.  FP64 blocked
+ * Cholesky + triangular inverse on DMMA (csrc/factor.cu); equal to the reference's LDLT solve to
+ * rounding.  Errors (check_inputs, admm.cpp:8-16): empty shapes, rho <= 0, k_total < 1, sizes not
+ * summing to cols -> PCB_E_SHAPE; a non-finite input (normal not positive definite) -> PCB_E_SHAPE. */
+pcb_status pcb_node_factors(const double* a, size_t rows, size_t cols, size_t lda, const double* y, size_t nblocks,
+                            const uint32_t* sizes, double rho, uint32_t k_total, int over_k, double* b_bar,
+                            double* alpha, pcb_stream stream);
+
 /* ---- homomorphic operations (public key suffices) ----------------------------------------- */
 
 /* out_i = a_i * b_i mod n^2 — Paillier::hom_add (paillier.cpp:428-432).  plain_bits tracking

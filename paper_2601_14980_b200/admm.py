@@ -157,16 +157,35 @@ def split_columns(cols: int, k: int) -> list[int]:
     return sizes
 
 
-def node_factor(a_k, y, rho: float, k_total: int, over_k: bool = False):
-    """admm.cpp:63-75 in FP64 on the GPU: B = rho (A^T A + rho I)^-1, alpha = (A^T A + rho I)^-1 A^T y."""
+def node_factors(a, y, sizes, rho: float, k_total: int, over_k: bool = False):
+    """node_factor (admm.cpp:63-75) of every block of the column split at once, on the device
+    (pcb_node_factors: FP64 Gram, blocked Cholesky, triangular inverse on DMMA, csrc/factor.cu):
+    [(B_k = rho (A_k^T A_k + rho I)^-1, alpha_k = (A_k^T A_k + rho I)^-1 A_k^T y_s)], y_s = y / K
+    under over_k.  a: (rows, cols) FP64 CUDA tensor, blocks = consecutive column ranges."""
     import torch
 
-    n = a_k.shape[1]
-    normal = a_k.T @ a_k + rho * torch.eye(n, dtype=torch.float64, device=a_k.device)
-    y_s = y / float(k_total) if over_k else y
-    b_bar = rho * torch.linalg.solve(normal, torch.eye(n, dtype=torch.float64, device=a_k.device))
-    alpha = torch.linalg.solve(normal, a_k.T @ y_s)
-    return b_bar, alpha
+    a = a.contiguous() if a.stride(1) != 1 else a
+    y = y.contiguous()
+    rows, cols = a.shape
+    sz = np.asarray(sizes, dtype=np.uint32)
+    b = torch.empty(int((sz.astype(np.uint64) ** 2).sum()), dtype=torch.float64, device=a.device)
+    al = torch.empty(cols, dtype=torch.float64, device=a.device)
+    st = C.c_void_p(torch.cuda.current_stream(a.device).cuda_stream)
+    # a column window of a wider row-major matrix is fine: rows keep unit stride, lda = stride(0)
+    _raise_for(L.lib().pcb_node_factors(C.c_void_p(a.data_ptr()), rows, cols, a.stride(0), L.ptr(y), len(sz), sz.ctypes.data,
+                                        float(rho), int(k_total), 1 if over_k else 0, L.ptr(b), L.ptr(al), st),
+               "node_factors")
+    out, mo, co = [], 0, 0
+    for c in sz.tolist():
+        out.append((b[mo:mo + c * c].view(c, c), al[co:co + c]))
+        mo += c * c
+        co += c
+    return out
+
+
+def node_factor(a_k, y, rho: float, k_total: int, over_k: bool = False):
+    """admm.cpp:63-75 for one block: B = rho (A^T A + rho I)^-1, alpha = (A^T A + rho I)^-1 A^T y_s."""
+    return node_factors(a_k, y, [a_k.shape[1]], rho, k_total, over_k)[0]
 
 
 def session_bounds(factors, sizes, rho, lam, iters, margin, delta):
@@ -420,7 +439,7 @@ class EncryptedSession(ShardedDriver):
         sizes = split_columns(a.shape[1], cfg.nodes)
         offs = np.cumsum([0] + sizes[:-1]).tolist()
         if factors is None:
-            factors = [node_factor(a[:, o:o + c], y, cfg.rho, cfg.nodes, cfg.over_k) for o, c in zip(offs, sizes)]
+            factors = node_factors(a, y, sizes, cfg.rho, cfg.nodes, cfg.over_k)
         else:
             factors = [(torch.as_tensor(b, dtype=torch.float64, device=dev),
                         torch.as_tensor(al, dtype=torch.float64, device=dev)) for b, al in factors]

@@ -41,6 +41,7 @@ SOURCES = [
     "rns.cu",
     "rnsx.cu",
     "wire.cu",
+    "factor.cu",
     "host/hbn.cpp",
 ]
 
