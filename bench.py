@@ -133,7 +133,7 @@ def run_admm(args, rank: int, world: int, local: int):
                       "iterations_timed": args.admm_iters, "warmup_iterations": args.admm_warmup,
                       "blocks_per_gpu": 8 // world if 8 % world == 0 else None},
            "iter_seconds": [round(v, 5) for v in res.iter_seconds],
-           "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall, "node_factors_s": t_fac,
+           "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall,
            "phases": {"t_pre_s": res.t_pre_s, "t_master_s": res.t_master_s,
                       "t_loc_s": [round(v, 4) for v in res.t_loc_s], "t_comm_s": [round(v, 4) for v in res.t_comm_s]}}
     if rank == 0 and not args.no_cpu_baseline:
@@ -267,7 +267,9 @@ def run_cfg5(args, rank: int, world: int, local: int):
            "config": {"workload": "cfg5 LASSO N=65536 (10% support), M=10000, K=64 blocks of 1024, 2048-bit key",
                       "iterations_timed": args.cfg5_iters, "blocks_per_gpu": 64 // world if 64 % world == 0 else None,
                       "data": "synthetic Gaussian A generated on the GPU"},
-           "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall}
+           "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall, "node_factors_s": t_fac,
+           "phases": {"t_pre_s": res.t_pre_s, "t_master_s": res.t_master_s,
+                      "t_loc_s": [round(v, 4) for v in res.t_loc_s], "t_comm_s": [round(v, 4) for v in res.t_comm_s]}}
     if rank == 0 and not args.no_cpu_baseline:
         # parity gate: the first iteration against the reference's integer shadow pipeline run
         # through the compiled reference, on the session's node factors and QuantSpec

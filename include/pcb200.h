@@ -58,6 +58,16 @@ pcb_status pcb_keygen(uint64_t* rng_state, uint32_t key_bits, uint32_t* n, uint3
  * keypair_from_primes).  out gets ceil(bits/32) limbs. */
 pcb_status pcb_random_prime(uint64_t* rng_state, uint32_t bits, uint32_t* out);
 
+/* The same two calls with the Miller-Rabin rounds batched (csrc/prime.cu, host/hbn.cpp
+ * random_prime_batched): the rounds of many candidates run at once, speculating that every
+ * trial-division survivor fails its first round, then committing / rewinding the stream exactly
+ * as the reference consumes it -- identical primes, keys and *rng_state.  device >= 0 evaluates
+ * the batches on that CUDA device (bits <= 2048 per prime); device < 0 evaluates them with the
+ * host pow_mod (the checker the CPU tests pin the speculation with). */
+pcb_status pcb_keygen_speculative(uint64_t* rng_state, uint32_t key_bits, int device, uint32_t* n, uint32_t* p,
+                                  uint32_t* q);
+pcb_status pcb_random_prime_speculative(uint64_t* rng_state, uint32_t bits, int device, uint32_t* out);
+
 /* ---- context ------------------------------------------------------------------------------ */
 
 /* Builds the per-key device constants (Montgomery contexts for p^2, q^2, p, q, n^2, exponent

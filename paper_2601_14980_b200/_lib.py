@@ -52,6 +52,8 @@ _vp = C.c_void_p
 SIGNATURES = {
     "pcb_keygen": (C.c_int, [_u64p, C.c_uint32, _u32p, _u32p, _u32p]),
     "pcb_random_prime": (C.c_int, [_u64p, C.c_uint32, _u32p]),
+    "pcb_keygen_speculative": (C.c_int, [_u64p, C.c_uint32, C.c_int, _u32p, _u32p, _u32p]),
+    "pcb_random_prime_speculative": (C.c_int, [_u64p, C.c_uint32, C.c_int, _u32p]),
     "pcb_ctx_create": (C.c_int, [C.POINTER(_vp), C.c_int, _u32p, C.c_uint32, _u32p, _u32p, C.c_uint32]),
     "pcb_ctx_destroy": (None, [_vp]),
     "pcb_ctx_set_generator": (C.c_int, [_vp, _vp, C.c_uint32]),

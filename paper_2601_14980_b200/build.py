@@ -42,6 +42,7 @@ SOURCES = [
     "rnsx.cu",
     "wire.cu",
     "factor.cu",
+    "prime.cu",
     "host/hbn.cpp",
 ]
 

@@ -457,6 +457,139 @@ HBN random_prime(HRng& rng, size_t bits, int mr_rounds) {
   }
 }
 
+namespace {
+// trial division exactly as is_probable_prime's prefix (bignat.cpp:471-473) for n > 6 bits:
+// false = composite (n is never one of the small primes at these widths)
+bool survives_trial_division(const HBN& n) {
+  for (uint32_t p : kSmallPrimes)
+    if (mod_small(n, p) == 0) return n == HBN(p);
+  return true;
+}
+// the witness loop of one round given x = a^d mod n (bignat.cpp:483-493): true = n passes
+bool round_passes(HBN x, const HBN& n, size_t s) {
+  const HBN nm1 = n - HBN(1);
+  if (x == HBN(1) || x == nm1) return true;
+  for (size_t i = 0; i + 1 < s; i++) {
+    x = mod(x * x, n);
+    if (x == nm1) return true;
+  }
+  return false;
+}
+struct Spec {
+  size_t march, step;  // which candidate
+  HBN n, d;
+  size_t s;
+  HRng after;  // stream state right after this survivor's first base draw
+};
+}  // namespace
+
+bool random_prime_batched(HRng& rng, size_t bits, int mr_rounds, int lookahead, MrPow pow, void* user, HBN& out) {
+  if (bits < 2) throw std::domain_error("random_prime: need >= 2 bits");
+  if (bits <= 64 || mr_rounds <= 0) {  // tiny widths / no rounds: nothing worth batching
+    out = random_prime(rng, bits, mr_rounds);
+    return true;
+  }
+  const HBN three(3), two(2);
+  // a march = the candidates of one random_bits draw (random_prime's inner loop)
+  auto march_of = [&](HRng& r) {
+    HBN cand = random_bits(r, bits);
+    std::vector<uint32_t> l = cand.limbs((bits + 63) / 64 * 2);
+    l[(bits - 1) / 32] |= 1u << ((bits - 1) % 32);
+    l[0] |= 1u;
+    cand = HBN::from_limbs(l.data(), l.size());
+    std::vector<HBN> cs;
+    for (int step = 0; step < 64; step++) {
+      cs.push_back(cand);
+      cand = cand + HBN(2);
+      if (cand.bit_length() != bits) break;
+    }
+    return cs;
+  };
+  std::vector<HBN> pending;  // the committed march still being examined
+  size_t pending_from = 0;
+  for (;;) {
+    HRng r = rng;
+    std::vector<std::vector<HBN>> marches;
+    std::vector<Spec> sp;
+    MrBatch b1;
+    auto emit = [&](size_t m, size_t from) {
+      for (size_t j = from; j < marches[m].size(); j++) {
+        const HBN& n = marches[m][j];
+        if (!survives_trial_division(n)) continue;
+        Spec x{m, j, n, n - HBN(1), 0, r};
+        while (!x.d.is_odd()) {
+          x.d = x.d >> 1;
+          x.s++;
+        }
+        b1.a.push_back(random_below(r, n - three) + two);
+        b1.n.push_back(n);
+        b1.d.push_back(x.d);
+        x.after = r;
+        sp.push_back(std::move(x));
+      }
+    };
+    if (!pending.empty()) {
+      marches.push_back(pending);
+      emit(0, pending_from);
+    }
+    for (int m = 0; m < lookahead; m++) {
+      marches.push_back(march_of(r));
+      emit(marches.size() - 1, 0);
+    }
+    std::vector<HBN> x1;
+    if (!b1.n.empty() && !pow(b1, x1, user)) return false;
+    size_t k = 0;
+    while (k < sp.size() && !round_passes(x1[k], sp[k].n, sp[k].s)) k++;
+    if (k == sp.size()) {  // every survivor fails its first round: all of it is committed
+      rng = r;
+      pending.clear();
+      continue;
+    }
+    // committed up to survivor k's first base draw; rounds 2.. of its candidate in one batch
+    rng = sp[k].after;
+    HRng r2 = rng;
+    MrBatch b2;
+    std::vector<HRng> snap;
+    for (int t = 1; t < mr_rounds; t++) {
+      b2.a.push_back(random_below(r2, sp[k].n - three) + two);
+      b2.n.push_back(sp[k].n);
+      b2.d.push_back(sp[k].d);
+      snap.push_back(r2);
+    }
+    std::vector<HBN> x2;
+    if (!b2.n.empty() && !pow(b2, x2, user)) return false;
+    size_t t = 0;
+    while (t < b2.n.size() && round_passes(x2[t], sp[k].n, sp[k].s)) t++;
+    if (t == b2.n.size()) {
+      if (!snap.empty()) rng = snap.back();
+      out = sp[k].n;
+      return true;
+    }
+    rng = snap[t];  // composite at round t + 2: continue its march after it
+    pending = marches[sp[k].march];
+    pending_from = sp[k].step + 1;
+  }
+}
+
+bool keygen_batched(HRng& rng, size_t key_bits, MrPow pow, void* user, HBN& p, HBN& q) {
+  if (key_bits != 64 && key_bits != 1024 && key_bits != 2048 && key_bits != 4096) return false;
+  size_t half = key_bits / 2;
+  for (int attempt = 0; attempt < 64; attempt++) {  // keygen's loop, paillier.cpp:110-121
+    HBN pp, qq;
+    if (!random_prime_batched(rng, half, 40, 16, pow, user, pp)) return false;
+    if (!random_prime_batched(rng, half, 40, 16, pow, user, qq)) return false;
+    if (pp == qq) continue;
+    HBN diff = pp > qq ? pp - qq : qq - pp;
+    if (diff.bit_length() < half - 7) continue;
+    if ((pp * qq).bit_length() != key_bits) continue;
+    (void)rng.next();  // finish_keys' g_seed draw (paillier.cpp:120)
+    p = pp;
+    q = qq;
+    return true;
+  }
+  throw std::runtime_error("key generation attempt budget exhausted");
+}
+
 bool keygen(HRng& rng, size_t key_bits, HBN& p, HBN& q) {
   if (key_bits != 64 && key_bits != 1024 && key_bits != 2048 && key_bits != 4096) return false;
   size_t half = key_bits / 2;

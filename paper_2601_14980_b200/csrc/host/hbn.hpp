@@ -70,6 +70,21 @@ HBN random_below(HRng& rng, const HBN& bound);      // bignat.cpp:438-445
 bool is_probable_prime(const HBN& n, HRng& rng, int rounds = 40);  // bignat.cpp:458-495
 HBN random_prime(HRng& rng, size_t bits, int mr_rounds = 40);     // bignat.cpp:497-515
 
+// Batched Miller-Rabin: x_i = a_i ^ d_i mod n_i for a batch of (odd) moduli -- the device
+// evaluates it (prime.cu); the CPU tests plug pow_mod in.
+struct MrBatch {
+  std::vector<HBN> n, d, a;
+};
+using MrPow = bool (*)(const MrBatch& b, std::vector<HBN>& x, void* user);
+// random_prime with the Miller-Rabin rounds evaluated in batches, consuming the rng EXACTLY like
+// random_prime (so the primes, and the rng state after, are the reference's).  Speculation: every
+// trial-division survivor of the next `lookahead` marches is assumed to fail its first round (the
+// base draws are then fixed by the stream), all first rounds run as one batch, and the prefix up
+// to the first survivor that passes is committed; its remaining rounds run as a second batch,
+// rewinding the stream to the first failing round if it turns out composite.  Returns false if
+// `pow` fails.
+bool random_prime_batched(HRng& rng, size_t bits, int mr_rounds, int lookahead, MrPow pow, void* user, HBN& out);
+bool keygen_batched(HRng& rng, size_t key_bits, MrPow pow, void* user, HBN& p, HBN& q);
 // keygen restated (paillier.cpp:106-123, binomial g): returns false on an unsupported size.
 // Consumes the rng exactly like the reference (including finish_keys' g_seed draw).
 bool keygen(HRng& rng, size_t key_bits, HBN& p, HBN& q);

@@ -84,25 +84,35 @@ class Ciphertext:
     plain_bits: int = 0
 
 
-def keygen(rng: Rng, key_bits: int) -> KeyPair:
-    """pcadmm::keygen(rng, key_bits, GMode::binomial); advances rng exactly like the reference."""
+def keygen(rng: Rng, key_bits: int, device: int | None = None) -> KeyPair:
+    """pcadmm::keygen(rng, key_bits, GMode::binomial); advances rng exactly like the reference.
+    device: run the Miller-Rabin rounds in batches on that CUDA device (pcb_keygen_speculative,
+    same key and rng state); None: the host search (pcb_keygen)."""
     nl = (key_bits + 31) // 32
     hl = (key_bits // 2 + 31) // 32
     st = C.c_uint64(rng.state)
     n = np.zeros(nl, np.uint32)
     p = np.zeros(hl, np.uint32)
     q = np.zeros(hl, np.uint32)
-    _raise_for(L.lib().pcb_keygen(C.byref(st), key_bits, n.ctypes.data_as(L._u32p), p.ctypes.data_as(L._u32p),
-                                  q.ctypes.data_as(L._u32p)), "keygen")
+    if device is not None:
+        _raise_for(L.lib().pcb_keygen_speculative(C.byref(st), key_bits, int(device), n.ctypes.data_as(L._u32p),
+                                                  p.ctypes.data_as(L._u32p), q.ctypes.data_as(L._u32p)), "keygen")
+    else:
+        _raise_for(L.lib().pcb_keygen(C.byref(st), key_bits, n.ctypes.data_as(L._u32p), p.ctypes.data_as(L._u32p),
+                                      q.ctypes.data_as(L._u32p)), "keygen")
     rng.state = st.value
     return KeyPair(L.limbs_to_int(n), L.limbs_to_int(p), L.limbs_to_int(q), key_bits)
 
 
-def random_prime(rng: Rng, bits: int) -> int:
-    """pcadmm::random_prime(rng, bits, 40) (bignat.cpp:497-515)."""
+def random_prime(rng: Rng, bits: int, device: int | None = None) -> int:
+    """pcadmm::random_prime(rng, bits, 40) (bignat.cpp:497-515); device as keygen."""
     st = C.c_uint64(rng.state)
     out = np.zeros((bits + 31) // 32, np.uint32)
-    _raise_for(L.lib().pcb_random_prime(C.byref(st), bits, out.ctypes.data_as(L._u32p)), "random_prime")
+    if device is not None:
+        _raise_for(L.lib().pcb_random_prime_speculative(C.byref(st), bits, int(device), out.ctypes.data_as(L._u32p)),
+                   "random_prime")
+    else:
+        _raise_for(L.lib().pcb_random_prime(C.byref(st), bits, out.ctypes.data_as(L._u32p)), "random_prime")
     rng.state = st.value
     return L.limbs_to_int(out)
 
