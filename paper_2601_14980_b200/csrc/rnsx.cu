@@ -157,6 +157,7 @@ struct XArgs {
   int dbg;  // timing experiments: 1 = tensor/stream only, 2 = CUDA cores only
   int cl;   // CTAs per cluster sharing the W stream (1 or 2)
   int nprod;  // W-stream producer warps (PCB_RNSX_NPROD for A/B; default kRxProducers)
+  int qbar;   // 1: the GEMM-1 epilogue's beta sum syncs the 4 warps of a lane quadrant, not all 16
   RxProg prog;  // kRxProg
 };
 
@@ -209,6 +210,7 @@ struct Thr {
   uint32_t rank;  // CTA rank in the pair (cta_group::2): rank 1 signals the leader's barriers
   float cthr;     // sum over this thread's primes of 2^23 (2^8 / m'): the bias of the beta terms
   uint64_t *dfull, *dfree, *a1, *a2;
+  uint32_t bar_id, bar_n;  // named barrier of the beta partial sums (quadrant or CTA-wide)
 };
 
 // hand-off arrive (A tile ready / TMEM buffer drained): the MMA issuer's barrier is local, or the
@@ -345,7 +347,7 @@ __device__ __forceinline__ void rx_e1(uint32_t (&XQ)[C::RPT], Thr<C>& T, uint8_t
   }
   sS[T.g * C::TILE + T.e] = __fsub_rn(sp, T.cthr);
   umma::fence_async_smem();
-  umma::named_sync(1, C::NCT);
+  umma::named_sync(T.bar_id, T.bar_n);
   if (T.g == 0) {
     const float S = sS[T.e] + sS[C::TILE + T.e] + sS[2 * C::TILE + T.e] + sS[3 * C::TILE + T.e];
     const uint32_t beta = (uint32_t)floorf(S + 0.00390625f);  // + 2^-8 (see above)
@@ -1158,6 +1160,11 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     T.dbi = 0;
     T.dph = 0;
     T.nowait = P.dbg == 2;
+    // beta of element e sums the partials of the 4 prime groups, i.e. of the 4 warps that share
+    // e's TMEM lane quadrant: a 128-thread named barrier per quadrant (ids 2..5) lets the
+    // quadrants run apart instead of all 16 compute warps meeting every product
+    T.bar_id = P.qbar ? 2u + (uint32_t)qd : 1u;
+    T.bar_n = P.qbar ? 128u : (uint32_t)C::NCT;
     if constexpr (C::CG == 2) T.rank = umma::cluster_ctarank();
     else T.rank = 0;
     T.dfull = bars + 2 * C::NSTAGE;
@@ -1294,6 +1301,8 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
     P.dbg = d ? atoi(d) : 0;
     const char* np = getenv("PCB_RNSX_NPROD");
     P.nprod = np ? atoi(np) : 0;
+    const char* qb = getenv("PCB_RNSX_QBAR");
+    P.qbar = qb ? atoi(qb) : 1;
   }
   int dev = 0, nsm = 0;
   cudaGetDevice(&dev);
