@@ -511,7 +511,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1 << 20)
+    ap.add_argument("--n", "--values", dest="n", type=int, default=1 << 20)
     ap.add_argument("--e2e-steps", type=int, default=2, help="timed end-to-end steps (>= 1)")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -534,9 +534,17 @@ def main() -> None:
     import torch
     import torch.distributed as dist
 
+    # PCB_BENCH_BACKEND=gloo + PCB_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo (a one-GPU
+    # rehearsal of the N-rank code path; its timings mean nothing)
+    if os.environ.get("PCB_BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("PCB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     from paper_2601_14980_b200 import _lib as L
     from paper_2601_14980_b200 import paillier as P
 
