@@ -716,7 +716,8 @@ def main() -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-            "config": {"workload": "cfg2: Paillier-2048 fused Gamma2-quantize+CRT-Enc then CRT-Dec of 2^20 values",
+            "config": {"workload": "cfg2: Paillier-2048 fused Gamma2-quantize+CRT-Enc then CRT-Dec of "
+                                   + ("2^20 values" if N == 1 << 20 else f"{N} values (a reduced run)") + " per GPU",
                        "values_per_gpu": N, "key_bits": 2048,
                        "parallelism": f"dp{world} (rank k: slice k of one job-wide value and sample_r stream)",
                        "l2": "inputs+outputs 0.8 GB/step > 126 MB L2 (no flush needed)",
