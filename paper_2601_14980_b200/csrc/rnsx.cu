@@ -41,6 +41,9 @@
 #ifndef PCB_RNSX_ROLE_WARPS
 #define PCB_RNSX_ROLE_WARPS 4
 #endif
+#ifndef PCB_RNSX_KCONS
+#define PCB_RNSX_KCONS 0  // 1: per-prime constants from the kernel parameters (measured: LDC hoisting spills, slower)
+#endif
 #ifndef PCB_RNSX_SLOT
 #define PCB_RNSX_SLOT 0  // 0: a third of the shared memory left for the ring (Cfg::SLOT)
 #endif
@@ -159,6 +162,12 @@ struct XArgs {
   int nprod;  // W-stream producer warps (PCB_RNSX_NPROD for A/B; default kRxProducers)
   int qbar;   // 1: the GEMM-1 epilogue's beta sum syncs the 4 warps of a lane quadrant, not all 16
   RxProg prog;  // kRxProg
+#if PCB_RNSX_KCONS
+  // the per-prime constant records in the kernel parameters: every lane of a warp reads the same
+  // record (one prime group per warp), so they come from the constant cache as broadcasts and
+  // keep the shared-memory pipe to the tensor core, the W stream and the A tiles
+  uint4 kcons[144 * 3];
+#endif
 };
 
 __device__ __forceinline__ uint32_t redc(uint64_t T, uint32_t m, uint32_t minv) {
@@ -943,11 +952,16 @@ __device__ __noinline__ void producer_role(const uint8_t* wimg0, size_t wstride,
   }
 }
 
-// DBG: 0 normal, 1 no compute handshakes (tensor + stream only), 3 stream only, 4 MMAs only
+// DBG: 0 normal, 1 no compute handshakes (tensor + stream only), 3 stream only, 4 MMAs only;
+// mma_fast: 5 = production tensor + stream path alone, 6 = it and the compute warps side by side
+// without hand-offs (the interference of the two paths, no dependency waits); 7 / 8 = the compute
+// warps beside the stream alone / the MMAs alone (single-slice debug loop)
 // Production MMA issue loop: the product's structure (GEMM -> chunk -> k-step) is the loop
 // structure, so the per-MMA work is one full-barrier wait, the descriptor adds, the MMA and the
 // slot release (one 8 KB slice per ring stage).
-template <class C>
+// WAIT = false (PCB_RNSX_DBG=5): the same loop without the compute hand-offs, to time the tensor +
+// stream path on its own
+template <class C, bool WAIT = true>
 __device__ __noinline__ void mma_fast(uint8_t* sm, uint32_t tm, uint64_t* bars, uint32_t nprod, int cl) {
   uint64_t* full = bars;
   uint64_t* empty = bars + C::NSTAGE;
@@ -966,8 +980,10 @@ __device__ __noinline__ void mma_fast(uint8_t* sm, uint32_t tm, uint64_t* bars, 
 #pragma unroll 1
     for (int seg = 0; seg < 2 * C::NT; seg++) {
       const int gm = seg / C::NT, tt = seg % C::NT;
-      umma::mbar_wait(abar + 2 * tt + gm, pr & 1);
-      umma::tmem_fence_after();
+      if (WAIT) {
+        umma::mbar_wait(abar + 2 * tt + gm, pr & 1);
+        umma::tmem_fence_after();
+      }
       const uint32_t alo = (gm ? a2lo : a1lo) + tt * ABLK16;
       const int ks = gm ? C::KS2 : C::KS1;
 #pragma unroll
@@ -977,7 +993,7 @@ __device__ __noinline__ void mma_fast(uint8_t* sm, uint32_t tm, uint64_t* bars, 
         const uint32_t ncol = (uint32_t)C::ncol(c);
         const uint32_t idesc = umma::idesc_i8(C::TILE, (int)ncol);
         const int sp = C::spc(c);  // slices per ring stage (one bulk copy)
-        if (dcnt >= (uint32_t)C::NB) {
+        if (WAIT && dcnt >= (uint32_t)C::NB) {
           umma::mbar_wait(dfree + dbi, dph ^ 1);
           umma::tmem_fence_after();
         }
@@ -1006,6 +1022,7 @@ __device__ __noinline__ void mma_fast(uint8_t* sm, uint32_t tm, uint64_t* bars, 
       }
     }
   }
+  if (!WAIT && nprod) umma::mbar_wait(dfull + (dbi + C::NB - 1) % C::NB, (dbi == 0) ? dph ^ 1 : dph);
 }
 
 template <class C, int DBG>
@@ -1132,15 +1149,16 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
       }
     } else if (warp == C::NCW) {
       if (P.dbg == 0) mma_fast<C>(sm, tm, bars, np, P.cl);
+      else if (P.dbg == 5 || P.dbg == 6) mma_fast<C, false>(sm, tm, bars, np, P.cl);
       else if (P.dbg == 1) mma_role<C, 1>(sm, tm, bars, np, P.cl);
-      else if (P.dbg == 3) mma_role<C, 3>(sm, tm, bars, np, P.cl);
-      else if (P.dbg == 4) mma_role<C, 4>(sm, tm, bars, np, P.cl);
+      else if (P.dbg == 3 || P.dbg == 7) mma_role<C, 3>(sm, tm, bars, np, P.cl);
+      else if (P.dbg == 4 || P.dbg == 8) mma_role<C, 4>(sm, tm, bars, np, P.cl);
     }
-    if (warp >= C::NCW + 1 && warp <= C::NCW + kRxProducers && P.dbg != 2 && P.dbg != 4) {
+    if (warp >= C::NCW + 1 && warp <= C::NCW + kRxProducers && P.dbg != 2 && P.dbg != 4 && P.dbg != 8) {
       const int npw = P.nprod > 0 && P.nprod <= kRxProducers ? P.nprod : kRxProducers;
       if (warp - C::NCW - 1 < npw)
         producer_role<C>(C::CG == 2 ? P.wimg2 : P.wimg, P.wimg_stride, sm, bars, np, lane, P.cl, rank,
-                         warp - C::NCW - 1, npw, P.dbg == 0 && C::CG == 1);
+                         warp - C::NCW - 1, npw, (P.dbg == 0 || P.dbg == 5 || P.dbg == 6) && C::CG == 1);
     }
     __syncwarp();
   } else {
@@ -1152,14 +1170,18 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     T.lane = lane;
     T.e = qd * 32 + lane;
     T.tl = tm + ((uint32_t)(qd * 32) << 16);
+#if PCB_RNSX_KCONS
+    T.rc = P.kcons + T.g * C::RPT * 3;
+#else
     T.rc = reinterpret_cast<const uint4*>(sm + C::OFF_CONS) + T.g * C::RPT * 3;
+#endif
     T.cthr = 0.0f;
     for (int w = 0; w < C::RPT; w++) T.cthr = __fmaf_rn(8388608.0f, __uint_as_float(T.rc[w * 3 + 2].y), T.cthr);
     T.NT = gridDim.x * C::NCT;
     T.gt = blockIdx.x * C::NCT + tid;
     T.dbi = 0;
     T.dph = 0;
-    T.nowait = P.dbg == 2;
+    T.nowait = P.dbg == 2 || P.dbg >= 6;
     // beta of element e sums the partials of the 4 prime groups, i.e. of the 4 warps that share
     // e's TMEM lane quadrant: a 128-thread named barrier per quadrant (ids 2..5) lets the
     // quadrants run apart instead of all 16 compute warps meeting every product
@@ -1171,7 +1193,7 @@ __global__ void __launch_bounds__(C::NTHR, 1) rnsx_kernel(const __grid_constant_
     T.dfree = T.dfull + C::NB;
     T.a1 = T.dfree + C::NB;
     T.a2 = T.a1 + 1;
-    if (P.dbg == 0 || P.dbg == 2) compute_role<C>(P, T, mine, nsteps, npre, s_x2, s_tab, s_main, s_fin);
+    if (P.dbg == 0 || P.dbg == 2 || P.dbg >= 6) compute_role<C>(P, T, mine, nsteps, npre, s_x2, s_tab, s_main, s_fin);
   }
   umma::tmem_fence_before();
   __syncthreads();
@@ -1284,6 +1306,10 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
   P.wimg2 = md.d_wimg2;
   P.wimg_stride = md.wimg_stride;
   P.cons = md.d_cons;
+#if PCB_RNSX_KCONS
+  if (md.h_cons.size() > sizeof(P.kcons) / 4) return PCB_E_SHAPE;
+  memcpy(P.kcons, md.h_cons.data(), md.h_cons.size() * 4);
+#endif
   P.cvec = reinterpret_cast<const uint32_t*>(md.d_cvec);
   P.slt = md.d_slt;
   P.ops = ops;
@@ -1662,6 +1688,7 @@ bool rnsx_build(const HBN& N, const HBN& n, int S, int K, RnsXModulus* out) {
     ok = ok && cudaMemcpy(md.d_wimg + r * md.wimg_stride, img.data(), img.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
          cudaMemcpy(md.d_wimg2 + r * md.wimg_stride, img2.data(), img2.size(), cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(md.d_cons, cons.data(), cons.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
+  md.h_cons = cons;
   ok = ok && cudaMemcpy(md.d_cvec, cvec.data(), cvec.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(md.d_out, otab.data(), otab.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;
   ok = ok && cudaMemcpy(md.d_slt, slt.data(), slt.size() * 4, cudaMemcpyHostToDevice) == cudaSuccess;

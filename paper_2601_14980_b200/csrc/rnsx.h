@@ -60,6 +60,7 @@ struct RnsXModulus {
   uint8_t* d_wimg2 = nullptr; // the same stream with every slice split in two row halves (cta_group::2)
   size_t wimg_stride = 0;
   uint4* d_cons = nullptr;    // per (g, w): {m, minv, c1, q64}, {m', minv', c2, c3}, {c4, invp, q64'}
+  std::vector<uint32_t> h_cons;  // host copy (kernel-parameter constants, PCB_RNSX_KCONS)
   uint4* d_cvec = nullptr;    // constant operands in thread order: [id][g][NV][4]
   uint32_t* d_slt = nullptr;  // per slice of a product: {image offset / 16, bytes}
   uint32_t* d_out = nullptr;  // output conversion: mod'[K] minv'[K] c4[K] invp[2K] M'/m'_j[K][mpw] M'[mpw] N[S]
