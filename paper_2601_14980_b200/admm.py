@@ -189,30 +189,33 @@ def node_factor(a_k, y, rho: float, k_total: int, over_k: bool = False):
 
 
 def session_bounds(factors, sizes, rho, lam, iters, margin, delta):
-    """protocol.cpp:29-70 (plaintext rehearsal of the block recurrence) + widen_bounds."""
+    """protocol.cpp:29-70 (plaintext rehearsal of the block recurrence) + widen_bounds, on the
+    device: the blocks of an iteration are independent, so they advance together as one batched
+    matvec over the zero-padded stack of node factors (padding rows stay 0, and 0 is already in
+    the running bounds), with the running min / max kept on the device -- one read-back at the end."""
     import torch
 
-    lo = hi = 0.0
-    for b_bar, alpha in factors:
-        lo = min(lo, float(alpha.min()), float(b_bar.min()))
-        hi = max(hi, float(alpha.max()), float(b_bar.max()))
-    n = sum(sizes)
     dev = factors[0][0].device
-    z = torch.zeros(n, dtype=torch.float64, device=dev)
-    v = torch.zeros(n, dtype=torch.float64, device=dev)
+    K, cmax = len(sizes), max(sizes)
+    B = torch.zeros((K, cmax, cmax), dtype=torch.float64, device=dev)
+    al = torch.zeros((K, cmax), dtype=torch.float64, device=dev)
+    for k, ((b_bar, alpha), c) in enumerate(zip(factors, sizes)):
+        B[k, :c, :c] = b_bar
+        al[k, :c] = alpha
+    zero = torch.zeros((), dtype=torch.float64, device=dev)
+    lo = torch.minimum(zero, torch.minimum(al.min(), B.min()))
+    hi = torch.maximum(zero, torch.maximum(al.max(), B.max()))
+    z = torch.zeros((K, cmax), dtype=torch.float64, device=dev)
+    v = torch.zeros((K, cmax), dtype=torch.float64, device=dev)
     kappa = lam / rho
     for _ in range(iters):
-        at = 0
-        for (b_bar, alpha), c in zip(factors, sizes):
-            zk, vk = z[at:at + c], v[at:at + c]
-            xk = alpha + b_bar @ (zk - vk)
-            xv = xk + vk
-            znew = torch.where(xv > kappa, xv - kappa, torch.where(xv < -kappa, xv + kappa, torch.zeros_like(xv)))
-            v[at:at + c] = vk + (xk - znew)
-            z[at:at + c] = znew
-            lo = min(lo, float(znew.min()), float((-v[at:at + c]).min()))
-            hi = max(hi, float(znew.max()), float((-v[at:at + c]).max()))
-            at += c
+        x = al + torch.bmm(B, (z - v).unsqueeze(2)).squeeze(2)
+        xv = x + v
+        z = torch.where(xv > kappa, xv - kappa, torch.where(xv < -kappa, xv + kappa, torch.zeros_like(xv)))
+        v = v + (x - z)
+        lo = torch.minimum(lo, torch.minimum(z.min(), (-v).min()))
+        hi = torch.maximum(hi, torch.maximum(z.max(), (-v).max()))
+    lo, hi = float(lo), float(hi)
     # widen_bounds (quantize.cpp:114-129)
     if hi - lo < 1e-12:
         lo -= 0.5

@@ -40,3 +40,24 @@ def test_mask_width_zero_draws_nothing():
     assert not ADMM.draw_masks(r, 10, 0).any() and r.state == 5
     with pytest.raises(ValueError, match="mask width above 64"):
         ADMM.draw_mask(r, 65)
+
+
+@pytest.mark.parametrize("m,n,k,iters", [(20, 30, 3, 10), (40, 64, 4, 25), (30, 50, 7, 6), (12, 8, 3, 5)])
+def test_batched_session_bounds_follow_the_restated_rehearsal(m, n, k, iters):
+    """session_bounds (protocol.cpp:29-70) advances every block at once over the zero-padded stack
+    of node factors; the QuantSpec equals the per-block restatement (oracle/admm_oracle.py)."""
+    import numpy as np
+    import torch
+
+    import admm_oracle as AO
+
+    a, y, _ = AO.gen_gaussian_problem(m, n, 0.1, 3)
+    sizes = AO.split_columns(n, k)
+    fac, at = [], 0
+    for c in sizes:
+        fac.append(AO.node_factor(a[:, at:at + c], y, 1.0, k))
+        at += c
+    want = AO.session_bounds(a, y, 1.0, 1.0, iters, sizes, 1.5, 1e15, fac)
+    got = ADMM.session_bounds([(torch.as_tensor(b), torch.as_tensor(al)) for b, al in fac], sizes, 1.0, 1.0, iters,
+                              1.5, 1e15)
+    assert np.allclose(got, want, rtol=1e-12, atol=0)
