@@ -13,7 +13,8 @@
 //     path (pcb_quantize_encrypt) is the g = n + 1 form, as north_star fixes it.
 //   * Engine::coeff_fft is accepted and runs the same CUDA path (the reference pins the two lanes
 //     to identical results, test_paillier.cpp:242-257); there is no second lane to dispatch to.
-//   * Keys above 3072 bits (4096) are refused by the device context (std::invalid_argument).
+//   * Keys up to 4096 bits (the reference keygen's largest size); larger moduli are refused by the
+//     device context.
 // Errors map 1:1 to the reference's exception types (paillier.cpp; pcb_status in pcb200.h).
 #pragma once
 

@@ -564,9 +564,9 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
     x->nbits = (uint32_t)x->n.bit_length();
     x->L = (x->nbits + 31) / 32;
     x->S2 = kernel_width_wide(2 * x->L);
-    // Keys above 3072 bits (the reference's keygen also offers 4096, paillier.cpp:107-109) need an
-    // 8192-bit n^2 core that this build does not have: refuse them explicitly, not as a shape error.
-    if (x->S2 == 0) return x->nbits > 3072 ? PCB_E_UNSUPPORTED : PCB_E_SHAPE;
+    // Keys up to 4096 bits (the reference keygen's largest size, paillier.cpp:107-109): n^2 on the
+    // radix core up to 8192 bits; anything larger is refused explicitly, not as a shape error.
+    if (x->S2 == 0) return x->nbits > 4096 ? PCB_E_UNSUPPORTED : PCB_E_SHAPE;
     x->has_prv = p && q;
     if (x->has_prv) {
       x->p = HBN::from_limbs(p, pq_limbs);
@@ -580,15 +580,15 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
         // streaming RNS core for the CRT halves (default; PCB_RNSX=0 selects the older cores)
         const char* ev = getenv("PCB_RNSX");
         int K = 0;
-        if ((!ev || atoi(ev) != 0) && (x->S == 64 || x->S == 96) && rnsx_shape((int)(32 * x->S), &K))
+        if ((!ev || atoi(ev) != 0) && (x->S == 64 || x->S == 96 || x->S == 128) && rnsx_shape((int)(32 * x->S), &K))
           x->use_rnsx = rnsx_build(p2, x->n, x->S, K, &x->rx_p) && rnsx_build(q2, x->n, x->S, K, &x->rx_q);
         x->has_rx = x->use_rnsx;
         const char* es = getenv("PCB_ENC_SPLIT");
         const size_t hb = (size_t)16 * x->S;  // half the p^2 width: p, q bits
-        if (x->use_rnsx && (x->S == 64 || x->S == 96) && x->p.bit_length() <= hb && x->q.bit_length() <= hb &&
+        if (x->use_rnsx && (x->S == 64 || x->S == 96 || x->S == 128) && x->p.bit_length() <= hb && x->q.bit_length() <= hb &&
             (!es || atoi(es) != 0)) {
           x->w1 = x->S / 2;
-          const int K1 = x->S == 64 ? 40 : 56;  // M > (2K+2)^2 p with 30-bit primes
+          const int K1 = x->S == 64 ? 40 : (x->S == 96 ? 56 : 72);  // M > (2K+2)^2 p with 30-bit primes
           // default: stage 1 on the RNS core; PCB_ENC_SPLIT=1 selects the carry core (1024-bit p only)
           if (!es || atoi(es) == 2 || x->S != 64)
             x->enc_split_rns =
@@ -623,6 +623,14 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
           const char* ev = getenv("PCB_RNS");
           if (!ev || atoi(ev) != 0)
             x->use_rns = rns_build(p2, x->n, 64, &x->rns_p) && rns_build(q2, x->n, 64, &x->rns_q);
+          break;
+        }
+        case 128: {
+          // 4096-bit keys: the CRT halves (4096-bit p^2, q^2) run on the streaming RNS core only
+          if (!x->use_rnsx) return PCB_E_UNSUPPORTED;
+          build_enc<128>(x.get());
+          build_dec<128>(x.get());
+          build_half<128>(x.get());
           break;
         }
         case 96: {
@@ -683,6 +691,7 @@ pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t
       else if (b2 + 4 <= 28 * 76) { rb = 28; nl = 76; tpi = 2; }
       else if (b2 + 4 <= 27 * 152) { rb = 27; nl = 152; tpi = 4; }
       else if (b2 + 4 <= 27 * 240) { rb = 27; nl = 240; tpi = 8; }
+      else if (b2 + 4 <= 27 * 304) { rb = 27; nl = 304; tpi = 8; }
       if (rb) {
         R28Mod c = r28_mod(x->n2, rb, nl);
         x->wide.rb = rb;
@@ -798,6 +807,7 @@ pcb_status pcb_ctx_set_generator(pcb_ctx* x, const uint32_t* g, uint32_t g_limbs
         case 32: build_dec<32>(x); build_half<32>(x); break;
         case 64: build_dec<64>(x); build_half<64>(x); break;
         case 96: build_dec<96>(x); build_half<96>(x); break;
+        case 128: build_dec<128>(x); build_half<128>(x); break;
         default: return PCB_E_UNSUPPORTED;
       }
     }
@@ -921,6 +931,7 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
           count);
     if (!e && S == 64) e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
     if (!e && S == 96) e = launch_garner<96>(*reinterpret_cast<const CrtEncConsts<96>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
+    if (!e && S == 128) e = launch_garner<128>(*reinterpret_cast<const CrtEncConsts<128>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
     scratch_free(up, st);
     scratch_free(uq, st);
   } else if (!e && x->use_rnsx) {
@@ -936,6 +947,7 @@ static pcb_status enc_core(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, cons
         count);
     if (!e && S == 64) e = launch_garner<64>(*reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
     if (!e && S == 96) e = launch_garner<96>(*reinterpret_cast<const CrtEncConsts<96>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
+    if (!e && S == 128) e = launch_garner<128>(*reinterpret_cast<const CrtEncConsts<128>*>(x->enc_blob.data()), yp, yq, stv, c, (int)x->L, count, st);
   } else if (!e && x->use_rns) {
     const auto& k = *reinterpret_cast<const CrtEncConsts<64>*>(x->enc_blob.data());
     const double mm = 2.0 * 64 * 64 + 64, alg = ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm + 2 * mm;
@@ -1023,6 +1035,7 @@ static pcb_status dec_core(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t
         count);
     if (!e && S == 64) e = launch_dec_finish<64>(*reinterpret_cast<const CrtDecConsts<64>*>(x->dec_blob.data()), yp, yq, stv, m, (int)x->L, count, st);
     if (!e && S == 96) e = launch_dec_finish<96>(*reinterpret_cast<const CrtDecConsts<96>*>(x->dec_blob.data()), yp, yq, stv, m, (int)x->L, count, st);
+    if (!e && S == 128) e = launch_dec_finish<128>(*reinterpret_cast<const CrtDecConsts<128>*>(x->dec_blob.data()), yp, yq, stv, m, (int)x->L, count, st);
   } else if (!e && x->use_rns) {
     const auto& k = *reinterpret_cast<const CrtDecConsts<64>*>(x->dec_blob.data());
     const double mm = 2.0 * 64 * 64 + 64,
@@ -1101,6 +1114,7 @@ static pcb_status run_wide(pcb_ctx* x, const WStep* prog, int nsteps, const uint
   PCB_W(28, 76, 2)
   PCB_W(27, 152, 4)
   PCB_W(27, 240, 8)
+  PCB_W(27, 304, 8)
 #undef PCB_W
   return PCB_E_UNSUPPORTED;
 }
@@ -1171,6 +1185,7 @@ static pcb_status run_pub_enc(pcb_ctx* x, const uint32_t* r, const uint32_t* m, 
   PCB_W(28, 76, 2)
   PCB_W(27, 152, 4)
   PCB_W(27, 240, 8)
+  PCB_W(27, 304, 8)
 #undef PCB_W
   return PCB_E_UNSUPPORTED;
 }
@@ -1483,6 +1498,9 @@ static pcb_status dwh_core(pcb_ctx* x, const uint32_t* c, const uint32_t* pw, si
   if (!e && S == 96)
     e = launch_dec_finish<96>(*reinterpret_cast<const CrtDecConsts<96>*>(x->half_blob.data()), yp, yq, stv, m,
                               (int)x->L, count, st);
+  if (!e && S == 128)
+    e = launch_dec_finish<128>(*reinterpret_cast<const CrtDecConsts<128>*>(x->half_blob.data()), yp, yq, stv, m,
+                              (int)x->L, count, st);
   scratch_free(yp, st);
   scratch_free(yq, st);
   return e;
@@ -1695,6 +1713,9 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
   if (!e && S == 96)
     e = launch_garner<96>(*reinterpret_cast<const CrtEncConsts<96>*>(x->enc_blob.data()), yp, yq, stv,
                           (uint32_t*)sc.dev, (int)x->L, count, st);
+  if (!e && S == 128)
+    e = launch_garner<128>(*reinterpret_cast<const CrtEncConsts<128>*>(x->enc_blob.data()), yp, yq, stv,
+                          (uint32_t*)sc.dev, (int)x->L, count, st);
   if (!e) e = unstage_out(c, &sc, st);
   if (!e) e = unstage_out(status, &ss, st);
   if (!e && !status) e = first_failure(stv, count, st);
@@ -1773,6 +1794,9 @@ pcb_status pcb_finish_split_encrypt_rn(pcb_ctx* x, const uint32_t* m, uint32_t m
                           count, st);
   if (!e && S == 96)
     e = launch_garner<96>(*reinterpret_cast<const CrtEncConsts<96>*>(x->enc_blob.data()), yp, yq, stv, c1, (int)x->L,
+                          count, st);
+  if (!e && S == 128)
+    e = launch_garner<128>(*reinterpret_cast<const CrtEncConsts<128>*>(x->enc_blob.data()), yp, yq, stv, c1, (int)x->L,
                           count, st);
   std::vector<WStep> p = prog_hom_add();  // CRT(...) * rn mod n^2; failed rows have c1 = 0 -> c = 0
   if (!e) e = run_wide(x, p.data(), (int)p.size(), (const uint32_t*)sr.dev, c1, nullptr, 1, count, count,

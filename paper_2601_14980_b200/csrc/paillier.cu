@@ -735,5 +735,6 @@ pcb_status launch_obfuscate(const uint32_t* value, int vw, const uint64_t* mask,
 PCB_INSTANTIATE(32)
 PCB_INSTANTIATE(64)
 PCB_INSTANTIATE(96)
+PCB_INSTANTIATE(128)
 
 }  // namespace pcb

@@ -77,12 +77,14 @@ inline int kernel_width(uint32_t limbs) {
   if (limbs <= 32) return 32;
   if (limbs <= 64) return 64;
   if (limbs <= 96) return 96;
+  if (limbs <= 128) return 128;  // 4096-bit keys: p^2, q^2 (RNS core only)
   return 0;
 }
 inline int kernel_width_wide(uint32_t limbs) {
   if (limbs <= 64) return 64;
   if (limbs <= 128) return 128;
   if (limbs <= 192) return 192;
+  if (limbs <= 256) return 256;  // 4096-bit keys: n^2 = 8192 bits
   return 0;
 }
 

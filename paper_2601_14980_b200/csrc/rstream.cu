@@ -39,10 +39,10 @@ struct RsArgs {
   int W;                // u64 words per candidate
   uint64_t topmask;     // mask of the top word (bits % 64 != 0)
   int L;                // n limbs (u32)
-  uint32_t n[96];       // n (LE u32, L limbs)
+  uint32_t n[128];      // n (LE u32, L limbs; <= 4096-bit keys)
   int has_prv;
   int H;                // p, q limbs
-  uint32_t p[48], q[48];
+  uint32_t p[64], q[64];
   uint32_t pinv, qinv;  // -p^-1, -q^-1 mod 2^32
   int32_t* flags;       // nblocks
   const int32_t* rank;  // nblocks (emit pass)
@@ -63,7 +63,7 @@ __device__ __forceinline__ void gen_candidate(const RsArgs& P, uint64_t k, uint3
 
 // REDC_p(c): c (L limbs, c < p 2^(32H)) -> c 2^(-32H) mod p; returns true iff the result is 0.
 __device__ bool divisible(const uint32_t* c, int L, const uint32_t* p, uint32_t pinv, int H) {
-  uint32_t t[2 * 48 + 2];
+  uint32_t t[2 * 64 + 2];
   for (int i = 0; i < 2 * H + 2; i++) t[i] = i < L ? c[i] : 0u;
   for (int i = 0; i < H; i++) {
     const uint32_t q = t[i] * pinv;
@@ -91,7 +91,7 @@ __device__ bool divisible(const uint32_t* c, int L, const uint32_t* p, uint32_t 
 
 // gcd(c, n) == 1 by binary gcd (public-key contexts only).
 __device__ bool coprime_binary(const uint32_t* c, const uint32_t* n, int L) {
-  uint32_t a[96], b[96];
+  uint32_t a[128], b[128];
   for (int i = 0; i < L; i++) {
     a[i] = c[i];
     b[i] = n[i];
@@ -142,7 +142,7 @@ __device__ bool coprime_binary(const uint32_t* c, const uint32_t* n, int L) {
 
 __global__ void rs_flag_kernel(const __grid_constant__ RsArgs P) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < P.nblocks; k += gridDim.x * blockDim.x) {
-    uint32_t c[96];
+    uint32_t c[128];
     gen_candidate(P, P.block0 + k, c);
     // < n ?  (random_below, bignat.cpp:438-445)
     bool lt = false;
@@ -169,7 +169,7 @@ __global__ void rs_emit_kernel(const __grid_constant__ RsArgs P, int base_rank) 
     if (!P.flags[k]) continue;
     const int r = base_rank + P.rank[k];
     if (r >= P.count) continue;
-    uint32_t c[96];
+    uint32_t c[128];
     gen_candidate(P, P.block0 + k, c);
     uint32_t* dst = P.r_out + (size_t)r * P.L;
     for (int i = 0; i < P.L; i++) dst[i] = c[i];
@@ -185,7 +185,7 @@ static uint32_t neg_inv(uint32_t m0) {
 // Host driver: fills r_out (device, count x L) and advances *state exactly like the reference.
 pcb_status rstream_sample(uint64_t* state, const uint32_t* n, int L, int nbits, const uint32_t* p, const uint32_t* q,
                           int H, size_t count, uint32_t* r_out, cudaStream_t st) {
-  if (L > 96 || H > 48) return PCB_E_UNSUPPORTED;
+  if (L > 128 || H > 64) return PCB_E_UNSUPPORTED;
   RsArgs P{};
   P.state0 = *state;
   P.W = (nbits + 63) / 64;

@@ -287,5 +287,6 @@ PCB_SIDE28(28, 76, 2)   // 2048-bit keys: p^2 <= 2124 bits; n^2 of 1024-bit keys
 PCB_SIDE28(28, 112, 2)  // 3072-bit keys: p^2 <= 3132 bits
 PCB_SIDE28(27, 152, 4)  // n^2 of 2048-bit keys (public-key encryption)
 PCB_SIDE28(27, 240, 8)  // n^2 of 3072-bit keys (6144 bits)
+PCB_SIDE28(27, 304, 8)  // n^2 of 4096-bit keys (8192 bits)
 
 }  // namespace pcb

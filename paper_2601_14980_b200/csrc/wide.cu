@@ -220,5 +220,6 @@ PCB_WIDE(28, 38, 1)   // n^2 <= 1060 bits (toy / 64-bit keys)
 PCB_WIDE(28, 76, 2)   // n^2 <= 2124 bits (1024-bit keys)
 PCB_WIDE(27, 152, 4)  // n^2 <= 4100 bits (2048-bit keys)
 PCB_WIDE(27, 240, 8)  // n^2 <= 6476 bits (3072-bit keys)
+PCB_WIDE(27, 304, 8)  // n^2 <= 8204 bits (4096-bit keys)
 
 }  // namespace pcb
