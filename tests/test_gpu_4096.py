@@ -74,3 +74,26 @@ def test_homomorphic_operations_and_aggregate(keys):
     agg = edge.aggregate_batch(c)
     d = ph.decrypt_batch(np.ascontiguousarray(agg.reshape(1, -1)))
     assert L.limbs_to_ints(d)[0] == sum(ms) % kp.n
+
+
+@pytest.mark.parametrize("variant", ["basic", "collab"])
+def test_session_4096_bit_exact_vs_shadow(keys, variant):
+    """The encrypted ADMM session on a 4096-bit key (both variants; the collaborative one delegates
+    the 4096-bit p^2 side to the edges) is bit-identical to the reference's shadow pipeline."""
+    import admm_oracle as AO
+    from paper_2601_14980_b200 import admm as ADMM
+
+    kp, _ = keys
+    iters = 3
+    a, y, _ = AO.gen_gaussian_problem(24, 40, 0.1, 2)
+    sizes = AO.split_columns(40, 2)
+    fac, at = [], 0
+    for c in sizes:
+        fac.append(AO.node_factor(a[:, at:at + c], y, 1.0, 2))
+        at += c
+    spec = AO.session_bounds(a, y, 1.0, 1.0, iters, sizes, 1.5, 1e15, fac)
+    res = ADMM.EncryptedSession(kp, ADMM.SessionConfig(nodes=2, iters=iters, variant=variant)).run(
+        a, y, factors=fac, spec=spec)
+    trace, z, v = AO.shadow_session_ref(fac, sizes, spec, 1.0, 1.0, iters)
+    assert all(np.array_equal(res.x_trace[t], trace[t]) for t in range(iters))
+    assert np.array_equal(res.z, z) and np.array_equal(res.v, v)
