@@ -1765,7 +1765,9 @@ pcb_status launch_rnsx(const RnsXModulus& md, int mode, const uint8_t* ops, int 
     const char* p3v = getenv("PCB_RNSX_NT3");
     if (pp && md.K == 40 && p3v && atoi(p3v) != 0 && count >= (size_t)nsm * 3 * 128)
       return launch_cfg<Cfg<40, 3>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
-    if (pp && count >= (size_t)nsm * 2 * 128) {  // pairs only pay once every SM has two tiles
+    // pairs only pay in latency once every SM has two tiles; background work (a low-priority
+    // context) takes them anyway: half the SMs for ~1.3x the time leaves the rest to the critical path
+    if (pp && (count >= (size_t)nsm * 2 * 128 || (md.prefer_pairs && count > 128))) {
       if (md.K == 72)
         return launch_cfg<Cfg<72, 2>>(md, mode, ops, nops, ntab, x, x_words, m, m_words, count, y, st, alg_mac32, nullptr, skip);
       if (md.K == 56)

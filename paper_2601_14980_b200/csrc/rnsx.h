@@ -55,6 +55,7 @@ struct RxProg {
 
 struct RnsXModulus {
   int K = 0, S = 0;           // primes per base, words of N
+  bool prefer_pairs = false;  // two tiles per CTA whatever the count (background work: least SM time)
   int mpw = 0;                // words of M' (output conversion)
   uint8_t* d_wimg = nullptr;  // base-extension stream: one slice (<= 128 x 32 bytes) per MMA, x kRxReplicas
   uint8_t* d_wimg2 = nullptr; // the same stream with every slice split in two row halves (cta_group::2)
