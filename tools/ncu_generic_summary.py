@@ -28,7 +28,7 @@ def byt(k):
 
 
 dur_ns = num("gpu__time_duration.sum") * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(
-    units.get("gpu__time_duration.sum"), 1)
+    units.get("gpu__time_duration.sum"), {"ms": 1e6, "us": 1e3, "ns": 1}.get(units.get("gpu__time_duration.sum"), 1))
 pipes = {k.replace("sm__pipe_", "").replace("_cycles_active.avg.pct_of_peak_sustained_active", ""): num(k)
          for k in d if k.startswith("sm__pipe_") and k.endswith("_cycles_active.avg.pct_of_peak_sustained_active")}
 stalls = {k.replace("smsp__average_warp_latency_issue_stalled_", "").replace(".ratio", ""): num(k)
