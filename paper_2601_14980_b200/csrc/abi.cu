@@ -552,6 +552,7 @@ pcb_status pcb_random_prime(uint64_t* rng_state, uint32_t bits, uint32_t* out) {
 
 pcb_status pcb_ctx_create(pcb_ctx** out, int device, const uint32_t* n, uint32_t n_limbs, const uint32_t* p,
                           const uint32_t* q, uint32_t pq_limbs) {
+  PCB_RANGE("pcb_ctx_create");
   if (!out || !n || n_limbs == 0) return PCB_E_SHAPE;
   *out = nullptr;
   std::unique_ptr<pcb_ctx> x(new (std::nothrow) pcb_ctx);
@@ -1329,6 +1330,7 @@ extern "C" {
 
 pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* r, size_t count, uint32_t* c,
                        int use_crt, int32_t* status, pcb_stream stream) {
+  PCB_RANGE("pcb_encrypt");
   if (!x || (count && (!m || !r || !c))) return PCB_E_SHAPE;
   if (m_limbs == 0 || m_limbs > x->L) return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
@@ -1402,6 +1404,7 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
 // (= pcb_encrypt(m = 0, r)); the value equals crt_encrypt_with_r(m, r) / encrypt_with_r(m, r).
 pcb_status pcb_encrypt_rn(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* rn, size_t count,
                           uint32_t* c, int32_t* status, pcb_stream stream) {
+  PCB_RANGE("pcb_encrypt_rn");
   if (!x || (count && (!m || !rn || !c))) return PCB_E_SHAPE;
   if (m_limbs == 0 || m_limbs > x->L) return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
@@ -1448,6 +1451,7 @@ pcb_status pcb_encrypt_rn(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const
 
 pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m, int use_crt, int32_t* status,
                        pcb_stream stream) {
+  PCB_RANGE("pcb_decrypt");
   if (!x || (count && (!c || !m))) return PCB_E_SHAPE;
   if (!x->has_prv) return PCB_E_NO_PRIVATE;
   if (count == 0) return PCB_OK;
@@ -1564,6 +1568,7 @@ void pcb_share_destroy(pcb_share* sh) {
 // core with a per-element 4-bit window table.
 pcb_status pcb_delegated_power(pcb_share* sh, const uint32_t* base, uint32_t base_limbs, const uint32_t* obf,
                                uint32_t obf_limbs, size_t count, uint32_t* out, pcb_stream stream) {
+  PCB_RANGE("pcb_delegated_power");
   if (!sh || (count && (!base || !obf || !out)) || base_limbs == 0 || base_limbs > (uint32_t)(2 * sh->S) || !obf_limbs)
     return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
@@ -1603,6 +1608,7 @@ pcb_status pcb_delegated_power(pcb_share* sh, const uint32_t* base, uint32_t bas
 
 pcb_status pcb_decrypt_with_half(pcb_ctx* x, const uint32_t* c, const uint32_t* p2_power, uint32_t pw_limbs,
                                  size_t count, uint32_t* m, int32_t* status, pcb_stream stream) {
+  PCB_RANGE("pcb_decrypt_with_half");
   if (!x || (count && (!c || !p2_power || !m)) || pw_limbs == 0 || pw_limbs > 2 * x->L) return PCB_E_SHAPE;
   if (!x->has_prv) return PCB_E_NO_PRIVATE;
   if (!x->has_rx) return PCB_E_UNSUPPORTED;
@@ -1643,6 +1649,7 @@ pcb_status pcb_decrypt_with_half(pcb_ctx* x, const uint32_t* c, const uint32_t* 
 pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* p2_g_power,
                                     uint32_t pg_limbs, const uint32_t* r, size_t count, uint32_t* c, int32_t* status,
                                     pcb_stream stream) {
+  PCB_RANGE("pcb_finish_split_encrypt");
   if (!x || (count && (!m || !p2_g_power || !r || !c)) || pg_limbs == 0 || pg_limbs > 2 * x->L) return PCB_E_SHAPE;
   if (!x->has_prv) return PCB_E_NO_PRIVATE;
   if (!x->has_rx) return PCB_E_UNSUPPORTED;
@@ -1750,6 +1757,7 @@ pcb_status pcb_finish_split_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_li
 pcb_status pcb_finish_split_encrypt_rn(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const uint32_t* p2_g_power,
                                        uint32_t pg_limbs, const uint32_t* rn, size_t count, uint32_t* c,
                                        int32_t* status, pcb_stream stream) {
+  PCB_RANGE("pcb_finish_split_encrypt_rn");
   if (!x || (count && (!m || !p2_g_power || !rn || !c)) || pg_limbs == 0 || pg_limbs > 2 * x->L) return PCB_E_SHAPE;
   if (m_limbs == 0 || m_limbs > x->L) return PCB_E_SHAPE;
   if (!x->has_prv) return PCB_E_NO_PRIVATE;
@@ -1828,6 +1836,7 @@ pcb_status pcb_finish_split_encrypt_rn(pcb_ctx* x, const uint32_t* m, uint32_t m
 
 pcb_status pcb_hom_add(pcb_ctx* x, const uint32_t* a, const uint32_t* b, size_t count, uint32_t* out,
                        pcb_stream stream) {
+  PCB_RANGE("pcb_hom_add");
   if (!x || (count && (!a || !b || !out))) return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
   if (auto e = set_device(x)) return e;
@@ -1852,6 +1861,7 @@ pcb_status pcb_hom_add(pcb_ctx* x, const uint32_t* a, const uint32_t* b, size_t 
 
 pcb_status pcb_hom_scalar_mul(pcb_ctx* x, const uint64_t* k, const uint32_t* c, size_t count, uint32_t* out,
                               pcb_stream stream) {
+  PCB_RANGE("pcb_hom_scalar_mul");
   if (!x || (count && (!k || !c || !out))) return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
   if (auto e = set_device(x)) return e;
@@ -1876,6 +1886,7 @@ pcb_status pcb_hom_scalar_mul(pcb_ctx* x, const uint64_t* k, const uint32_t* c, 
 }
 
 pcb_status pcb_aggregate(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* out, pcb_stream stream) {
+  PCB_RANGE("pcb_aggregate");
   if (!x || !c || !out || count == 0) return PCB_E_SHAPE;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
@@ -2101,6 +2112,7 @@ static pcb_status matvec_core(pcb_ctx* x, const uint32_t* alpha, const uint64_t*
 
 pcb_status pcb_hom_matvec(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo, const uint32_t* zv, size_t rows,
                           size_t cols, uint32_t window, uint32_t* out, pcb_stream stream) {
+  PCB_RANGE("pcb_hom_matvec");
   if (!x || (rows && (!alpha || !out)) || (rows && cols && (!expo || !zv))) return PCB_E_SHAPE;
   if (window < 1 || window > 8) return PCB_E_SHAPE;  // paillier.cpp:449
   if (rows == 0) return PCB_OK;
@@ -2254,6 +2266,7 @@ pcb_status pcb_edge_step(pcb_ctx* x, const uint32_t* alpha, const uint64_t* expo
 pcb_status pcb_edge_step_blocks(pcb_ctx* x, size_t nblocks, const uint32_t* sizes, const uint32_t* alpha,
                                 const uint64_t* expo, const uint32_t* zc, const uint32_t* vc, uint32_t window,
                                 uint32_t* out, pcb_stream stream) {
+  PCB_RANGE("pcb_edge_step_blocks");
   return edge_entry(x, nblocks, sizes, alpha, expo, zc, vc, window, out, stream);
 }
 
@@ -2340,6 +2353,7 @@ pcb_status pcb_decrypt_update_blocks(pcb_ctx* x, size_t nblocks, const uint32_t*
                                      const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv, double z_min,
                                      double z_max, double delta, double kappa, double* xo, double* zo, double* vo,
                                      int32_t* status, pcb_stream stream) {
+  PCB_RANGE("pcb_decrypt_update_blocks");
   return update_entry(x, nblocks, sizes, c, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, status, stream);
 }
 
@@ -2415,6 +2429,7 @@ pcb_status pcb_edge_step_blocks_async(pcb_ctx* x, size_t nblocks, const uint32_t
                                       const uint64_t* expo, uint32_t expo_bits, const uint32_t* zc,
                                       const uint32_t* vc, uint32_t window, uint32_t* out, int32_t* err_dev,
                                       pcb_stream stream) {
+  PCB_RANGE("pcb_edge_step_blocks_async");
   if (!x || (nblocks && !sizes) || !err_dev) return PCB_E_SHAPE;
   if (window < 1 || window > 8) return PCB_E_SHAPE;
   size_t total = 0;
@@ -2444,6 +2459,7 @@ pcb_status pcb_decrypt_update_blocks_async(pcb_ctx* x, size_t nblk, const uint32
                                            const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
                                            double z_min, double z_max, double delta, double kappa, double* xo,
                                            double* zo, double* vo, int32_t* err_dev, pcb_stream stream) {
+  PCB_RANGE("pcb_decrypt_update_blocks_async");
   if (!x || (nblk && !sizes) || !err_dev) return PCB_E_SHAPE;
   std::vector<long long> seg(nblk + 1, 0);
   for (size_t k = 0; k < nblk; k++) seg[k + 1] = seg[k] + sizes[k];
@@ -2483,6 +2499,7 @@ pcb_status pcb_decrypt_update_blocks_half(pcb_ctx* x, size_t nblocks, const uint
                                           const uint32_t* p2_power, const uint64_t* rowsum, const uint64_t* q_z,
                                           const uint64_t* q_nv, double z_min, double z_max, double delta, double kappa,
                                           double* xo, double* zo, double* vo, int32_t* status, pcb_stream stream) {
+  PCB_RANGE("pcb_decrypt_update_blocks_half");
   if (!p2_power) return PCB_E_SHAPE;
   return update_entry(x, nblocks, sizes, c, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, status, stream,
                       p2_power);
@@ -2540,6 +2557,7 @@ pcb_status pcb_quantize(const double* v, size_t count, double z_min, double z_ma
 }
 
 pcb_status pcb_sample_r(pcb_ctx* x, uint64_t* rng_state, size_t count, uint32_t* r_out, pcb_stream stream) {
+  PCB_RANGE("pcb_sample_r");
   if (!x || !rng_state || (count && !r_out)) return PCB_E_SHAPE;
   if (count == 0) return PCB_OK;
   if (auto e = set_device(x)) return e;
@@ -2564,6 +2582,7 @@ pcb_status pcb_sample_r(pcb_ctx* x, uint64_t* rng_state, size_t count, uint32_t*
 pcb_status pcb_quantize_encrypt(pcb_ctx* x, const double* v, size_t count, double z_min, double z_max, double delta,
                                 int fine, const uint32_t* r, int use_crt, uint32_t* c, uint64_t* q_out,
                                 uint64_t* clamps, pcb_stream stream) {
+  PCB_RANGE("pcb_quantize_encrypt");
   if (!x || (count && (!v || !r || !c))) return PCB_E_SHAPE;
   // check_spec (quantize.cpp:8-15)
   if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
@@ -2647,6 +2666,7 @@ pcb_status pcb_quantize_encrypt(pcb_ctx* x, const double* v, size_t count, doubl
 
 pcb_status pcb_modexp_batch(const uint32_t* m, uint32_t m_limbs, const uint32_t* e, uint32_t e_limbs,
                             const uint32_t* xs, size_t count, uint32_t* y, pcb_stream stream) {
+  PCB_RANGE("pcb_modexp_batch");
   if (!m || !e || (count && (!xs || !y))) return PCB_E_SHAPE;
   const int S = kernel_width(m_limbs);
   if (!S) return PCB_E_SHAPE;

@@ -416,6 +416,7 @@ pcb_status node_factors_core(const double* a, size_t rows, size_t cols, size_t l
 extern "C" pcb_status pcb_node_factors(const double* a, size_t rows, size_t cols, size_t lda, const double* y,
                                        size_t nblocks, const uint32_t* sizes, double rho, uint32_t k_total,
                                        int over_k, double* b_bar, double* alpha, pcb_stream stream) {
+  PCB_RANGE("pcb_node_factors");
   using namespace pcb;
   // check_inputs (admm.cpp:8-16), node_factor's k_total check (admm.cpp:66), split shape
   if (!a || !y || !sizes || !b_bar || !alpha || rows == 0 || cols == 0 || lda < cols || nblocks == 0)

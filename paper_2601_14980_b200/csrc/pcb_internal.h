@@ -1,6 +1,7 @@
 // pcb_internal.h — shared host/device plumbing of the CUDA library (not part of the ABI).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstddef>
@@ -71,6 +72,16 @@ pcb_status stage_in(const void* p, size_t bytes, cudaStream_t st, Staged* s);
 pcb_status stage_out(void* p, size_t bytes, cudaStream_t st, Staged* s);
 pcb_status unstage_out(void* p, Staged* s, cudaStream_t st);  // copies back if host
 void unstage(Staged* s, cudaStream_t st);
+
+// NVTX range around an ABI call (header-only NVTX v3: a no-op unless a profiler injects itself),
+// so nsys / ncu --nvtx timelines show the library's calls by name.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define PCB_RANGE(name) ::pcb::NvtxRange pcb_nvtx_range_(name)
 
 // Kernel width (limbs) used for a modulus of `limbs` limbs.
 inline int kernel_width(uint32_t limbs) {

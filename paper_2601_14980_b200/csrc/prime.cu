@@ -204,6 +204,7 @@ bool host_pow(const MrBatch& b, std::vector<HBN>& x, void*) {
 extern "C" {
 
 pcb_status pcb_random_prime_speculative(uint64_t* rng_state, uint32_t bits, int device, uint32_t* out) {
+  PCB_RANGE("pcb_random_prime_speculative");
   using namespace pcb;
   if (!rng_state || !out || bits < 2) return PCB_E_SHAPE;
   if (bits > 2048) return PCB_E_SHAPE;
@@ -223,6 +224,7 @@ pcb_status pcb_random_prime_speculative(uint64_t* rng_state, uint32_t bits, int 
 
 pcb_status pcb_keygen_speculative(uint64_t* rng_state, uint32_t key_bits, int device, uint32_t* n, uint32_t* p,
                                   uint32_t* q) {
+  PCB_RANGE("pcb_keygen_speculative");
   using namespace pcb;
   if (!rng_state || !n || !p || !q) return PCB_E_SHAPE;
   HRng rng(*rng_state);

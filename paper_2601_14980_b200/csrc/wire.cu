@@ -114,6 +114,7 @@ extern "C" {
 
 pcb_status pcb_wire_put_cipher_vec(const uint32_t* c, uint32_t W, const uint32_t* plain_bits, size_t count,
                                    uint8_t* out, size_t out_cap, size_t* out_len, pcb_stream stream) {
+  PCB_RANGE("pcb_wire_put_cipher_vec");
   if (!out_len || W == 0 || (count && !c) || count > 0xffffffffu) return PCB_E_SHAPE;
   cudaStream_t st = (cudaStream_t)stream;
   Staged sc, sp, so;
@@ -164,6 +165,7 @@ pcb_status pcb_wire_put_cipher_vec(const uint32_t* c, uint32_t W, const uint32_t
 
 pcb_status pcb_wire_get_cipher_vec(const uint8_t* in, size_t in_len, size_t* off, uint32_t W, size_t max_count,
                                    size_t* count_out, uint32_t* c, uint32_t* plain_bits, pcb_stream stream) {
+  PCB_RANGE("pcb_wire_get_cipher_vec");
   if (!in || !off || !count_out || W == 0) return PCB_E_SHAPE;
   cudaStream_t st = (cudaStream_t)stream;
   const bool dev_in = is_device_ptr(in);
