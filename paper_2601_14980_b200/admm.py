@@ -70,6 +70,10 @@ class SessionConfig:
 
     def validate(self) -> None:
         """The argument errors run_session raises (protocol.cpp:384, 86-88; protocol.hpp:24-41)."""
+        if self.nodes < 1:
+            raise ValueError("need at least one node")  # protocol.cpp:533
+        if self.iters < 1:
+            raise ValueError("need at least one iteration")  # protocol.cpp:534
         if self.variant not in ("basic", "collab"):
             raise ValueError(f"unknown protocol variant {self.variant!r}")
         if self.r_mode not in ("fresh", "pooled"):
@@ -112,6 +116,17 @@ class SessionResult:
     t_master_s: float = 0.0
     master: RoleStats = None
     edges: RoleStats = None  # this rank's edges together
+
+
+def check_spec(spec) -> None:
+    """check_spec (quantize.cpp:8-15) / run_session's window check (protocol.cpp:535-536)."""
+    import math
+
+    z_min, z_max, delta = spec
+    if not (math.isfinite(z_min) and math.isfinite(z_max)) or z_max <= z_min:
+        raise ValueError("quantization window is empty or non-finite")
+    if not (delta >= 1.0) or delta > 9.0e15:
+        raise ValueError("delta outside [1, 9e15]")
 
 
 def draw_mask(rng: Rng, bits: int = 64) -> int:
@@ -284,6 +299,7 @@ class ShardedDriver:
 
         cfg = self.cfg
         cfg.validate()
+        check_spec(spec)
         sync = (lambda: torch.cuda.synchronize(self.dev)) if self.dev != "cpu" else (lambda: None)
         m0 = time.perf_counter()
         n = a.shape[1]
@@ -832,6 +848,7 @@ class FaithfulDriver:
         cfg.validate()
         if cfg.variant != "basic":
             raise ValueError("the faithful-trust driver runs the basic variant")
+        check_spec(spec)
         m0 = time.perf_counter()
         n = a.shape[1]
         self.sizes = split_columns(n, cfg.nodes)

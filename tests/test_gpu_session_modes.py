@@ -204,3 +204,16 @@ def test_finish_split_encrypt_rn_matches_the_r_form():
     c_bad = ph.finish_split_encrypt_rn_batch(M, G, rn, status=st)
     assert st[3] == L.PCB_E_RANDOMNESS_RANGE and (np.delete(st, 3) == 0).all()
     assert not c_bad[3].any() and np.array_equal(np.delete(c_bad, 3, 0), np.delete(c_r, 3, 0))
+
+
+def test_tight_window_clamps_are_counted(bench):
+    """test_protocol.cpp:353-369: a window far too narrow for the factors clamps (and counts it);
+    the properly sized one on the same problem reports none."""
+    a, y, sizes, fac, spec, keys = bench
+    cfg = ADMM.SessionConfig(nodes=NODES, iters=2, seed=SEED, delta=1e6)
+    r = ADMM.EncryptedSession(keys, cfg).run(a, y, factors=fac, spec=(-0.02, 0.02, 1e6))
+    assert r.clamps > 0
+    r_ok = ADMM.EncryptedSession(keys, cfg).run(a, y, factors=fac, spec=spec)
+    assert r_ok.clamps == 0
+    with pytest.raises(ValueError, match="window"):
+        ADMM.EncryptedSession(keys, cfg).run(a, y, factors=fac, spec=(1.0, 1.0, 1e6))

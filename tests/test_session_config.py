@@ -61,3 +61,20 @@ def test_batched_session_bounds_follow_the_restated_rehearsal(m, n, k, iters):
     got = ADMM.session_bounds([(torch.as_tensor(b), torch.as_tensor(al)) for b, al in fac], sizes, 1.0, 1.0, iters,
                               1.5, 1e15)
     assert np.allclose(got, want, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("kw,msg", [({"nodes": 0}, "need at least one node"),
+                                    ({"iters": 0}, "need at least one iteration")])
+def test_session_counts_validated(kw, msg):  # protocol.cpp:533-534, test_protocol.cpp:371-392
+    with pytest.raises(ValueError, match=msg):
+        ADMM.SessionConfig(**kw).validate()
+
+
+@pytest.mark.parametrize("spec", [(1.0, 1.0, 1e6), (2.0, 1.0, 1e6), (float("nan"), 1.0, 1e6), (-1.0, 1.0, 0.5),
+                                  (-1.0, 1.0, 1e16)])
+def test_quant_spec_validated(spec):  # quantize.cpp:8-15, protocol.cpp:535-536
+    with pytest.raises(ValueError):
+        ADMM.check_spec(spec)
+    ADMM.check_spec((-1.0, 1.0, 1e15))
+    with pytest.raises(ValueError):
+        ADMM.split_columns(8, 9)  # more nodes than columns (test_protocol.cpp:388-391)
