@@ -78,3 +78,22 @@ def test_quant_spec_validated(spec):  # quantize.cpp:8-15, protocol.cpp:535-536
     ADMM.check_spec((-1.0, 1.0, 1e15))
     with pytest.raises(ValueError):
         ADMM.split_columns(8, 9)  # more nodes than columns (test_protocol.cpp:388-391)
+
+
+def test_session_bounds_cover_the_rehearsal_extremes():  # test_protocol.cpp:97-123
+    import torch
+
+    import admm_oracle as AO
+
+    a, y, _ = AO.gen_gaussian_problem(30, 24, 0.2, 11)
+    sizes = AO.split_columns(24, 3)
+    fac, at = [], 0
+    for c in sizes:
+        fac.append(AO.node_factor(a[:, at:at + c], y, 1.0, 3))
+        at += c
+    tf = [(torch.as_tensor(b), torch.as_tensor(al)) for b, al in fac]
+    lo, hi, d = ADMM.session_bounds(tf, sizes, 1.0, 1.0, 20, 1.5, 1e6)
+    assert lo < 0.0 < hi and d == 1e6
+    assert all(lo <= float(v) <= hi for _, al in fac for v in al)
+    lo3, hi3, _ = ADMM.session_bounds(tf, sizes, 1.0, 1.0, 20, 3.0, 1e6)
+    assert lo3 < lo and hi3 > hi
