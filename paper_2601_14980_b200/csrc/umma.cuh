@@ -50,7 +50,19 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+#ifndef PCB_MBAR_SUSPEND_NS
+#define PCB_MBAR_SUSPEND_NS 0  // > 0: try_wait's suspend-time hint (fewer re-polls of a pending phase)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+#if PCB_MBAR_SUSPEND_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+      "r"(parity), "n"(PCB_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
@@ -58,6 +70,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {

@@ -83,3 +83,21 @@ def test_argument_errors():
     a[3, 2] = float("nan")
     with pytest.raises(ValueError):
         ADMM.node_factors(a, y, [5, 5], 1.0, 2)  # not positive definite
+
+
+def test_node_factor_closed_form_for_orthonormal_columns():
+    """test_admm.cpp:112-130: A^T A = I gives B = rho / (1 + rho) I and alpha = A^T y / (1 + rho);
+    YScaling::over_k divides y by K first."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    q, _ = np.linalg.qr(rng.standard_normal((60, 40)))
+    y = rng.standard_normal(60)
+    rho = 0.5
+    for over_k, k in ((False, 4), (True, 4)):
+        got = ADMM.node_factors(torch.as_tensor(q, device="cuda"), torch.as_tensor(y, device="cuda"), [40], rho, k,
+                                over_k)
+        b, al = got[0][0].cpu().numpy(), got[0][1].cpu().numpy()
+        ys = y / k if over_k else y
+        assert np.abs(b - rho / (1 + rho) * np.eye(40)).max() < 1e-13
+        assert np.abs(al - q.T @ ys / (1 + rho)).max() < 1e-13
