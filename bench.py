@@ -284,6 +284,50 @@ def run_cfg5(args, rank: int, world: int, local: int):
     return out
 
 
+def run_p4096(args, rank: int, world: int, local: int):
+    """Paillier-4096 (the reference keygen's largest key, paillier.cpp:107-109; the n = 4096 column of
+    PAPER.md Table II): key from keygen(Rng(4096), 4096) with the Miller-Rabin rounds batched on the
+    device (same key as the reference's keygen), then CRT Enc + CRT Dec of this rank's slice of
+    `p4096_n` values, CUDA-event timed after a warm-up pass, round trip checked."""
+    import torch
+    from paper_2601_14980_b200 import paillier as P
+
+    kp = P.keygen(P.Rng(4096), 4096, device=local)
+    ph = P.Paillier(kp, device=local)
+    off, n = ADMM_slice(args.p4096_n, world, rank)
+    vals = splitmix_units(13, n, offset=off)
+    q64 = np.floor(vals * 2.0**60).astype(np.uint64)
+    m = torch.zeros((n, ph.L), dtype=torch.int32, device="cuda")
+    m[:, 0] = torch.from_numpy((q64 & 0xFFFFFFFF).astype(np.uint32).view(np.int32)).cuda()
+    m[:, 1] = torch.from_numpy((q64 >> 32).astype(np.uint32).view(np.int32)).cuda()
+    rr = P.Rng(17)
+    ph.skip_r(rr, off)
+    r = ph.sample_r_batch(rr, n)
+    st = torch.zeros(n, dtype=torch.int32, device="cuda")
+    w = min(n, 1 << 13)
+    ph.decrypt_batch(ph.encrypt_batch(m[:w], r[:w], True, status=st[:w]), True, status=st[:w])  # warm-up
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    c = ph.encrypt_batch(m, r, True, status=st)
+    e[1].record()
+    d = ph.decrypt_batch(c, True, status=st)
+    e[2].record()
+    torch.cuda.synchronize()
+    te, td = e[0].elapsed_time(e[1]) / 1e3, e[1].elapsed_time(e[2]) / 1e3
+    ok = bool(torch.equal(d, m)) and int(st.ne(0).sum().item()) == 0
+    t = torch.tensor([te + td], device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"metric": "Paillier-4096 Enc+Dec pairs/s", "value": args.p4096_n / float(t.item()),
+            "unit": "Enc+Dec pairs/s", "higher_is_better": True, "enc_per_s": n / te, "dec_per_s": n / td,
+            "parity_check": ok,
+            "config": {"workload": "4096-bit key (keygen(Rng(4096), 4096)), CRT Enc + CRT Dec, values < 2^60",
+                       "values_total": args.p4096_n, "values_per_gpu": n}}
+
+
 def ADMM_slice(total: int, world: int, rank: int):
     from paper_2601_14980_b200 import admm as ADMM
 
@@ -521,6 +565,7 @@ def main() -> None:
     ap.add_argument("--admm-collab-iters", type=int, default=3, help="timed collaborative-variant cfg3 iterations (0 = skip)")
     ap.add_argument("--cfg4-n", type=int, default=1 << 22, help="cfg4 3072-bit values per job, sliced over ranks (0 = skip)")
     ap.add_argument("--cfg5-iters", type=int, default=0, help="timed cfg5 ADMM iterations (N=65536, 64 blocks; 0 = skip)")
+    ap.add_argument("--p4096-n", type=int, default=1 << 17, help="Paillier-4096 values per job (0 = skip)")
     args = ap.parse_args()
     args.e2e_steps = max(1, args.e2e_steps)
 
@@ -689,6 +734,7 @@ def main() -> None:
     admm_c = run_admm_collab(args, rank, world, local) if args.admm_collab_iters > 0 else None
     cfg4 = run_cfg4(args, rank, world, local) if args.cfg4_n > 0 else None
     cfg5 = run_cfg5(args, rank, world, local) if args.cfg5_iters > 0 else None
+    p4096 = run_p4096(args, rank, world, local) if args.p4096_n > 0 else None
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -734,6 +780,7 @@ def main() -> None:
             "admm_collab": admm_c,
             "cfg4": cfg4,
             "cfg5": cfg5,
+            "p4096": p4096,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
