@@ -157,6 +157,8 @@ bool device_pow(const MrBatch& b, std::vector<HBN>& x, void* user) {
   }
   uint32_t* dv = nullptr;
   const size_t words = cnt * L;
+  int prev_dev = 0;
+  cudaGetDevice(&prev_dev);  // the caller's current device is restored below
   pcb_status e = cuda_check(cudaSetDevice(u->device));
   if (!e) e = scratch_alloc((5 * words + cnt) * 4, (void**)&dv, u->st);
   uint32_t *dn = dv, *d1 = dv + words, *d2 = dv + 2 * words, *da = dv + 3 * words, *dd = dv + 4 * words,
@@ -182,6 +184,7 @@ bool device_pow(const MrBatch& b, std::vector<HBN>& x, void* user) {
   if (!e) e = cuda_check(cudaStreamSynchronize(u->st));
   scratch_free(dv, u->st);
   scratch_free(dxo, u->st);
+  cudaSetDevice(prev_dev);
   if (e) {
     u->err = e;
     return false;
