@@ -120,6 +120,7 @@ def run_admm(args, rank: int, world: int, local: int):
     cfg = ADMM.SessionConfig(nodes=8, iters=iters)
     group = dist.group.WORLD if world > 1 else None
     sess = ADMM.EncryptedSession(keys, cfg, device=local, rank=rank, world=world, group=group)
+    sess.profile_iters = (args.admm_warmup, args.admm_warmup + args.admm_iters - 1)
     t0 = time.perf_counter()
     res = sess.run(a, y, record_trace=True)  # x is gathered after the timed part of each iteration
     wall = time.perf_counter() - t0
@@ -136,6 +137,21 @@ def run_admm(args, rank: int, world: int, local: int):
            "final_objective": res.objective[-1], "setup_plus_run_wall_s": wall,
            "phases": {"t_pre_s": res.t_pre_s, "t_master_s": res.t_master_s,
                       "t_loc_s": [round(v, 4) for v in res.t_loc_s], "t_comm_s": [round(v, 4) for v in res.t_comm_s]}}
+    if res.profile and res.profile["kernel_ms"] > 0:
+        # tensor roofline of the iteration's RNS-core launches (the hom_matvec programs at K = 144 dominate,
+        # with the CRT Enc / Dec at K = 40 / 72): int8 ops issued / summed per-launch CUDA-event time
+        here = os.path.dirname(os.path.abspath(__file__))
+        mp_path = os.path.join(here, "MEASURED_PEAKS.json")
+        mp = json.load(open(mp_path)) if os.path.exists(mp_path) else {}
+        i8_peak = 2.0 * float(mp.get("bf16_tflops_sustained", mp.get("bf16_tflops", 1400.0)))
+        ach = 2.0 * res.profile["int8_macs"] / (res.profile["kernel_ms"] / 1e3) / 1e12
+        mv_path = os.path.join(here, "profiles", "r02_matvec_cfg3_ncu.json")
+        mv = json.load(open(mv_path)) if os.path.exists(mv_path) else {}
+        out["roofline"] = {"bound": "tensor", "achieved": ach, "peak": i8_peak, "unit": "TOPS (int8 dense)",
+                           "frac": ach / i8_peak, "kernel": "pcb::rnsx_kernel<144> hom_matvec programs (+ <72>/<40> "
+                           "CRT Enc/Dec)", "launches": res.profile["launches"],
+                           "kernel_ms_per_iteration": res.profile["kernel_ms"] / res.profile["iterations"],
+                           "traffic": mv.get("traffic_bytes_per_launch"), "ncu_pipes_matvec_B": mv.get("pipes")}
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = admm_cpu_leg(sess, res)
     return out

@@ -116,6 +116,7 @@ class SessionResult:
     t_master_s: float = 0.0
     master: RoleStats = None
     edges: RoleStats = None  # this rank's edges together
+    profile: dict = None  # RNS-core launches of the profiled iterations (ShardedDriver.profile_iters)
 
 
 def check_spec(spec) -> None:
@@ -314,7 +315,10 @@ class ShardedDriver:
         res.clamps += self.setup_all()
         sync()
         res.t_pre_s = time.perf_counter() - m0
+        prof = getattr(self, "profile_iters", None)  # (first, last): RNS-core launch profile of those iterations
         for t in range(cfg.iters):
+            if prof and t == prof[0]:
+                L.lib().pcb_profile_begin()
             it0 = time.perf_counter()
             t0 = time.perf_counter()
             comm = 0.0
@@ -349,6 +353,11 @@ class ShardedDriver:
                 res.x_trace.append(xt)
             res.t_comm_s.append(comm)
             res.t_loc_s.append(time.perf_counter() - it0 - comm)
+            if prof and t == prof[1]:
+                ms, nl, alg = C.c_double(), C.c_uint64(), C.c_double()
+                _raise_for(L.lib().pcb_profile_end(C.byref(ms), C.byref(nl), C.byref(alg)), "profile")
+                res.profile = {"kernel_ms": ms.value, "launches": int(nl.value),
+                               "int8_macs": L.lib().pcb_profile_int8_macs(), "iterations": prof[1] - prof[0] + 1}
         res.t_master_s = time.perf_counter() - m0
         self.role_stats(res)
         res.x, res.z, res.v = (self._gather(t_).cpu().numpy() for t_ in (self.x, self.z, self.v))
