@@ -56,6 +56,13 @@ def _worker(rank, world, port, mode, q):
         res = ADMM.EncryptedSession(keys, cfg, device=0, rank=rank, world=world, group=dist.group.WORLD).run(
             a, y, factors=fac, spec=spec)
         out = [t.tolist() for t in res.x_trace]
+    elif mode == "sharded_pooled":
+        cfg = ADMM.SessionConfig(nodes=2, iters=ITERS, r_mode="pooled", pool_size=3)
+        sess = ADMM.EncryptedSession(keys, cfg, device=0, rank=rank, world=world, group=dist.group.WORLD)
+        sess.capture = {"iters": ITERS}
+        res = sess.run(a, y, factors=fac, spec=spec)
+        cts = [c.cpu().numpy().tolist() for c in sess.capture.get("ct", [])]
+        out = ([t.tolist() for t in res.x_trace], cts, sess.mine)
     else:
         dev = torch.device("cuda:0")
         drv = ADMM.FaithfulDriver(ADMM.FaithfulGpuBackend(keys, rank, 0), cfg, rank=rank, world=world,
@@ -105,3 +112,30 @@ def test_faithful_driver_two_ranks_cuda_backend():
     want = [t.tolist() for t in single.x_trace]
     out = _run(2, "faithful")
     assert out[0][1] == want and out[1][1] == []
+
+
+def test_sharded_pooled_session_slices_the_pool_like_one_rank():
+    """Pooled randomness over 3 ranks (one owns nothing): every rank indexes the shared pool at the
+    reference's stream positions, so its enc_state rows equal the single-rank session's."""
+    from paper_2601_14980_b200 import admm as ADMM
+    from paper_2601_14980_b200 import paillier as P
+
+    a, y, fac, spec = _problem()
+    sess = ADMM.EncryptedSession(P.keygen(P.Rng(9), 1024),
+                                 ADMM.SessionConfig(nodes=2, iters=ITERS, r_mode="pooled", pool_size=3))
+    sess.capture = {"iters": ITERS}
+    single = sess.run(a, y, factors=fac, spec=spec)
+    want = [t.tolist() for t in single.x_trace]
+    sizes, n = sess.sizes, sum(sess.sizes)
+    offs = [0, sizes[0]]
+    out = _run(3, "sharded_pooled")
+    for rank, (tr, cts, mine) in out:
+        assert tr == want, rank
+        if not mine:
+            assert cts == []
+            continue
+        for t in range(ITERS):
+            full = sess.capture["ct"][t].cpu().numpy()
+            rows = [full[offs[k]:offs[k] + sizes[k]] for k in mine] + \
+                   [full[n + offs[k]:n + offs[k] + sizes[k]] for k in mine]
+            assert np.array_equal(np.array(cts[t]), np.concatenate(rows)), (rank, t)
