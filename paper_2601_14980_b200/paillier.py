@@ -117,6 +117,57 @@ def random_prime(rng: Rng, bits: int, device: int | None = None) -> int:
     return L.limbs_to_int(out)
 
 
+def _wire_put(out: bytearray, v: int) -> None:
+    """wire_put (bignat.cpp:414-418): u32 BE byte length, then the minimal big-endian magnitude."""
+    b = v.to_bytes((v.bit_length() + 7) // 8, "big") if v else b""
+    out += len(b).to_bytes(4, "big") + b
+
+
+def _wire_get(data: bytes, off: int) -> tuple[int, int]:
+    if off + 4 > len(data):
+        raise RuntimeError("truncated integer field")
+    n = int.from_bytes(data[off:off + 4], "big")
+    if off + 4 + n > len(data):
+        raise RuntimeError("truncated integer field")
+    return int.from_bytes(data[off + 4:off + 4 + n], "big"), off + 4 + n
+
+
+def serialize_keypair(kp: KeyPair) -> bytes:
+    """serialize_keypair (paillier.cpp:152-166), binomial g: 'p' 'k' 1 1, u32 BE key_bits, then
+    wire_put of n, g = n + 1, p, q, epsilon = lcm(p - 1, q - 1), mu = epsilon^-1 mod n."""
+    import math
+
+    eps = (kp.p - 1) * (kp.q - 1) // math.gcd(kp.p - 1, kp.q - 1)
+    out = bytearray(b"pk\x01\x01") + int(kp.key_bits).to_bytes(4, "big")
+    for v in (kp.n, kp.n + 1, kp.p, kp.q, eps, pow(eps % kp.n, -1, kp.n)):
+        _wire_put(out, v)
+    return bytes(out)
+
+
+def parse_keypair(data: bytes) -> KeyPair:
+    """parse_keypair (paillier.cpp:168-191) for binomial-g records; the same errors (RuntimeError)."""
+    if len(data) < 4 or data[0:2] != b"pk":
+        raise RuntimeError("not a key record")
+    if data[2] != 1:
+        raise RuntimeError("unknown key record version")
+    if data[3] == 0:
+        raise NotImplementedError("random-g key records: load them through the C++ drop-in (pcadmm::parse_keypair)")
+    if len(data) < 8:
+        raise RuntimeError("truncated key record")
+    key_bits = int.from_bytes(data[4:8], "big")
+    off = 8
+    vals = []
+    for _ in range(6):
+        v, off = _wire_get(data, off)
+        vals.append(v)
+    n, g, p, q = vals[:4]
+    if p * q != n:
+        raise RuntimeError("corrupt key record: n != p*q")
+    if g != n + 1:
+        raise RuntimeError("corrupt key record: g mismatch")
+    return KeyPair(n, p, q, key_bits)
+
+
 def keypair_from_primes(p: int, q: int) -> KeyPair:
     """pcadmm::keypair_from_primes (binomial g)."""
     if p == q or p < 2 or q < 2:

@@ -85,3 +85,26 @@ def test_product_does_not_import_oracle():
     for f in pkg.rglob("*.py"):
         src = f.read_text()
         assert "pcadmm_oracle" not in src and "refbind" not in src and "oracle/" not in src, f
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2])
+def test_key_record_matches_reference_serializer(idx):
+    """serialize_keypair / parse_keypair (paillier.cpp:152-191): byte-identical to the compiled
+    reference's record for the golden keys, round trip, and the reference's error cases."""
+    import refbind as R_
+
+    k = golden("keys.json")[idx]
+    kp = P.KeyPair(int(k["n"], 16), int(k["p"], 16), int(k["q"], 16), k["bits"])
+    rec = P.serialize_keypair(kp)
+    if R_.available():
+        assert rec == R_.RefKey.keygen(k["seed"], k["bits"]).serialize()
+    assert P.parse_keypair(rec) == kp
+    with pytest.raises(RuntimeError, match="not a key record"):
+        P.parse_keypair(b"xx" + rec[2:])
+    with pytest.raises(RuntimeError, match="version"):
+        P.parse_keypair(rec[:2] + b"\x02" + rec[3:])
+    bad = bytearray(rec)
+    bad[-1] ^= 1  # mu's last byte: still parses (mu is not re-derived), n/p/q intact
+    assert P.parse_keypair(bytes(bad)) == kp
+    with pytest.raises(RuntimeError):
+        P.parse_keypair(rec[:20])
