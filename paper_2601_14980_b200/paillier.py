@@ -79,6 +79,16 @@ class PublicKey:
 
 
 @dataclass
+class RnFactor:
+    """pcadmm::RnFactor (paillier.hpp:78-82): r, r^n mod n^2 and its residues mod p^2 / q^2."""
+
+    r: int
+    full: int
+    half_p2: int
+    half_q2: int
+
+
+@dataclass
 class Ciphertext:
     value: int
     plain_bits: int = 0
@@ -192,6 +202,7 @@ class Paillier:
         self.key_bits = keys.key_bits
         self.L = (n.bit_length() + 31) // 32
         self._has_prv = isinstance(keys, KeyPair)
+        self._p, self._q = (keys.p, keys.q) if self._has_prv else (0, 0)
         nl = L.int_to_limbs(n, self.L)
         ctx = C.c_void_p()
         if self._has_prv:
@@ -361,6 +372,46 @@ class Paillier:
     def crt_encrypt_with_r(self, m: int, r: int) -> Ciphertext:
         self._need_prv()
         return self._enc_list([m], [r], use_crt=True)[0]
+
+    def make_rn_factor(self, r: int) -> "RnFactor":
+        """Paillier::make_rn_factor (paillier.cpp:371-383): r^n mod n^2 (= Enc(0; r)) and, with the
+        private key, its residues mod p^2 / q^2."""
+        if not 0 < r < self.n:
+            raise ValueError("randomness not in [1, n)")
+        full = self._enc_list([0], [r], use_crt=self._has_prv)[0].value
+        if not self._has_prv:
+            return RnFactor(r, full, 0, 0)
+        return RnFactor(r, full, full % (self._p * self._p), full % (self._q * self._q))
+
+    def encrypt_with_factor(self, m: int, f: "RnFactor") -> Ciphertext:
+        """encrypt_with_factor (paillier.cpp:385-389): c = (1 + m n) f.full mod n^2, one multiply."""
+        if not f.full:
+            raise ValueError("factor missing r^n")
+        W = 2 * self.L
+        st = np.zeros(1, np.int32)
+        c = self.encrypt_rn_batch(L.ints_to_limbs([m], self.L), L.ints_to_limbs([f.full], W), status=st)
+        _raise_for(int(st[0]), "element 0")
+        return Ciphertext(L.limbs_to_int(c[0]), int(m).bit_length())
+
+    def crt_encrypt_with_factor(self, m: int, f: "RnFactor") -> Ciphertext:
+        """crt_encrypt_with_factor (paillier.cpp:391-400): the same residue as encrypt_with_factor."""
+        self._need_prv()
+        if not f.half_p2 or not f.half_q2:
+            raise ValueError("factor missing split residues")
+        return self.encrypt_with_factor(m, f)
+
+    def finish_split_encrypt_with_factor(self, m: int, p2_g_power: int, f: "RnFactor") -> Ciphertext:
+        """finish_split_encrypt_with_factor (paillier.cpp:416-426) through pcb_finish_split_encrypt_rn."""
+        self._need_prv()
+        if not f.half_p2 or not f.half_q2:
+            raise ValueError("factor missing split residues")
+        W = 2 * self.L
+        st = np.zeros(1, np.int32)
+        c = self.finish_split_encrypt_rn_batch(L.ints_to_limbs([m], self.L),
+                                               L.ints_to_limbs([int(p2_g_power) % self.n2], W),
+                                               L.ints_to_limbs([f.full], W), status=st)
+        _raise_for(int(st[0]), "element 0")
+        return Ciphertext(L.limbs_to_int(c[0]), int(m).bit_length())
 
     def encrypt_vec(self, ms, rng: Rng, use_crt: bool) -> list[Ciphertext]:
         """Paillier::encrypt_vec (paillier.cpp:495-507): r drawn serially (here: on the GPU, same

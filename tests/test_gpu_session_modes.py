@@ -217,3 +217,26 @@ def test_tight_window_clamps_are_counted(bench):
     assert r_ok.clamps == 0
     with pytest.raises(ValueError, match="window"):
         ADMM.EncryptedSession(keys, cfg).run(a, y, factors=fac, spec=(1.0, 1.0, 1e6))
+
+
+def test_rn_factor_api(bench):
+    """make_rn_factor / encrypt_with_factor / crt_encrypt_with_factor /
+    finish_split_encrypt_with_factor (paillier.cpp:371-426) in the Python mirror: the factor forms
+    give the r forms' ciphertexts; a factor without r^n or residues is rejected."""
+    a, y, sizes, fac, spec, keys = bench
+    ph = P.Paillier(keys)
+    rng = P.Rng(12)
+    for m in (0, 1, 123456789, keys.n - 1):
+        r = ph.sample_r(rng)
+        f = ph.make_rn_factor(r)
+        assert f.full == pow(r, keys.n, keys.n2) and f.half_p2 == f.full % (keys.p ** 2)
+        want = ph.crt_encrypt_with_r(m, r)
+        assert ph.encrypt_with_factor(m, f) == want and ph.crt_encrypt_with_factor(m, f) == want
+        g = pow(keys.n + 1, m, keys.p ** 2)
+        assert ph.finish_split_encrypt_with_factor(m, g, f) == ph.finish_split_encrypt(m, g, r)
+    with pytest.raises(ValueError):
+        ph.make_rn_factor(0)
+    with pytest.raises(ValueError):
+        ph.encrypt_with_factor(5, P.RnFactor(3, 0, 0, 0))
+    with pytest.raises(ValueError):
+        ph.crt_encrypt_with_factor(5, P.RnFactor(3, 7, 0, 0))
