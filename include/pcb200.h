@@ -154,6 +154,11 @@ void pcb_share_destroy(pcb_share* share);
  * base: count x base_limbs (<= 2 x p^2 words), obf: count x obf_limbs, out: count x (p^2 words). */
 pcb_status pcb_delegated_power(pcb_share* share, const uint32_t* base, uint32_t base_limbs, const uint32_t* obf,
                                uint32_t obf_limbs, size_t count, uint32_t* out, pcb_stream stream);
+/* The same for the binomial generator g = n + 1 shared by the batch (n: n_limbs words): the
+ * collapse (1 + n)^e = 1 + e n (mod p^2) (n^2 = 0 mod p^2, as g_power_half, paillier.cpp:259-263);
+ * bit-identical to pcb_delegated_power(base = n + 1, obf) without the exponentiation. */
+pcb_status pcb_delegated_power_binomial(pcb_share* share, const uint32_t* n, uint32_t n_limbs, const uint32_t* obf,
+                                        uint32_t obf_limbs, size_t count, uint32_t* out, pcb_stream stream);
 
 /* out_i = value_i + mask_i * n_eps — obfuscate_exponent (protocol.cpp:11-13), the master's masked
  * exponents for the edges' delegated powers.  value: count x value_limbs, mask: count u64 (draw_mask,

@@ -73,6 +73,7 @@ SIGNATURES = {
     "pcb_share_create": (C.c_int, [C.POINTER(_vp), C.c_int, _vp, C.c_uint32, _vp, C.c_uint32]),
     "pcb_share_destroy": (None, [_vp]),
     "pcb_delegated_power": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_uint32, C.c_size_t, _vp, _vp]),
+    "pcb_delegated_power_binomial": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_uint32, C.c_size_t, _vp, _vp]),
     "pcb_node_factors": (C.c_int, [_vp, C.c_size_t, C.c_size_t, C.c_size_t, _vp, C.c_size_t, _vp, C.c_double,
                                    C.c_uint32, C.c_int, _vp, _vp, _vp]),
     "pcb_finish_split_encrypt": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp, _vp]),

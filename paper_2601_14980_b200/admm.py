@@ -34,6 +34,7 @@ all-reduce, and x/z/v blocks are all-gathered at the end.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -616,6 +617,7 @@ class EncryptedSession(ShardedDriver):
         self.neps_dev = torch.from_numpy(L.int_to_limbs(self.n_eps, self.ne_words).view(np.int32)).to(self.dev)
         g = L.int_to_limbs(self.master.n + 1, 2 * S).view(np.int32)
         self.gbase = torch.from_numpy(np.tile(g, (2 * n, 1))).to(self.dev)  # g for every delegated g power
+        self.n_dev = torch.from_numpy(L.int_to_limbs(self.master.n, self.L).view(np.int32)).to(self.dev)
         rows = []
         for k in self.mine:  # each edge's obf_dec, repeated over its block's rows
             rows.append(np.tile(L.int_to_limbs(self.obf_dec[k], self.ow), (self.sizes[k], 1)))
@@ -644,7 +646,10 @@ class EncryptedSession(ShardedDriver):
         _raise_for(self.lib.pcb_obfuscate_exponent(L.ptr(q), 2, L.ptr(mask), L.ptr(self.neps_dev), self.ne_words, n2,
                                                    L.ptr(self.obf_buf), self.ow, st), "obfuscate_exponent")
         ev = self._wait_begin()
-        gp = self.share.delegated_power_tensor(self.gbase, self.obf_buf, st)
+        if os.environ.get("PCB_COLLAB_GENERIC_GPOW") == "1":  # the generic exponentiation (A/B)
+            gp = self.share.delegated_power_tensor(self.gbase, self.obf_buf, st)
+        else:  # g = n + 1: the binomial collapse, bit-identical (pcb_delegated_power_binomial)
+            gp = self.share.delegated_power_binomial_tensor(self.n_dev, self.obf_buf, st)
         self._wait_end(ev)
         self.delegated_pows += n2
         if self.cfg.r_mode == "pooled":  # finish_split_encrypt_with_factor (protocol.cpp:401-403)

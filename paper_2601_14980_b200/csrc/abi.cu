@@ -342,6 +342,8 @@ pcb_status launch_obfuscate(const uint32_t* value, int vw, const uint64_t* mask,
                             size_t count, uint32_t* out, int ow, cudaStream_t stream);
 pcb_status launch_mod_words(const uint32_t* a, int aw, size_t count, const uint32_t* v_norm, int s, int shift,
                             uint32_t* out, cudaStream_t stream);
+pcb_status launch_mul_add1(const uint32_t* a, int aw, const uint32_t* b, int bw, size_t count, uint32_t* out,
+                           cudaStream_t stream);
 pcb_status launch_combined_update(const uint64_t* qa, const uint64_t* qb, const uint64_t* qz, const uint64_t* qnv,
                                   size_t rows, size_t cols, uint64_t* out, cudaStream_t stream);
 pcb_status launch_inverse_x(const uint64_t* q, const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
@@ -1521,6 +1523,8 @@ struct pcb_share {  // an edge's CrtShare (paillier.hpp:64-66): p^2 and phi(p^2)
   RnsXModulus md;
   uint32_t* d_phi = nullptr;  // phi(p^2) normalised for the device long division (exponent reduction)
   int phi_words = 0, phi_shift = 0;
+  uint32_t* d_p2n = nullptr;  // p^2 normalised likewise (the binomial form's final reduction)
+  int p2_shift = 0;
 };
 extern "C" {
 
@@ -1546,6 +1550,10 @@ pcb_status pcb_share_create(pcb_share** out, int device, const uint32_t* p2, uin
     const std::vector<uint32_t> vn = (sh->phi << (size_t)sh->phi_shift).limbs(sh->phi_words);
     if (cudaMalloc(&sh->d_phi, vn.size() * 4) != cudaSuccess) return PCB_E_ALLOC;
     if (cudaMemcpy(sh->d_phi, vn.data(), vn.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
+    sh->p2_shift = (int)(32 * sh->S - sh->p2.bit_length());
+    const std::vector<uint32_t> pn = (sh->p2 << (size_t)sh->p2_shift).limbs(sh->S);
+    if (cudaMalloc(&sh->d_p2n, pn.size() * 4) != cudaSuccess) return PCB_E_ALLOC;
+    if (cudaMemcpy(sh->d_p2n, pn.data(), pn.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
   } catch (const std::bad_alloc&) {
     return PCB_E_ALLOC;
   } catch (...) {
@@ -1560,6 +1568,7 @@ void pcb_share_destroy(pcb_share* sh) {
   cudaSetDevice(sh->device);
   rnsx_free(&sh->md);
   if (sh->d_phi) cudaFree(sh->d_phi);
+  if (sh->d_p2n) cudaFree(sh->d_p2n);
   delete sh;
 }
 
@@ -1600,6 +1609,40 @@ pcb_status pcb_delegated_power(pcb_share* sh, const uint32_t* base, uint32_t bas
   scratch_free(er, st);
   const bool any_host = sb.host || so.host || sx.host;
   unstage(&sb, st);
+  unstage(&sx, st);
+  unstage(&so, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  return e;
+}
+
+// delegated_power (protocol.cpp:15-18) of the binomial generator g = n + 1 for every element:
+// g^(obf mod phi(p^2)) mod p^2 = 1 + (obf mod phi(p^2)) n mod p^2, because n^2 = 0 mod p^2 -- the same
+// collapse the reference uses for g_power_half (paillier.cpp:259-263).  Exponent reduction, one
+// (PW x L)-word product and one reduction mod p^2 instead of a 2048-bit exponentiation; the result
+// is bit-identical to pcb_delegated_power(base = n + 1, obf).
+pcb_status pcb_delegated_power_binomial(pcb_share* sh, const uint32_t* n, uint32_t n_limbs, const uint32_t* obf,
+                                        uint32_t obf_limbs, size_t count, uint32_t* out, pcb_stream stream) {
+  PCB_RANGE("pcb_delegated_power_binomial");
+  if (!sh || !n || !n_limbs || (count && (!obf || !out)) || !obf_limbs) return PCB_E_SHAPE;
+  if (count == 0) return PCB_OK;
+  if (cudaSetDevice(sh->device) != cudaSuccess) return PCB_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = sh->S, PW = sh->phi_words, NL = (int)n_limbs;
+  Staged sn, so, sx;
+  uint32_t *er = nullptr, *pr = nullptr;
+  pcb_status e = stage_in(n, (size_t)NL * 4, st, &sn);
+  if (!e) e = stage_in(obf, count * obf_limbs * 4, st, &sx);
+  if (!e) e = stage_out(out, count * S * 4, st, &so);
+  if (!e) e = scratch_alloc(count * PW * 4, (void**)&er, st);
+  if (!e) e = scratch_alloc(count * (size_t)(PW + NL) * 4, (void**)&pr, st);
+  if (!e) e = launch_mod_words((const uint32_t*)sx.dev, (int)obf_limbs, count, sh->d_phi, PW, sh->phi_shift, er, st);
+  if (!e) e = launch_mul_add1(er, PW, (const uint32_t*)sn.dev, NL, count, pr, st);
+  if (!e) e = launch_mod_words(pr, PW + NL, count, sh->d_p2n, S, sh->p2_shift, (uint32_t*)so.dev, st);
+  if (!e) e = unstage_out(out, &so, st);
+  scratch_free(er, st);
+  scratch_free(pr, st);
+  const bool any_host = sn.host || so.host || sx.host;
+  unstage(&sn, st);
   unstage(&sx, st);
   unstage(&so, st);
   if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;

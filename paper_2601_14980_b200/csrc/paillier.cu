@@ -696,6 +696,40 @@ pcb_status launch_mod_words(const uint32_t* a, int aw, size_t count, const uint3
   return cuda_check(cudaGetLastError());
 }
 
+// out_i = a_i * b + 1 (a_i: aw words per element, b: bw words shared, out: aw + bw words), schoolbook
+// per thread -- the binomial collapse of a delegated g power (pcb_delegated_power_binomial)
+__global__ void mul_add1_kernel(const uint32_t* a, int aw, const uint32_t* b, int bw, int count, uint32_t* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    const uint32_t* x = a + (size_t)i * aw;
+    uint32_t* o = out + (size_t)i * (aw + bw);
+    for (int k = 0; k < aw + bw; k++) o[k] = 0;
+    for (int u = 0; u < aw; u++) {
+      const uint64_t xu = x[u];
+      if (!xu) continue;
+      uint64_t carry = 0;
+      for (int v = 0; v < bw; v++) {
+        const uint64_t t = xu * b[v] + o[u + v] + carry;
+        o[u + v] = (uint32_t)t;
+        carry = t >> 32;
+      }
+      o[u + bw] = (uint32_t)carry;
+    }
+    uint64_t c = 1;
+    for (int k = 0; k < aw + bw && c; k++) {
+      const uint64_t t = (uint64_t)o[k] + c;
+      o[k] = (uint32_t)t;
+      c = t >> 32;
+    }
+  }
+}
+
+pcb_status launch_mul_add1(const uint32_t* a, int aw, const uint32_t* b, int bw, size_t count, uint32_t* out,
+                           cudaStream_t stream) {
+  mul_add1_kernel<<<small_grid(count), 128, 0, stream>>>(a, aw, b, bw, (int)count, out);
+  count_launch();
+  return cuda_check(cudaGetLastError());
+}
+
 // obfuscate_exponent (protocol.cpp:11-13): out = value + mask * n_eps, per element (value: vw words,
 // mask: u64, n_eps: nw words shared, out: ow words, ow >= nw + 3)
 __global__ void obfuscate_kernel(const uint32_t* value, int vw, const uint64_t* mask, const uint32_t* neps, int nw,

@@ -626,6 +626,16 @@ class CrtShare:
                                                base.shape[0], L.ptr(out), stream), "delegated_power")
         return out
 
+    def delegated_power_binomial_tensor(self, n_limbs, obf, stream=None):
+        """delegated_power with base g = n + 1 for every element (n_limbs: the n limbs, a device
+        tensor or host array): 1 + (obf mod phi(p^2)) n mod p^2, no exponentiation, same bits."""
+        torch = _torch()
+        out = torch.empty((obf.shape[0], self.S), dtype=torch.int32, device=obf.device)
+        _raise_for(L.lib().pcb_delegated_power_binomial(self._h, L.ptr(n_limbs), n_limbs.shape[-1], L.ptr(obf),
+                                                        obf.shape[1], obf.shape[0], L.ptr(out), stream),
+                   "delegated_power_binomial")
+        return out
+
     def delegated_power_batch(self, base, obf):
         """base: (count, <= 2S) limbs, obf: (count, k) limbs -> (count, S) limbs of
         (base mod p^2)^(obf mod phi(p^2)) mod p^2."""

@@ -191,3 +191,28 @@ def test_collab_session_masks_exponents_and_ledger():
         a, y, factors=fac, spec=spec)
     for t in range(iters):
         assert res.x_trace[t].tolist() == basic.x_trace[t].tolist()
+
+
+def test_binomial_delegated_power_equals_the_exponentiation(key2048):
+    """pcb_delegated_power_binomial (g = n + 1: 1 + (obf mod phi(p^2)) n mod p^2) is bit-identical to
+    the generic delegated_power (protocol.cpp:15-18) for masked, bare and edge exponents."""
+    import torch
+
+    kp, _ = key2048
+    share = P.crt_share(kp)
+    n, p2 = kp.n, kp.p * kp.p
+    eps = _lcm(kp.p - 1, kp.q - 1)
+    phi = p2 - kp.p
+    rnd = random.Random(23)
+    obfs = [rnd.getrandbits(60) + rnd.getrandbits(64) * n * eps for _ in range(200)]
+    obfs += [0, 1, phi, phi - 1, phi + 1, 5 * phi, n * eps, rnd.getrandbits(60)]
+    ow = max(o.bit_length() for o in obfs) // 32 + 1
+    O = torch.from_numpy(L.ints_to_limbs(obfs, ow).view(np.int32)).cuda()
+    W = 2 * share.S
+    G = torch.from_numpy(np.tile(L.int_to_limbs(n + 1, W), (len(obfs), 1)).view(np.int32)).cuda()
+    nd = torch.from_numpy(L.int_to_limbs(n, (n.bit_length() + 31) // 32).view(np.int32)).cuda()
+    got = share.delegated_power_binomial_tensor(nd, O)
+    want = share.delegated_power_tensor(G, O)
+    assert torch.equal(got, want)
+    vals = L.limbs_to_ints(got.cpu().numpy().view(np.uint32))
+    assert vals == [pow(n + 1, o % phi, p2) for o in obfs]
