@@ -257,8 +257,18 @@ R28Mod r28_mod(const HBN& m, int rb, int n) {
   return c;
 }
 
-constexpr int kWindow = 5;
-constexpr int kTab = 1 << (kWindow - 1);
+// Sliding-window width of the fixed-exponent schedules (table of 2^(w-1) odd powers per element).
+// PCB_WINDOW overrides it for A/B runs (1..6), read once per process before any context exists.
+int window_width() {
+  static const int w = [] {
+    const char* v = getenv("PCB_WINDOW");
+    const int x = v ? atoi(v) : 5;
+    return x >= 1 && x <= 6 ? x : 5;
+  }();
+  return w;
+}
+#define kWindow (window_width())
+#define kTab (1 << (kWindow - 1))
 
 }  // namespace pcb
 
