@@ -1356,6 +1356,15 @@ pcb_status launch_cfg(const RnsXModulus& md, int mode, const uint8_t* ops, int n
   P.cl = cl;
   int blocks = units < nsm ? units : nsm;
   if (cl == 2) blocks = std::min((units + 1) & ~1, nsm & ~1);
+  {
+    // PCB_RNSX_NP (A/B): bit 0 = step programs, bit 1 = every other mode, launched one unit per
+    // CTA (grid = units) instead of persistent: the block scheduler then hands SMs freed by a
+    // concurrent kernel (another stream) to whichever CTAs are pending, instead of a static
+    // blockIdx + k gridDim split that waits for the slowest SM.
+    const char* npv = getenv("PCB_RNSX_NP");
+    const int np = npv ? atoi(npv) : 0;
+    if (cl == 1 && (np & (mode == kRxProg ? 1 : 2))) blocks = units;
+  }
   const size_t nthr = (size_t)blocks * C::NCT;
   pcb_status e = PCB_OK;
   P.tab = nullptr;
