@@ -319,6 +319,21 @@ pcb_status pcb_decrypt_update_blocks_async(pcb_ctx* ctx, size_t nblocks, const u
                                            double z_max, double delta, double kappa, double* x,
                                            double* z, double* v, int32_t* err_dev, pcb_stream stream);
 
+/* The master's own CRT half of Paillier::decrypt_with_half (paillier.cpp:366) on its own:
+ * q2_half (count x S words, S = the CRT half width) = (c mod q^2)^(eps mod phi(q^2)) mod q^2.
+ * It needs only c, so the master can run it while the edge computes the p^2 side
+ * (delegated_power); device pointers, no host synchronisation. */
+pcb_status pcb_decrypt_half_q(pcb_ctx* ctx, const uint32_t* c, size_t count, uint32_t* q2_half, pcb_stream stream);
+
+/* pcb_decrypt_update_blocks_half without host synchronisation (errors into *err_dev as above).
+ * q2_half: nullable; the pcb_decrypt_half_q output for the same c, else it is computed here. */
+pcb_status pcb_decrypt_update_blocks_half_async(pcb_ctx* ctx, size_t nblocks, const uint32_t* sizes,
+                                                const uint32_t* c, const uint32_t* p2_power,
+                                                const uint32_t* q2_half, const uint64_t* rowsum,
+                                                const uint64_t* q_z, const uint64_t* q_nv, double z_min,
+                                                double z_max, double delta, double kappa, double* x,
+                                                double* z, double* v, int32_t* err_dev, pcb_stream stream);
+
 /* ---- wire format (interop with the reference's SimCarrier / TcpCarrier sessions) ---------- */
 
 /* put_cipher_vec (wire.cpp:125-132) on the device: u32 BE count, then per element u32 BE byte

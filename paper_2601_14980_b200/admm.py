@@ -493,6 +493,7 @@ class EncryptedSession(ShardedDriver):
         # owns no block (world > nodes): it still advances the shared r stream each iteration
         self.pstream = torch.cuda.Stream(device=self.device, priority=0)  # least priority (offline work)
         self.mstream = torch.cuda.Stream(device=self.device, priority=-1)  # critical path
+        self.qstream = torch.cuda.Stream(device=self.device, priority=-1)  # collab: the master's own Dec half
         self.rn_ready = [torch.cuda.Event() for _ in range(2)]
         self.enc_done = torch.cuda.Event()
         self.rall = torch.empty((2 * sum(self.sizes), self.L), dtype=torch.int32, device=self.dev)
@@ -767,12 +768,20 @@ class EncryptedSession(ShardedDriver):
                 self.edge._ctx, len(sz), sz.ctypes.data, L.ptr(self.alpha_hat), L.ptr(self.expo), self.expo_bits,
                 L.ptr(ct[:n]), L.ptr(ct[n:]), cfg.window, L.ptr(upd), L.ptr(self.err), st), "edge step")
             if cfg.variant == "collab":  # edge: delegated Dec powers; master: decrypt_with_half + update
+                # The master's own CRT half of decrypt_with_half needs only the update ciphertexts,
+                # so it runs on its own stream while the edge computes the p^2 side (same results;
+                # the edge's update is simply consumed before its delegated powers arrive).
+                yq = torch.empty((n, self.master.crt_half_words()), dtype=torch.int32, device=self.dev)
+                self.qstream.wait_stream(cur)
+                _raise_for(self.lib.pcb_decrypt_half_q(self.master._ctx, L.ptr(upd), n, L.ptr(yq),
+                                                       C.c_void_p(self.qstream.cuda_stream)), "decrypt_with_half (q)")
                 px = self._collab_dec_powers(upd)
                 self._wait_end(ev)
-                _raise_for(self.lib.pcb_decrypt_update_blocks_half(
-                    self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(px), L.ptr(self.rowsum),
+                cur.wait_stream(self.qstream)
+                _raise_for(self.lib.pcb_decrypt_update_blocks_half_async(
+                    self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(px), L.ptr(yq), L.ptr(self.rowsum),
                     L.ptr(q[:n]), L.ptr(q[n:]), spec[0], spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
-                    L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), None, st), "master update (collab)")
+                    L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), L.ptr(self.err), st), "master update (collab)")
             else:
                 self._wait_end(ev)
                 if not cfg.use_crt:  # decrypt_vec(use_crt = false): one full each (paillier.cpp:345-350)

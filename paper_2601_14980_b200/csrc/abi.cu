@@ -1496,20 +1496,29 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
 
 // ---- collaborative variant (paper Alg. 3) ---------------------------------------
 }  // extern "C"
-// device core of decrypt_with_half: c (count x 2L), pw (count x 2L: the p-half, any representative)
+// the master's own CRT half of decrypt_with_half: yq = (c mod q^2)^(eps mod phi(q^2)) mod q^2
+// (paillier.cpp:366); it needs only c, so a caller may run it while the edge computes the p side
+static pcb_status dwh_q(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* yq, cudaStream_t st) {
+  const int S = x->S;
+  const double mm = 2.0 * S * S + S;
+  return launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_epsq, x->len_epsq, kTab, c, 2 * (int)x->L, nullptr, 0, count,
+                     yq, st, ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm);
+}
+
+// device core of decrypt_with_half: c (count x 2L), pw (count x 2L: the p-half, any representative);
+// yq_pre (nullable): the q side already computed by dwh_q
 static pcb_status dwh_core(pcb_ctx* x, const uint32_t* c, const uint32_t* pw, size_t count, uint32_t* m, int32_t* stv,
-                           cudaStream_t st) {
+                           cudaStream_t st, const uint32_t* yq_pre) {
   const int S = x->S, L2 = 2 * (int)x->L;
   uint32_t *yp = nullptr, *yq = nullptr;
   pcb_status e = scratch_alloc(count * S * 4, (void**)&yp, st);
-  if (!e) e = scratch_alloc(count * S * 4, (void**)&yq, st);
+  if (!e && !yq_pre) e = scratch_alloc(count * S * 4, (void**)&yq, st);
   if (!e) e = launch_dec_prep(c, x->d_n2, (int)x->L, stv, count, st);  // c < n^2 (paillier.cpp:365)
   const double mm = 2.0 * S * S + S;
   // p side: p2_power mod p^2 (reference: mod(p2_power, crt_.p2)); q side: c^(eps mod phi(q^2)) mod q^2
   if (!e) e = launch_rnsx(x->rx_p, kRxDec, x->d_sched + x->off_one, x->len_one, kTab, pw, L2, nullptr, 0, count, yp, st, mm);
-  if (!e)
-    e = launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_epsq, x->len_epsq, kTab, c, L2, nullptr, 0, count, yq, st,
-                    ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm);
+  if (!e && !yq_pre) e = dwh_q(x, c, count, yq, st);
+  if (yq_pre) yq = const_cast<uint32_t*>(yq_pre);
   if (!e && S == 32)
     e = launch_dec_finish<32>(*reinterpret_cast<const CrtDecConsts<32>*>(x->half_blob.data()), yp, yq, stv, m,
                               (int)x->L, count, st);
@@ -1523,7 +1532,7 @@ static pcb_status dwh_core(pcb_ctx* x, const uint32_t* c, const uint32_t* pw, si
     e = launch_dec_finish<128>(*reinterpret_cast<const CrtDecConsts<128>*>(x->half_blob.data()), yp, yq, stv, m,
                               (int)x->L, count, st);
   scratch_free(yp, st);
-  scratch_free(yq, st);
+  if (!yq_pre) scratch_free(yq, st);
   return e;
 }
 struct pcb_share {  // an edge's CrtShare (paillier.hpp:64-66): p^2 and phi(p^2) only
@@ -1683,7 +1692,7 @@ pcb_status pcb_decrypt_with_half(pcb_ctx* x, const uint32_t* c, const uint32_t* 
   if (!e)
     e = cuda_check(cudaMemcpy2DAsync(pw, L2 * 4, sp.dev, pw_limbs * 4, pw_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
   (void)S;
-  if (!e) e = dwh_core(x, (const uint32_t*)sc.dev, pw, count, (uint32_t*)sm.dev, stv, st);
+  if (!e) e = dwh_core(x, (const uint32_t*)sc.dev, pw, count, (uint32_t*)sm.dev, stv, st, nullptr);
   if (!e) e = unstage_out(m, &sm, st);
   if (!e) e = unstage_out(status, &ss, st);
   if (!e && !status) e = first_failure(stv, count, st);
@@ -2325,7 +2334,8 @@ pcb_status pcb_edge_step_blocks(pcb_ctx* x, size_t nblocks, const uint32_t* size
 
 extern "C++" {
 static pcb_status dwh_core(pcb_ctx* x, const uint32_t* c, const uint32_t* pw, size_t count, uint32_t* m, int32_t* stv,
-                           cudaStream_t st);
+                           cudaStream_t st, const uint32_t* yq_pre);
+static pcb_status dwh_q(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* yq, cudaStream_t st);
 }
 static pcb_status update_entry(pcb_ctx* x, size_t nblk, const uint32_t* sizes, const uint32_t* c,
                                const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv, double z_min,
@@ -2364,7 +2374,7 @@ static pcb_status update_entry(pcb_ctx* x, size_t nblk, const uint32_t* sizes, c
   Staged sp;
   if (p2pow && !x->has_rx) e = e ? e : PCB_E_UNSUPPORTED;
   if (!e && p2pow) e = stage_in(p2pow, count * 2 * x->L * 4, st, &sp);
-  if (!e) e = p2pow ? dwh_core(x, (const uint32_t*)sc.dev, (const uint32_t*)sp.dev, count, m, stv, st)  // collaborative
+  if (!e) e = p2pow ? dwh_core(x, (const uint32_t*)sc.dev, (const uint32_t*)sp.dev, count, m, stv, st, nullptr)  // collaborative
                     : dec_core(x, (const uint32_t*)sc.dev, count, m, stv, st);
   if (!e)
     e = launch_update(m, (int)x->L, (const uint64_t*)sr.dev, (const uint64_t*)sz.dev, (const uint64_t*)sn.dev, z_min,
@@ -2545,6 +2555,61 @@ pcb_status pcb_decrypt_update_blocks_async(pcb_ctx* x, size_t nblk, const uint32
   scratch_free(m, st);
   scratch_free(segd, st);
   if (!e) x->pow_half += 2 * (uint64_t)count;
+  return e;
+}
+
+pcb_status pcb_decrypt_half_q(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* q2_half, pcb_stream stream) {
+  PCB_RANGE("pcb_decrypt_half_q");
+  if (!x || (count && (!c || !q2_half))) return PCB_E_SHAPE;
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (!x->has_rx) return PCB_E_UNSUPPORTED;
+  if (count == 0) return PCB_OK;
+  if (!is_device_ptr(c) || !is_device_ptr(q2_half)) return PCB_E_SHAPE;
+  if (auto e = set_device(x)) return e;
+  const pcb_status e = dwh_q(x, c, count, q2_half, (cudaStream_t)stream);
+  if (!e) x->pow_half += (uint64_t)count;  // the q half of decrypt_with_half
+  return e;
+}
+
+pcb_status pcb_decrypt_update_blocks_half_async(pcb_ctx* x, size_t nblk, const uint32_t* sizes, const uint32_t* c,
+                                                const uint32_t* p2_power, const uint32_t* q2_half,
+                                                const uint64_t* rowsum, const uint64_t* q_z, const uint64_t* q_nv,
+                                                double z_min, double z_max, double delta, double kappa, double* xo,
+                                                double* zo, double* vo, int32_t* err_dev, pcb_stream stream) {
+  PCB_RANGE("pcb_decrypt_update_blocks_half_async");
+  if (!x || (nblk && !sizes) || !err_dev) return PCB_E_SHAPE;
+  std::vector<long long> seg(nblk + 1, 0);
+  for (size_t k = 0; k < nblk; k++) seg[k + 1] = seg[k] + sizes[k];
+  const size_t count = (size_t)seg[nblk];
+  if (count && (!c || !p2_power || !rowsum || !q_z || !q_nv || !xo || !zo || !vo)) return PCB_E_SHAPE;
+  if (!std::isfinite(z_min) || !std::isfinite(z_max) || !(z_max > z_min) || !(delta >= 1.0) || delta > 9.0e15)
+    return PCB_E_SHAPE;
+  if (!x->has_prv) return PCB_E_NO_PRIVATE;
+  if (!x->has_rx) return PCB_E_UNSUPPORTED;
+  if (count == 0) return PCB_OK;
+  if (count > 0x7fffffffu) return PCB_E_SHAPE;
+  for (const void* p : {(const void*)c, (const void*)p2_power, (const void*)rowsum, (const void*)q_z,
+                        (const void*)q_nv, (const void*)xo, (const void*)zo, (const void*)vo, (const void*)err_dev})
+    if (!is_device_ptr(p)) return PCB_E_SHAPE;
+  if (q2_half && !is_device_ptr(q2_half)) return PCB_E_SHAPE;
+  if (auto e = set_device(x)) return e;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* m = nullptr;
+  int32_t* stv = nullptr;
+  long long* segd = nullptr;
+  pcb_status e = scratch_alloc(count * 4, (void**)&stv, st);
+  if (!e) e = scratch_alloc(count * x->L * 4, (void**)&m, st);
+  if (!e) e = scratch_alloc(seg.size() * 8, (void**)&segd, st);
+  if (!e) e = cuda_check(cudaMemcpyAsync(segd, seg.data(), seg.size() * 8, cudaMemcpyHostToDevice, st));
+  if (!e) e = dwh_core(x, c, p2_power, count, m, stv, st, q2_half);
+  if (!e)
+    e = launch_update(m, (int)x->L, rowsum, q_z, q_nv, z_min, z_max, delta, kappa, xo, zo, vo, stv, count, segd,
+                      (int)nblk, st);
+  if (!e) e = launch_status_flag(stv, count, err_dev, st);
+  scratch_free(stv, st);
+  scratch_free(m, st);
+  scratch_free(segd, st);
+  if (!e && !q2_half) x->pow_half += (uint64_t)count;
   return e;
 }
 

@@ -225,6 +225,16 @@ class Paillier:
     def has_private(self) -> bool:
         return self._has_prv
 
+    def crt_half_words(self) -> int:
+        """u32 words per element of a CRT half on the device (the context's S: the kernel width
+        that holds p^2, q^2 and n), e.g. pcb_decrypt_half_q's output row."""
+        l2 = (max((self._p * self._p).bit_length(), (self._q * self._q).bit_length()) + 31) // 32
+        need = max(l2, self.L)
+        for w in (32, 64, 96, 128):
+            if need <= w:
+                return w
+        raise ValueError("no CRT half width for this key")
+
     def counters(self) -> tuple[int, int]:
         """(pow_full, pow_half) — pcadmm::OpCount (paillier.hpp:84-87)."""
         a, b = C.c_uint64(), C.c_uint64()

@@ -216,3 +216,29 @@ def test_binomial_delegated_power_equals_the_exponentiation(key2048):
     assert torch.equal(got, want)
     vals = L.limbs_to_ints(got.cpu().numpy().view(np.uint32))
     assert vals == [pow(n + 1, o % phi, p2) for o in obfs]
+
+
+def test_decrypt_half_q_is_the_masters_crt_half(key2048):
+    """pcb_decrypt_half_q = (c mod q^2)^(eps mod phi(q^2)) mod q^2 (paillier.cpp:366), the half the
+    collaborative session computes while the edge works on the p^2 side."""
+    import torch
+
+    kp, _ = key2048
+    ph = P.Paillier(kp)
+    n, p, q = kp.n, kp.p, kp.q
+    q2 = q * q
+    e = _lcm(p - 1, q - 1) % (q2 - q)
+    rnd = random.Random(23)
+    count = 130  # two tiles, the second ragged
+    cs = [rnd.randrange(1, n * n) for _ in range(count - 2)] + [1, n * n - 1]
+    W, S = 2 * ph.L, ph.crt_half_words()
+    c = torch.from_numpy(L.ints_to_limbs(cs, W).view(np.int32)).cuda()
+    yq = torch.zeros((count, S), dtype=torch.int32, device="cuda")
+    f0, h0 = ph.counters()
+    assert L.lib().pcb_decrypt_half_q(ph._ctx, L.ptr(c), count, L.ptr(yq), None) == 0
+    torch.cuda.synchronize()
+    got = L.limbs_to_ints(yq.cpu().numpy().view(np.uint32))
+    assert got == [pow(x % q2, e, q2) for x in cs]
+    assert ph.counters() == (f0, h0 + count)  # one half per element
+    # host pointers are refused (device-only asynchronous form)
+    assert L.lib().pcb_decrypt_half_q(ph._ctx, c.cpu().numpy().ctypes.data, count, L.ptr(yq), None) != 0
