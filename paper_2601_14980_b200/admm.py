@@ -598,9 +598,9 @@ class EncryptedSession(ShardedDriver):
             _raise_for(self.lib.pcb_sample_r(self.pre._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
                        "sample_r")
             self.rng_r.state = s_.value
-            if self.n_own and self.cfg.variant == "collab":
-                self.rn[slot][:, : self.L].copy_(self.rall.index_select(0, self.rperm))  # r itself (Enc is online)
-            elif self.n_own:
+            # both variants: rn = r^n mod n^2, data-independent, so it is computed here, off the
+            # critical path (the collaborative finish_split_encrypt then takes it as its factor)
+            if self.n_own:
                 r_in = self.rall.index_select(0, self.rperm).contiguous()
                 _raise_for(self.lib.pcb_encrypt(self.pre._ctx, L.ptr(self.m0), 1, L.ptr(r_in), r_in.shape[0],
                                                 L.ptr(self.rn[slot]), 1 if self.cfg.use_crt else 0,
@@ -653,14 +653,12 @@ class EncryptedSession(ShardedDriver):
             gp = self.share.delegated_power_binomial_tensor(self.n_dev, self.obf_buf, st)
         self._wait_end(ev)
         self.delegated_pows += n2
-        if self.cfg.r_mode == "pooled":  # finish_split_encrypt_with_factor (protocol.cpp:401-403)
-            _raise_for(self.lib.pcb_finish_split_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(gp), gp.shape[1],
-                                                            L.ptr(r), n2, L.ptr(ct), L.ptr(self.st_enc), st),
-                       "finish_split_encrypt_with_factor")
-        else:
-            _raise_for(self.lib.pcb_finish_split_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(gp), gp.shape[1],
-                                                         L.ptr(r), n2, L.ptr(ct), L.ptr(self.st_enc), st),
-                       "finish_split_encrypt")
+        # r: the factor r^n mod n^2 (pooled: protocol.cpp:401-403; fresh: finish_split_encrypt with r,
+        # paillier.cpp:402-414, whose two r half_pows ran -- and were counted -- in the offline
+        # precompute, _precompute), so the online step is finish_split_encrypt_with_factor
+        _raise_for(self.lib.pcb_finish_split_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(gp), gp.shape[1],
+                                                        L.ptr(r), n2, L.ptr(ct), L.ptr(self.st_enc), st),
+                   "finish_split_encrypt_with_factor")
         if self.capture is not None:
             self.capture.setdefault("obf", []).append(self.obf_buf.clone())
         return ct
@@ -733,7 +731,7 @@ class EncryptedSession(ShardedDriver):
         cur.wait_event(self.rn_ready[slot])
         n = self.n_own
         clamps = 0
-        if n and cfg.variant != "collab" and cfg.r_mode == "fresh":
+        if n and cfg.r_mode == "fresh":
             self.bad |= self.st_pre[slot].ne(0).any().to(torch.int32)
         if n:
             lo = self.own_lo
@@ -745,8 +743,7 @@ class EncryptedSession(ShardedDriver):
                 q = self._quantize_async(vin, spec)
             ct = torch.empty((2 * n, W), dtype=torch.int32, device=self.dev)
             if cfg.variant == "collab":
-                rr = self.rn[slot] if cfg.r_mode == "pooled" else self.rn[slot][:, : self.L].contiguous()
-                ct = self._collab_encrypt(q, rr, ct)
+                ct = self._collab_encrypt(q, self.rn[slot], ct)
                 self.bad |= self.st_enc.ne(0).any().to(torch.int32)
             else:
                 _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(self.rn[slot]), 2 * n,

@@ -185,8 +185,9 @@ def test_collab_session_masks_exponents_and_ledger():
                 assert obf[n_tot + o + i] == int(q[n_tot + o + i]) + masks[2 * o + c + i] * n_eps
             o += c
     # ledger
-    full, half = sess.master.counters()
-    assert half == 5 * n_tot * iters and sess.delegated_pows == 3 * n_tot * iters
+    # the master role = its online context + the offline r^n precompute (the 2 x 2 r halves)
+    assert res.master.pow_half == 5 * n_tot * iters and sess.delegated_pows == 3 * n_tot * iters
+    assert res.edges.delegated_pows == 3 * n_tot * iters
     basic = ADMM.EncryptedSession(keys, ADMM.SessionConfig(nodes=2, iters=iters, seed=seed)).run(
         a, y, factors=fac, spec=spec)
     for t in range(iters):
