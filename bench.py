@@ -114,9 +114,9 @@ def run_admm(args, rank: int, world: int, local: int):
 
     a, y = gen_problem_fast(512, 4096, 0.1, 1)
     keys = P.keygen(P.Rng(KEY_SEED), 2048)
-    # one extra untimed iteration at the end: every timed iteration then also runs the offline
-    # half of the next one (steady state), as in a long session
-    iters = args.admm_warmup + args.admm_iters + 1
+    # untimed iterations at the end: every timed iteration then also runs the offline half of a
+    # later one (steady state), as in a long session
+    iters = args.admm_warmup + args.admm_iters + ADMM.pre_ahead()
     cfg = ADMM.SessionConfig(nodes=8, iters=iters)
     group = dist.group.WORLD if world > 1 else None
     sess = ADMM.EncryptedSession(keys, cfg, device=local, rank=rank, world=world, group=group)
@@ -168,7 +168,7 @@ def run_admm_collab(args, rank: int, world: int, local: int):
 
     a, y = gen_problem_fast(512, 4096, 0.1, 1)
     keys = P.keygen(P.Rng(KEY_SEED), 2048)
-    iters = args.admm_warmup + args.admm_collab_iters + 1
+    iters = args.admm_warmup + args.admm_collab_iters + ADMM.pre_ahead()
     cfg = ADMM.SessionConfig(nodes=8, iters=iters, variant="collab")
     group = dist.group.WORLD if world > 1 else None
     sess = ADMM.EncryptedSession(keys, cfg, device=local, rank=rank, world=world, group=group)
@@ -259,7 +259,7 @@ def run_cfg5(args, rank: int, world: int, local: int):
     x[idx] = torch.randn(6554, dtype=torch.float64, device="cuda", generator=g)
     y = a @ x
     keys = P.keygen(P.Rng(KEY_SEED), 2048)
-    iters = args.admm_warmup + args.cfg5_iters + 1
+    iters = args.admm_warmup + args.cfg5_iters + ADMM.pre_ahead()
     cfg = ADMM.SessionConfig(nodes=64, iters=iters)
     group = dist.group.WORLD if world > 1 else None
     sess = ADMM.EncryptedSession(keys, cfg, device=local, rank=rank, world=world, group=group)

@@ -494,13 +494,20 @@ class EncryptedSession(ShardedDriver):
         self.pstream = torch.cuda.Stream(device=self.device, priority=0)  # least priority (offline work)
         self.mstream = torch.cuda.Stream(device=self.device, priority=-1)  # critical path
         self.qstream = torch.cuda.Stream(device=self.device, priority=-1)  # collab: the master's own Dec half
-        self.rn_ready = [torch.cuda.Event() for _ in range(2)]
+        # the offline r^n runs pre_ahead() iterations ahead: 2 (default) queues it behind the edge
+        # step, so it fills the SMs the latency-bound decryption leaves idle (three rn slots;
+        # profiles/r02_pre_ahead_ab.txt); PCB_PRE_AHEAD=1: the next iteration's, beside the edge step
+        self.pre_ahead = pre_ahead()
+        nslot = self.pre_ahead + 1
+        self.nslot = nslot
+        self.edge_done = torch.cuda.Event()
+        self.rn_ready = [torch.cuda.Event() for _ in range(nslot)]
         self.enc_done = torch.cuda.Event()
         self.rall = torch.empty((2 * sum(self.sizes), self.L), dtype=torch.int32, device=self.dev)
-        self.rn = [torch.empty((2 * n_own, 2 * self.L), dtype=torch.int32, device=self.dev) for _ in range(2)]
+        self.rn = [torch.empty((2 * n_own, 2 * self.L), dtype=torch.int32, device=self.dev) for _ in range(nslot)]
         # per-element statuses of the asynchronous encryptions, checked once per iteration after
         # the update's own stream synchronisation (no extra host sync on the critical path)
-        self.st_pre = [torch.zeros(2 * n_own, dtype=torch.int32, device=self.dev) for _ in range(2)]
+        self.st_pre = [torch.zeros(2 * n_own, dtype=torch.int32, device=self.dev) for _ in range(nslot)]
         self.st_enc = torch.zeros(2 * n_own, dtype=torch.int32, device=self.dev)
         self.bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
         # asynchronous iteration (pcb_*_async): first failing element's code, clamps on the device
@@ -583,6 +590,8 @@ class EncryptedSession(ShardedDriver):
 
         ps = self.pstream
         ps.wait_event(self.enc_done)  # the slot was last read by an earlier online encryption
+        if self.pre_ahead == 2 and self._edge_launched:
+            ps.wait_event(self.edge_done)
         with torch.cuda.stream(ps):
             st = C.c_void_p(ps.cuda_stream)
             if self.cfg.r_mode == "pooled":
@@ -724,9 +733,12 @@ class EncryptedSession(ShardedDriver):
         import torch
 
         cfg, spec, st = self.cfg, self.spec, self._stream()
-        slot = t % 2
+        slot = t % self.nslot
         if t == 0:
+            self._edge_launched = False
             self._precompute(slot)
+            if self.pre_ahead == 2 and cfg.iters > 1:
+                self._precompute(1)
         cur = torch.cuda.current_stream(self.device)
         cur.wait_event(self.rn_ready[slot])
         n = self.n_own
@@ -755,8 +767,8 @@ class EncryptedSession(ShardedDriver):
         if not n and cfg.variant == "collab":
             draw_masks(self.mask_rng, 2 * sum(self.sizes), cfg.mask_bits)  # keep the shared mask stream in step
         self.enc_done.record(cur)
-        if t + 1 < cfg.iters:
-            self._precompute(1 - slot)
+        if self.pre_ahead == 1 and t + 1 < cfg.iters:
+            self._precompute((t + 1) % self.nslot)
         if n:
             upd = torch.empty((n, W), dtype=torch.int32, device=self.dev)
             sz = self.own_sizes
@@ -764,6 +776,8 @@ class EncryptedSession(ShardedDriver):
             _raise_for(self.lib.pcb_edge_step_blocks_async(
                 self.edge._ctx, len(sz), sz.ctypes.data, L.ptr(self.alpha_hat), L.ptr(self.expo), self.expo_bits,
                 L.ptr(ct[:n]), L.ptr(ct[n:]), cfg.window, L.ptr(upd), L.ptr(self.err), st), "edge step")
+            self.edge_done.record(cur)
+            self._edge_launched = True
             if cfg.variant == "collab":  # edge: delegated Dec powers; master: decrypt_with_half + update
                 # The master's own CRT half of decrypt_with_half needs only the update ciphertexts,
                 # so it runs on its own stream while the edge computes the p^2 side (same results;
@@ -788,10 +802,18 @@ class EncryptedSession(ShardedDriver):
                     self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(self.rowsum), L.ptr(q[:n]),
                     L.ptr(q[n:]), spec[0], spec[1], spec[2], self.kappa, L.ptr(self.x[lo:lo + n]),
                     L.ptr(self.z[lo:lo + n]), L.ptr(self.v[lo:lo + n]), L.ptr(self.err), st), "master update")
+        if self.pre_ahead == 2 and t + 2 < cfg.iters:
+            self._precompute((t + 2) % self.nslot)
         return clamps
 
 
 # ---- faithful trust: the private key on rank 0 only (north_star 5) -------------
+
+def pre_ahead() -> int:
+    """How many iterations ahead EncryptedSession computes the offline r^n (PCB_PRE_AHEAD, 1 or 2):
+    a run's last pre_ahead() iterations have no precompute left to overlap."""
+    return 1 if os.environ.get("PCB_PRE_AHEAD") == "1" else 2
+
 
 def rank_slice(total: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous near-equal slice [offset, offset + count) of `total` items for `rank` (the first
