@@ -159,6 +159,13 @@ pcb_status pcb_delegated_power(pcb_share* share, const uint32_t* base, uint32_t 
  * bit-identical to pcb_delegated_power(base = n + 1, obf) without the exponentiation. */
 pcb_status pcb_delegated_power_binomial(pcb_share* share, const uint32_t* n, uint32_t n_limbs, const uint32_t* obf,
                                         uint32_t obf_limbs, size_t count, uint32_t* out, pcb_stream stream);
+/* The same for exponents that are multiples of p - 1, e_i = u_i (p - 1) with 0 < u_i < p (half_pow
+ * with w = 0, paillier.cpp:275-305): out_i = 1 + p (L_p(base_i^(p-1) mod p^2) u_i mod p), or 0 when
+ * p | base_i -- one |p|-bit chain instead of a |p^2|-bit one; bit-identical to pcb_delegated_power
+ * with obf_i = e_i.  The collaborative session's obf_dec = eps (1 + mask n) reduces to this form.
+ * u_mont: count x (p^2 words / 2), u_i R mod p with R = 2^(16 x p^2 words).  2048/3072-bit keys. */
+pcb_status pcb_delegated_power_fermat(pcb_share* share, const uint32_t* base, uint32_t base_limbs,
+                                      const uint32_t* u_mont, size_t count, uint32_t* out, pcb_stream stream);
 
 /* out_i = value_i + mask_i * n_eps — obfuscate_exponent (protocol.cpp:11-13), the master's masked
  * exponents for the edges' delegated powers.  value: count x value_limbs, mask: count u64 (draw_mask,
@@ -319,10 +326,13 @@ pcb_status pcb_decrypt_update_blocks_async(pcb_ctx* ctx, size_t nblocks, const u
                                            double z_max, double delta, double kappa, double* x,
                                            double* z, double* v, int32_t* err_dev, pcb_stream stream);
 
-/* The master's own CRT half of Paillier::decrypt_with_half (paillier.cpp:366) on its own:
- * q2_half (count x S words, S = the CRT half width) = (c mod q^2)^(eps mod phi(q^2)) mod q^2.
- * It needs only c, so the master can run it while the edge computes the p^2 side
- * (delegated_power); device pointers, no host synchronisation. */
+/* The master's own CRT half of Paillier::decrypt_with_half (paillier.cpp:366) on its own: the q^2
+ * chain, q2_half (count x S words, S = the CRT half width).  eps mod phi(q^2) = u (q - 1), so for
+ * u != 0 (every key but toy ones) the chain is c^(q-1) mod q^2 and the factor u is applied in the
+ * finish (half_pow, paillier.cpp:275-305); else (c mod q^2)^(eps mod phi(q^2)) mod q^2.  An
+ * intermediate for pcb_decrypt_update_blocks_half_async on the same context.  It needs only c, so
+ * the master can run it while the edge computes the p^2 side (delegated_power); device pointers,
+ * no host synchronisation. */
 pcb_status pcb_decrypt_half_q(pcb_ctx* ctx, const uint32_t* c, size_t count, uint32_t* q2_half, pcb_stream stream);
 
 /* pcb_decrypt_update_blocks_half without host synchronisation (errors into *err_dev as above).

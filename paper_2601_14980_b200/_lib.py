@@ -109,6 +109,7 @@ SIGNATURES = {
                                              _vp, _vp]),
     "pcb_decrypt_update_blocks_async": (C.c_int, [_vp, C.c_size_t, _vp, _vp, _vp, _vp, _vp, C.c_double, C.c_double,
                                                   C.c_double, C.c_double, _vp, _vp, _vp, _vp, _vp]),
+    "pcb_delegated_power_fermat": (C.c_int, [_vp, _vp, C.c_uint32, _vp, C.c_size_t, _vp, _vp]),
     "pcb_decrypt_half_q": (C.c_int, [_vp, _vp, C.c_size_t, _vp, _vp]),
     "pcb_decrypt_update_blocks_half_async": (C.c_int, [_vp, C.c_size_t, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                                        C.c_double, C.c_double, C.c_double, C.c_double, _vp, _vp,

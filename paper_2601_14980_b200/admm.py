@@ -632,6 +632,13 @@ class EncryptedSession(ShardedDriver):
         for k in self.mine:  # each edge's obf_dec, repeated over its block's rows
             rows.append(np.tile(L.int_to_limbs(self.obf_dec[k], self.ow), (self.sizes[k], 1)))
         self.obf_dec_rows = torch.from_numpy(np.concatenate(rows).view(np.int32)).to(self.dev) if rows else None
+        # obf_dec = eps (1 + mask n) is a multiple of p - 1: the edges' Dec powers take the Fermat form
+        # (one |p|-bit chain, pcb_delegated_power_fermat), bit-identical to the generic power
+        fac = [self.share.fermat_factor(self.obf_dec[k]) for k in self.mine]
+        self.u_mont_rows = None
+        if rows and all(f is not None for f in fac) and os.environ.get("PCB_COLLAB_GENERIC_DEC") != "1":
+            self.u_mont_rows = torch.from_numpy(np.concatenate(
+                [np.tile(f, (self.sizes[k], 1)) for f, k in zip(fac, self.mine)]).view(np.int32)).to(self.dev)
         self.obf_buf = torch.empty((2 * n, self.ow), dtype=torch.int32, device=self.dev)
 
     def _iteration_masks(self):
@@ -709,7 +716,10 @@ class EncryptedSession(ShardedDriver):
         import torch
 
         n = upd.shape[0]
-        px = self.share.delegated_power_tensor(upd, self.obf_dec_rows, self._stream())
+        if self.u_mont_rows is not None:
+            px = self.share.delegated_power_fermat_tensor(upd, self.u_mont_rows, self._stream())
+        else:
+            px = self.share.delegated_power_tensor(upd, self.obf_dec_rows, self._stream())
         self.delegated_pows += n
         full = torch.zeros((n, 2 * self.L), dtype=torch.int32, device=self.dev)
         full[:, : px.shape[1]] = px

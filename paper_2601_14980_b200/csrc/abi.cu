@@ -287,6 +287,10 @@ struct pcb_ctx {
   int off_dec_p = 0, len_dec_p = 0, off_dec_q = 0, len_dec_q = 0;
   int off_epsq = 0, len_epsq = 0, off_one = 0, len_one = 0;  // eps mod phi(q^2); e = 1
   std::vector<uint8_t> half_blob;  // CrtDecConsts with h_p = q^-1 mu mod p, h_q = p^-1 mu mod q
+  // eps mod phi(q^2) = u (q - 1) (eps is a multiple of q - 1): decrypt_with_half's q side is then
+  // c^(q-1) mod q^2 (the Dec chain) with u folded into h_q (half_pow, paillier.cpp:275-305)
+  std::vector<uint8_t> half_blob_u;
+  bool half_fold = false;
   int off_pub = 0, len_pub = 0;  // exponent n at n^2 (direct encryption)
   uint32_t* d_n = nullptr;       // n (L limbs), n^2 (2L limbs) for the argument checks
   uint32_t* d_n2 = nullptr;
@@ -339,6 +343,9 @@ pcb_status launch_garner(const CrtEncConsts<S>& k, const uint32_t* cp, const uin
 template <int S>
 pcb_status launch_dec_finish(const CrtDecConsts<S>& k, const uint32_t* xp, const uint32_t* xq, int32_t* st,
                              uint32_t* m, int L, size_t count, cudaStream_t stream);
+template <int S>
+pcb_status launch_fermat_finish(const ModCtx<S / 2>& sp, const uint32_t* pinv_lo, const uint32_t* p,
+                                const uint32_t* s, const uint32_t* u, uint32_t* out, size_t count, cudaStream_t stream);
 pcb_status launch_enc_prep(const uint32_t* m, int m_limbs, const double* v, double zmin, double zmax, double delta,
                            int fine, uint32_t* m_out, int m_out_limbs, uint64_t* q_out, unsigned long long* clamps,
                            const uint32_t* r, const uint32_t* n_dev, int L, int32_t* st, size_t count,
@@ -461,6 +468,22 @@ void build_half(pcb_ctx* x) {
     mod(mod(inv * mu, pr) * RH, pr).to_limbs(side ? k.hq : k.hp, H);
   }
   x->half_blob.assign(reinterpret_cast<uint8_t*>(&k), reinterpret_cast<uint8_t*>(&k) + sizeof(k));
+  // x_q = c^(eps mod phi(q^2)) mod q^2 with eps mod phi(q^2) = u (q - 1), u != 0: x_q = s^u for
+  // s = c^(q-1) mod q^2 = 1 + q L_q(s), so L_q(x_q) = u L_q(s) mod q and the finish may run on s with
+  // h_q u.  (s = 0 iff q | c, and then x_q = 0 too: the same PCB_E_NOT_UNIT.)  u = 0 (toy keys
+  // only) keeps the direct power, whose c^0 = 1 differs from s^0 when q | c.
+  {
+    const HBN q2 = x->q * x->q, qm1 = x->q - HBN(1);
+    HBN u, w;
+    divmod(mod(eps, q2 - x->q), qm1, u, w);
+    if (w.is_zero() && !u.is_zero()) {
+      HBN inv;
+      if (!mod_inverse(mod(x->p, x->q), x->q, inv)) throw std::invalid_argument("p and q share a factor");
+      mod(mod(mod(inv * mu, x->q) * u, x->q) * RH, x->q).to_limbs(k.hq, H);
+      x->half_blob_u.assign(reinterpret_cast<uint8_t*>(&k), reinterpret_cast<uint8_t*>(&k) + sizeof(k));
+      x->half_fold = true;
+    }
+  }
 }
 
 pcb_status set_device(const pcb_ctx* x) { return cuda_check(cudaSetDevice(x->device)); }
@@ -1501,6 +1524,9 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
 static pcb_status dwh_q(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* yq, cudaStream_t st) {
   const int S = x->S;
   const double mm = 2.0 * S * S + S;
+  if (x->half_fold)  // c^(q-1) mod q^2; the factor u of the exponent is folded into the finish (build_half)
+    return launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_dec_q, x->len_dec_q, kTab, c, 2 * (int)x->L, nullptr, 0,
+                       count, yq, st, ((double)(x->nbits / 2) + (double)((x->nbits / 2 + 3) / 4)) * mm);
   return launch_rnsx(x->rx_q, kRxDec, x->d_sched + x->off_epsq, x->len_epsq, kTab, c, 2 * (int)x->L, nullptr, 0, count,
                      yq, st, ((double)x->nbits + (double)((x->nbits + 3) / 4)) * mm);
 }
@@ -1520,16 +1546,16 @@ static pcb_status dwh_core(pcb_ctx* x, const uint32_t* c, const uint32_t* pw, si
   if (!e && !yq_pre) e = dwh_q(x, c, count, yq, st);
   if (yq_pre) yq = const_cast<uint32_t*>(yq_pre);
   if (!e && S == 32)
-    e = launch_dec_finish<32>(*reinterpret_cast<const CrtDecConsts<32>*>(x->half_blob.data()), yp, yq, stv, m,
+    e = launch_dec_finish<32>(*reinterpret_cast<const CrtDecConsts<32>*>((x->half_fold ? x->half_blob_u : x->half_blob).data()), yp, yq, stv, m,
                               (int)x->L, count, st);
   if (!e && S == 64)
-    e = launch_dec_finish<64>(*reinterpret_cast<const CrtDecConsts<64>*>(x->half_blob.data()), yp, yq, stv, m,
+    e = launch_dec_finish<64>(*reinterpret_cast<const CrtDecConsts<64>*>((x->half_fold ? x->half_blob_u : x->half_blob).data()), yp, yq, stv, m,
                               (int)x->L, count, st);
   if (!e && S == 96)
-    e = launch_dec_finish<96>(*reinterpret_cast<const CrtDecConsts<96>*>(x->half_blob.data()), yp, yq, stv, m,
+    e = launch_dec_finish<96>(*reinterpret_cast<const CrtDecConsts<96>*>((x->half_fold ? x->half_blob_u : x->half_blob).data()), yp, yq, stv, m,
                               (int)x->L, count, st);
   if (!e && S == 128)
-    e = launch_dec_finish<128>(*reinterpret_cast<const CrtDecConsts<128>*>(x->half_blob.data()), yp, yq, stv, m,
+    e = launch_dec_finish<128>(*reinterpret_cast<const CrtDecConsts<128>*>((x->half_fold ? x->half_blob_u : x->half_blob).data()), yp, yq, stv, m,
                               (int)x->L, count, st);
   scratch_free(yp, st);
   if (!yq_pre) scratch_free(yq, st);
@@ -1544,7 +1570,32 @@ struct pcb_share {  // an edge's CrtShare (paillier.hpp:64-66): p^2 and phi(p^2)
   int phi_words = 0, phi_shift = 0;
   uint32_t* d_p2n = nullptr;  // p^2 normalised likewise (the binomial form's final reduction)
   int p2_shift = 0;
+  // pcb_delegated_power_fermat: p = p^2 - phi(p^2), the p - 1 exponent schedule and the mod-p
+  // constants of the finish (ModCtx<S/2>, p^-1 mod 2^(16 S), p), by kernel width
+  uint8_t* d_ops_pm1 = nullptr;
+  int len_pm1 = 0;
+  std::vector<uint8_t> fermat_blob;
 };
+
+template <int S>
+struct FermatConsts {
+  ModCtx<S / 2> sp;
+  uint32_t pinv_lo[S / 2];
+  uint32_t p[S / 2];
+};
+
+template <int S>
+static void build_fermat(pcb_share* sh, const HBN& p) {
+  constexpr int H = S / 2;
+  FermatConsts<S> k;
+  std::memset(&k, 0, sizeof(k));
+  fill_mod<H>(k.sp, p);
+  HBN t;
+  if (!mod_inverse(p, HBN(1) << (32 * H), t)) throw std::invalid_argument("even p");
+  t.to_limbs(k.pinv_lo, H);
+  p.to_limbs(k.p, H);
+  sh->fermat_blob.assign(reinterpret_cast<uint8_t*>(&k), reinterpret_cast<uint8_t*>(&k) + sizeof(k));
+}
 extern "C" {
 
 pcb_status pcb_share_create(pcb_share** out, int device, const uint32_t* p2, uint32_t p2_limbs, const uint32_t* phi_p2,
@@ -1573,6 +1624,16 @@ pcb_status pcb_share_create(pcb_share** out, int device, const uint32_t* p2, uin
     const std::vector<uint32_t> pn = (sh->p2 << (size_t)sh->p2_shift).limbs(sh->S);
     if (cudaMalloc(&sh->d_p2n, pn.size() * 4) != cudaSuccess) return PCB_E_ALLOC;
     if (cudaMemcpy(sh->d_p2n, pn.data(), pn.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
+    // the Fermat form (pcb_delegated_power_fermat) when phi = p^2 - p for a p with p^2 = p2
+    const HBN p = sh->p2 - sh->phi;
+    if (p * p == sh->p2 && (sh->S == 64 || sh->S == 96)) {
+      const std::vector<uint8_t> ops = build_ops(p - HBN(1), kWindow);
+      if (cudaMalloc(&sh->d_ops_pm1, ops.size()) != cudaSuccess) return PCB_E_ALLOC;
+      if (cudaMemcpy(sh->d_ops_pm1, ops.data(), ops.size(), cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
+      sh->len_pm1 = (int)ops.size();
+      if (sh->S == 64) build_fermat<64>(sh.get(), p);
+      else build_fermat<96>(sh.get(), p);
+    }
   } catch (const std::bad_alloc&) {
     return PCB_E_ALLOC;
   } catch (...) {
@@ -1588,7 +1649,55 @@ void pcb_share_destroy(pcb_share* sh) {
   rnsx_free(&sh->md);
   if (sh->d_phi) cudaFree(sh->d_phi);
   if (sh->d_p2n) cudaFree(sh->d_p2n);
+  if (sh->d_ops_pm1) cudaFree(sh->d_ops_pm1);
   delete sh;
+}
+
+// delegated_power for exponents that are multiples of p - 1 (half_pow with w = 0, paillier.cpp:275-305):
+// out_i = (base_i mod p^2)^(u_i (p - 1)) mod p^2 = 1 + p (L_p(s_i) u_i mod p) with s_i = base_i^(p-1)
+// mod p^2 (0 when p | base_i) -- one |p|-bit chain instead of a |p^2|-bit one.  u_mont: count x S/2
+// words, u_i R mod p (R = 2^(16 S)), u_i != 0.  The collaborative session's obf_dec = eps (1 + mask n)
+// is such an exponent (protocol.cpp:11-13, 352-353).
+pcb_status pcb_delegated_power_fermat(pcb_share* sh, const uint32_t* base, uint32_t base_limbs, const uint32_t* u_mont,
+                                      size_t count, uint32_t* out, pcb_stream stream) {
+  PCB_RANGE("pcb_delegated_power_fermat");
+  if (!sh || (count && (!base || !u_mont || !out)) || base_limbs == 0 || base_limbs > (uint32_t)(2 * sh->S))
+    return PCB_E_SHAPE;
+  if (!sh->d_ops_pm1) return PCB_E_UNSUPPORTED;
+  if (count == 0) return PCB_OK;
+  if (cudaSetDevice(sh->device) != cudaSuccess) return PCB_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int S = sh->S, W = 2 * S, H = S / 2;
+  Staged sb, su, so;
+  uint32_t *bw = nullptr, *sv = nullptr;
+  pcb_status e = stage_in(base, count * base_limbs * 4, st, &sb);
+  if (!e) e = stage_in(u_mont, count * H * 4, st, &su);
+  if (!e) e = stage_out(out, count * S * 4, st, &so);
+  if (!e) e = scratch_alloc(count * W * 4, (void**)&bw, st);
+  if (!e) e = scratch_alloc(count * S * 4, (void**)&sv, st);
+  if (!e) e = cuda_check(cudaMemset2DAsync(bw, W * 4, 0, W * 4, count, st));
+  if (!e) e = cuda_check(cudaMemcpy2DAsync(bw, W * 4, sb.dev, base_limbs * 4, base_limbs * 4, count, cudaMemcpyDeviceToDevice, st));
+  const double mm = 2.0 * S * S + S;
+  const double bits = (double)(sh->p2.bit_length() / 2);
+  if (!e) e = launch_rnsx(sh->md, kRxDec, sh->d_ops_pm1, sh->len_pm1, kTab, bw, W, nullptr, 0, count, sv, st,
+                          (bits + (bits + 3) / 4) * mm);
+  if (!e && S == 64) {
+    const auto& k = *reinterpret_cast<const FermatConsts<64>*>(sh->fermat_blob.data());
+    e = launch_fermat_finish<64>(k.sp, k.pinv_lo, k.p, sv, (const uint32_t*)su.dev, (uint32_t*)so.dev, count, st);
+  }
+  if (!e && S == 96) {
+    const auto& k = *reinterpret_cast<const FermatConsts<96>*>(sh->fermat_blob.data());
+    e = launch_fermat_finish<96>(k.sp, k.pinv_lo, k.p, sv, (const uint32_t*)su.dev, (uint32_t*)so.dev, count, st);
+  }
+  if (!e) e = unstage_out(out, &so, st);
+  scratch_free(bw, st);
+  scratch_free(sv, st);
+  const bool any_host = sb.host || su.host || so.host;
+  unstage(&sb, st);
+  unstage(&su, st);
+  unstage(&so, st);
+  if (any_host && cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+  return e;
 }
 
 // delegated_power (protocol.cpp:15-18): out_i = (base_i mod p^2)^(obf_i mod phi(p^2)) mod p^2.

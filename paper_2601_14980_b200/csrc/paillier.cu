@@ -578,6 +578,73 @@ pcb_status launch_dec_finish(const CrtDecConsts<S>& k, const uint32_t* xp, const
   return cuda_check(cudaGetLastError());
 }
 
+// half_pow for exponents e = u (p - 1) (paillier.cpp:275-305 with w = 0): with s = b^(p-1) mod p^2,
+// b^e mod p^2 = s^u = 1 + p (L_p(s) u mod p) when p does not divide b (s = 1 + p L_p(s)), and 0 when
+// it does (then s = 0: p^2 | b^(p-1), and u >= 1).  u comes per element in Montgomery form u R_h mod p.
+template <int S>
+struct FermatArgs {
+  ModCtx<S / 2> sp;        // p
+  uint32_t pinv_lo[S / 2]; // p^-1 mod 2^(16 S)
+  uint32_t p[S / 2];
+  const uint32_t* s;       // count x S: b^(p-1) mod p^2
+  const uint32_t* u;       // count x S/2: u R_h mod p
+  uint32_t* out;           // count x S: b^(u (p - 1)) mod p^2
+  int count;
+};
+
+template <int S>
+__global__ void __launch_bounds__(kThreadsPerBlock) fermat_finish_kernel(const __grid_constant__ FermatArgs<S> P) {
+  constexpr int H = S / 2;
+  extern __shared__ __align__(16) uint32_t smem[];
+  smod_fill<H>(smem, P.sp.m);
+  __syncthreads();
+  const SMod<H> Sp{smem_addr(smem), P.sp.minv};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* slots = smem + H;
+  const Slot<H> A{smem_addr(slots + warp * (64 * H) + lane * 4)};
+  const Slot<H> B{smem_addr(slots + warp * (64 * H) + 32 * H + lane * 4)};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.count; i += gridDim.x * blockDim.x) {
+    const uint32_t* si = P.s + (size_t)i * S;
+    uint32_t* out = P.out + (size_t)i * S;
+    uint32_t K[H];
+    if (!l_half<S>(K, si, P.pinv_lo, P.p, P.u + (size_t)i * H, A, B, Sp)) {
+      for (int j = 0; j < S; j++) out[j] = 0;  // s = 0: p | b
+      continue;
+    }
+    B.store(K);
+    uint32_t one[H], Hi[H];
+#pragma unroll
+    for (int j = 0; j < H; j++) one[j] = j == 0 ? 1u : 0u;
+    mul_add_smod<H>(Hi, one, B, Sp);  // 1 + p K (< p^2)
+#pragma unroll
+    for (int j = 0; j < H; j++) out[j] = B.digit(j);
+#pragma unroll
+    for (int j = 0; j < H; j++) out[H + j] = Hi[j];
+  }
+}
+
+template <int S>
+pcb_status launch_fermat_finish(const ModCtx<S / 2>& sp, const uint32_t* pinv_lo, const uint32_t* p,
+                                const uint32_t* s, const uint32_t* u, uint32_t* out, size_t count, cudaStream_t stream) {
+  constexpr int H = S / 2;
+  FermatArgs<S> P;
+  P.sp = sp;
+  for (int j = 0; j < H; j++) {
+    P.pinv_lo[j] = pinv_lo[j];
+    P.p[j] = p[j];
+  }
+  P.s = s;
+  P.u = u;
+  P.out = out;
+  P.count = (int)count;
+  const size_t smem = (size_t)kThreadsPerBlock * H * 8 + H * 4;
+  int blocks = 0;
+  if (auto e = item_grid(fermat_finish_kernel<S>, smem, count, &blocks)) return e;
+  fermat_finish_kernel<S><<<blocks, kThreadsPerBlock, smem, stream>>>(P);
+  count_launch();
+  return cuda_check(cudaGetLastError());
+}
+
 // combined_quantized_update (quantize.cpp:66-82) on the device: q_i = qa_i + sum_j qb_ij (qz_j + qnv_j)
 // in u128 (wrapping like the reference's u128 arithmetic), one row per thread
 __global__ void combined_update_kernel(const uint64_t* qa, const uint64_t* qb, const uint64_t* qz, const uint64_t* qnv,
@@ -765,7 +832,9 @@ pcb_status launch_obfuscate(const uint32_t* value, int vw, const uint64_t* mask,
   template pcb_status launch_garner<S>(const CrtEncConsts<S>&, const uint32_t*, const uint32_t*, const int32_t*,  \
                                        uint32_t*, int, size_t, cudaStream_t);                                      \
   template pcb_status launch_dec_finish<S>(const CrtDecConsts<S>&, const uint32_t*, const uint32_t*, int32_t*,    \
-                                           uint32_t*, int, size_t, cudaStream_t);
+                                           uint32_t*, int, size_t, cudaStream_t);                                  \
+  template pcb_status launch_fermat_finish<S>(const ModCtx<S / 2>&, const uint32_t*, const uint32_t*,             \
+                                              const uint32_t*, const uint32_t*, uint32_t*, size_t, cudaStream_t);
 PCB_INSTANTIATE(32)
 PCB_INSTANTIATE(64)
 PCB_INSTANTIATE(96)

@@ -636,6 +636,25 @@ class CrtShare:
                                                base.shape[0], L.ptr(out), stream), "delegated_power")
         return out
 
+    def delegated_power_fermat_tensor(self, base, u_mont, stream=None):
+        """Device tensors: base (count, <= 2S), u_mont (count, S/2: u R mod p) -> (count, S) tensor of
+        (base mod p^2)^(u (p - 1)) mod p^2 (pcb_delegated_power_fermat: one |p|-bit chain)."""
+        torch = _torch()
+        out = torch.empty((base.shape[0], self.S), dtype=torch.int32, device=base.device)
+        _raise_for(L.lib().pcb_delegated_power_fermat(self._h, L.ptr(base), base.shape[1], L.ptr(u_mont),
+                                                      base.shape[0], L.ptr(out), stream), "delegated_power_fermat")
+        return out
+
+    def fermat_factor(self, obf: int):
+        """(u R mod p) limbs when obf mod phi(p^2) = u (p - 1) with u != 0 (the Fermat form), else None."""
+        p = self.p2 - self.phi_p2
+        if p * p != self.p2 or self.S % 2:
+            return None
+        u, w = divmod(int(obf) % self.phi_p2, p - 1)
+        if w or not u:
+            return None
+        return L.int_to_limbs(u * (1 << (16 * self.S)) % p, self.S // 2)
+
     def delegated_power_binomial_tensor(self, n_limbs, obf, stream=None):
         """delegated_power with base g = n + 1 for every element (n_limbs: the n limbs, a device
         tensor or host array): 1 + (obf mod phi(p^2)) n mod p^2, no exponentiation, same bits."""

@@ -220,8 +220,9 @@ def test_binomial_delegated_power_equals_the_exponentiation(key2048):
 
 
 def test_decrypt_half_q_is_the_masters_crt_half(key2048):
-    """pcb_decrypt_half_q = (c mod q^2)^(eps mod phi(q^2)) mod q^2 (paillier.cpp:366), the half the
-    collaborative session computes while the edge works on the p^2 side."""
+    """pcb_decrypt_half_q: the q^2 chain of decrypt_with_half (paillier.cpp:366), which the
+    collaborative session runs while the edge works on the p^2 side.  eps mod phi(q^2) = u (q - 1), so
+    the chain is c^(q-1) mod q^2 and u is folded into the finish (half_pow, paillier.cpp:275-305)."""
     import torch
 
     kp, _ = key2048
@@ -239,7 +240,42 @@ def test_decrypt_half_q_is_the_masters_crt_half(key2048):
     assert L.lib().pcb_decrypt_half_q(ph._ctx, L.ptr(c), count, L.ptr(yq), None) == 0
     torch.cuda.synchronize()
     got = L.limbs_to_ints(yq.cpu().numpy().view(np.uint32))
-    assert got == [pow(x % q2, e, q2) for x in cs]
+    u, w = divmod(e, q - 1)
+    assert w == 0 and u != 0
+    assert got == [pow(x % q2, q - 1, q2) for x in cs]
+    assert [1 + q * ((((g - 1) // q) * u) % q) if g else 0 for g in got] == [pow(x % q2, e, q2) for x in cs]
     assert ph.counters() == (f0, h0 + count)  # one half per element
     # host pointers are refused (device-only asynchronous form)
     assert L.lib().pcb_decrypt_half_q(ph._ctx, c.cpu().numpy().ctypes.data, count, L.ptr(yq), None) != 0
+
+
+def test_delegated_power_fermat_equals_generic(key2048):
+    """pcb_delegated_power_fermat (one |p|-bit chain + 1 + p (L_p(s) u mod p)) == pcb_delegated_power
+    for exponents u (p - 1), the form of the collaborative obf_dec = eps (1 + mask n); bases include
+    multiples of p (result 0) and 1."""
+    import torch
+
+    kp, _ = key2048
+    share = P.crt_share(kp)
+    p, q, n = kp.p, kp.q, kp.n
+    p2 = p * p
+    eps = _lcm(p - 1, q - 1)
+    rnd = random.Random(29)
+    count = 140
+    bases = [rnd.randrange(1, n * n) for _ in range(count - 4)] + [p, 3 * p * q, 1, n * n - 1]
+    obfs = [eps * (1 + rnd.getrandbits(64) * n) for _ in range(count)]
+    W, S = 2 * share.S, share.S
+    B = torch.from_numpy(L.ints_to_limbs(bases, W).view(np.int32)).cuda()
+    facs = [share.fermat_factor(o) for o in obfs]
+    assert all(f is not None for f in facs)
+    U = torch.from_numpy(np.stack(facs).view(np.int32)).cuda()
+    got = L.limbs_to_ints(share.delegated_power_fermat_tensor(B, U).cpu().numpy().view(np.uint32))
+    ow = max((o.bit_length() + 31) // 32 for o in obfs)
+    O = torch.from_numpy(L.ints_to_limbs(obfs, ow).view(np.int32)).cuda()
+    ref = L.limbs_to_ints(share.delegated_power_tensor(B, O).cpu().numpy().view(np.uint32))
+    torch.cuda.synchronize()
+    assert got == ref
+    assert got[:3] == [pow(b % p2, o % (p2 - p), p2) for b, o in zip(bases[:3], obfs[:3])]
+    assert got[count - 4] == 0 and got[count - 3] == 0 and got[count - 2] == 1
+    # an exponent that is not a multiple of p - 1 has no Fermat form
+    assert share.fermat_factor(eps + 1) is None
