@@ -984,9 +984,11 @@ class FaithfulGpuBackend:
         return C.c_void_p(torch.cuda.current_stream(self.dev_index).cuda_stream)
 
     def sync(self):
+        """The critical path (the current stream, which the collectives join), not the offline
+        precompute on its own stream: the phase timers measure what the master waits on."""
         import torch
 
-        torch.cuda.synchronize(self.device)
+        torch.cuda.current_stream(self.device).synchronize()
 
     def setup_edges(self, mine, factors, sizes, spec, cfg):
         import torch
@@ -1057,6 +1059,20 @@ class FaithfulGpuBackend:
                                             None, st), "make_rn_factor")
             self.adj_full += P  # make_rn_factor's full (paillier.cpp:376)
             self.pool_at = 0
+        else:
+            # fresh r: rn = r^n mod n^2 of the next iteration computed offline on a low-priority
+            # stream and context (as EncryptedSession), the online Enc is one multiplication
+            self.pre = Paillier(self.keys, device=self.dev_index)
+            _raise_for(self.lib.pcb_ctx_set_priority(self.pre._ctx, 0), "priority")
+            _raise_for(self.lib.pcb_ctx_set_priority(self.master._ctx, 1), "priority")
+            self.pstream = torch.cuda.Stream(device=self.device, priority=0)
+            self.rn = [torch.empty((2 * n, self.width), dtype=torch.int32, device=self.device) for _ in range(2)]
+            self.st_pre = [torch.zeros(2 * n, dtype=torch.int32, device=self.device) for _ in range(2)]
+            self.pre_bad = torch.zeros((), dtype=torch.int32, device=self.device)
+            self.m0 = torch.zeros((2 * n, 1), dtype=torch.int32, device=self.device)
+            self.rn_ready = [torch.cuda.Event() for _ in range(2)]
+            self.enc_done = torch.cuda.Event()
+            self.enc_done.record(torch.cuda.current_stream(self.device))
 
     def master_encrypt(self, z, v, t):
         import torch
@@ -1074,14 +1090,37 @@ class FaithfulGpuBackend:
             _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(rn), vin.numel(), L.ptr(ct),
                                                L.ptr(self.st_enc), st), "enc_state")
         else:
+            slot = t % 2
+            if t == 0:
+                self._precompute(slot)
+            cur = torch.cuda.current_stream(self.device)
+            cur.wait_event(self.rn_ready[slot])
+            self.pre_bad |= self.st_pre[slot].ne(0).any().to(torch.int32)
+            _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(self.rn[slot]), vin.numel(),
+                                               L.ptr(ct), L.ptr(self.st_enc), st), "enc_state")
+            self.enc_done.record(cur)
+            if t + 1 < self.cfg.iters:
+                self._precompute(1 - slot)
+        return ct, q
+
+    def _precompute(self, slot):
+        """The offline half of an iteration's enc_state (crt_encrypt_with_r, protocol.cpp:410): draw the
+        master r stream in reference order, rn = Enc(0; r) = r^n mod n^2 on the low-priority stream."""
+        import torch
+
+        ps = self.pstream
+        ps.wait_event(self.enc_done)  # the slot was last read by the previous online encryption
+        with torch.cuda.stream(ps):
+            st = C.c_void_p(ps.cuda_stream)
             s_ = C.c_uint64(self.rng_r.state)
-            _raise_for(self.lib.pcb_sample_r(self.master._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
+            _raise_for(self.lib.pcb_sample_r(self.pre._ctx, C.byref(s_), self.rall.shape[0], L.ptr(self.rall), st),
                        "sample_r")
             self.rng_r.state = s_.value
             r = self.rall.index_select(0, self.rperm).contiguous()
-            _raise_for(self.lib.pcb_encrypt(self.master._ctx, L.ptr(q), 2, L.ptr(r), vin.numel(), L.ptr(ct),
-                                            1 if self.cfg.use_crt else 0, L.ptr(self.st_enc), st), "enc_state")
-        return ct, q
+            _raise_for(self.lib.pcb_encrypt(self.pre._ctx, L.ptr(self.m0), 1, L.ptr(r), r.shape[0],
+                                            L.ptr(self.rn[slot]), 1 if self.cfg.use_crt else 0,
+                                            L.ptr(self.st_pre[slot]), st), "offline encryption")
+            self.rn_ready[slot].record(ps)
 
     def edge_step(self, mine, sizes, offs, ct):
         import torch
@@ -1102,6 +1141,9 @@ class FaithfulGpuBackend:
         """Ledgers as EncryptedSession.role_stats: the master's on rank 0, each rank's edges."""
         if rank == 0:
             f, h = self.master.counters()
+            if hasattr(self, "pre"):  # the offline r^n context (fresh r)
+                f2, h2 = self.pre.counters()
+                f, h = f + f2, h + h2
             res.master = RoleStats(f + self.adj_full, h + self.adj_half, 0)
         fe, he = self.edge.counters()
         res.edges = RoleStats(fe, he, 0)
@@ -1121,7 +1163,7 @@ class FaithfulGpuBackend:
         code = int(self.err.item())
         if code:
             _raise_for(code, f"iteration {t}")
-        if int(self.st_enc.ne(0).any().item()):
+        if int(self.st_enc.ne(0).any().item()) or (hasattr(self, "pre_bad") and int(self.pre_bad.item())):
             raise ValueError("encryption argument out of range (crt_encrypt_with_r, paillier.cpp:322-323)")
         total = int(self.clamps_dev.sum().item())
         new, self.clamps_seen = total - self.clamps_seen, total
