@@ -583,7 +583,7 @@ def main() -> None:
     ap.add_argument("--admm-faithful-iters", type=int, default=3, help="timed faithful-trust cfg3 iterations (0 = skip)")
     ap.add_argument("--admm-collab-iters", type=int, default=3, help="timed collaborative-variant cfg3 iterations (0 = skip)")
     ap.add_argument("--cfg4-n", type=int, default=1 << 22, help="cfg4 3072-bit values per job, sliced over ranks (0 = skip)")
-    ap.add_argument("--cfg5-iters", type=int, default=0, help="timed cfg5 ADMM iterations (N=65536, 64 blocks; 0 = skip)")
+    ap.add_argument("--cfg5-iters", type=int, default=2, help="timed cfg5 ADMM iterations (N=65536, 64 blocks; 0 = skip)")
     ap.add_argument("--p4096-n", type=int, default=1 << 17, help="Paillier-4096 values per job (0 = skip)")
     args = ap.parse_args()
     args.e2e_steps = max(1, args.e2e_steps)

@@ -163,7 +163,7 @@ pcb_status pcb_delegated_power_binomial(pcb_share* share, const uint32_t* n, uin
  * with w = 0, paillier.cpp:275-305): out_i = 1 + p (L_p(base_i^(p-1) mod p^2) u_i mod p), or 0 when
  * p | base_i -- one |p|-bit chain instead of a |p^2|-bit one; bit-identical to pcb_delegated_power
  * with obf_i = e_i.  The collaborative session's obf_dec = eps (1 + mask n) reduces to this form.
- * u_mont: count x (p^2 words / 2), u_i R mod p with R = 2^(16 x p^2 words).  2048/3072-bit keys. */
+ * u_mont: count x (p^2 words / 2), u_i R mod p with R = 2^(16 x p^2 words).  2048/3072/4096-bit keys. */
 pcb_status pcb_delegated_power_fermat(pcb_share* share, const uint32_t* base, uint32_t base_limbs,
                                       const uint32_t* u_mont, size_t count, uint32_t* out, pcb_stream stream);
 

@@ -1626,13 +1626,14 @@ pcb_status pcb_share_create(pcb_share** out, int device, const uint32_t* p2, uin
     if (cudaMemcpy(sh->d_p2n, pn.data(), pn.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
     // the Fermat form (pcb_delegated_power_fermat) when phi = p^2 - p for a p with p^2 = p2
     const HBN p = sh->p2 - sh->phi;
-    if (p * p == sh->p2 && (sh->S == 64 || sh->S == 96)) {
+    if (p * p == sh->p2 && (sh->S == 64 || sh->S == 96 || sh->S == 128)) {
       const std::vector<uint8_t> ops = build_ops(p - HBN(1), kWindow);
       if (cudaMalloc(&sh->d_ops_pm1, ops.size()) != cudaSuccess) return PCB_E_ALLOC;
       if (cudaMemcpy(sh->d_ops_pm1, ops.data(), ops.size(), cudaMemcpyHostToDevice) != cudaSuccess) return PCB_E_CUDA;
       sh->len_pm1 = (int)ops.size();
       if (sh->S == 64) build_fermat<64>(sh.get(), p);
-      else build_fermat<96>(sh.get(), p);
+      else if (sh->S == 96) build_fermat<96>(sh.get(), p);
+      else build_fermat<128>(sh.get(), p);
     }
   } catch (const std::bad_alloc&) {
     return PCB_E_ALLOC;
@@ -1688,6 +1689,10 @@ pcb_status pcb_delegated_power_fermat(pcb_share* sh, const uint32_t* base, uint3
   if (!e && S == 96) {
     const auto& k = *reinterpret_cast<const FermatConsts<96>*>(sh->fermat_blob.data());
     e = launch_fermat_finish<96>(k.sp, k.pinv_lo, k.p, sv, (const uint32_t*)su.dev, (uint32_t*)so.dev, count, st);
+  }
+  if (!e && S == 128) {
+    const auto& k = *reinterpret_cast<const FermatConsts<128>*>(sh->fermat_blob.data());
+    e = launch_fermat_finish<128>(k.sp, k.pinv_lo, k.p, sv, (const uint32_t*)su.dev, (uint32_t*)so.dev, count, st);
   }
   if (!e) e = unstage_out(out, &so, st);
   scratch_free(bw, st);

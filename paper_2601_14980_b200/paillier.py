@@ -648,7 +648,7 @@ class CrtShare:
     def fermat_factor(self, obf: int):
         """(u R mod p) limbs when obf mod phi(p^2) = u (p - 1) with u != 0 (the Fermat form), else None."""
         p = self.p2 - self.phi_p2
-        if p * p != self.p2 or self.S % 2:
+        if p * p != self.p2 or self.S not in (64, 96, 128):  # the widths pcb_delegated_power_fermat serves
             return None
         u, w = divmod(int(obf) % self.phi_p2, p - 1)
         if w or not u:
