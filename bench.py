@@ -116,7 +116,7 @@ def run_admm(args, rank: int, world: int, local: int):
     keys = P.keygen(P.Rng(KEY_SEED), 2048)
     # untimed iterations at the end: every timed iteration then also runs the offline half of a
     # later one (steady state), as in a long session
-    iters = args.admm_warmup + args.admm_iters + ADMM.pre_ahead()
+    iters = args.admm_warmup + args.admm_iters + ADMM.PRE_AHEAD_MAX
     cfg = ADMM.SessionConfig(nodes=8, iters=iters)
     group = dist.group.WORLD if world > 1 else None
     sess = ADMM.EncryptedSession(keys, cfg, device=local, rank=rank, world=world, group=group)
@@ -171,7 +171,7 @@ def run_admm_collab(args, rank: int, world: int, local: int):
     # one more warm-up iteration than the basic line: the collaborative step runs on three streams,
     # and the stream-ordered scratch pool grows over its first iterations
     wu = args.admm_warmup + 1
-    iters = wu + args.admm_collab_iters + ADMM.pre_ahead()
+    iters = wu + args.admm_collab_iters + ADMM.PRE_AHEAD_MAX
     cfg = ADMM.SessionConfig(nodes=8, iters=iters, variant="collab")
     group = dist.group.WORLD if world > 1 else None
     sess = ADMM.EncryptedSession(keys, cfg, device=local, rank=rank, world=world, group=group)
@@ -262,7 +262,7 @@ def run_cfg5(args, rank: int, world: int, local: int):
     x[idx] = torch.randn(6554, dtype=torch.float64, device="cuda", generator=g)
     y = a @ x
     keys = P.keygen(P.Rng(KEY_SEED), 2048)
-    iters = args.admm_warmup + args.cfg5_iters + ADMM.pre_ahead()
+    iters = args.admm_warmup + args.cfg5_iters + ADMM.PRE_AHEAD_MAX
     cfg = ADMM.SessionConfig(nodes=64, iters=iters)
     group = dist.group.WORLD if world > 1 else None
     sess = ADMM.EncryptedSession(keys, cfg, device=local, rank=rank, world=world, group=group)

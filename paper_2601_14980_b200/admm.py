@@ -494,10 +494,11 @@ class EncryptedSession(ShardedDriver):
         self.pstream = torch.cuda.Stream(device=self.device, priority=0)  # least priority (offline work)
         self.mstream = torch.cuda.Stream(device=self.device, priority=-1)  # critical path
         self.qstream = torch.cuda.Stream(device=self.device, priority=-1)  # collab: the master's own Dec half
-        # the offline r^n runs pre_ahead() iterations ahead: 2 (default) queues it behind the edge
-        # step, so it fills the SMs the latency-bound decryption leaves idle (three rn slots;
-        # profiles/r02_pre_ahead_ab.txt); PCB_PRE_AHEAD=1: the next iteration's, beside the edge step
-        self.pre_ahead = pre_ahead()
+        # the offline r^n runs pre_ahead() iterations ahead: 2 queues it behind the edge step, so it
+        # fills the SMs a latency-bound decryption (fewer tiles than SMs) leaves idle (three rn
+        # slots); 1 runs the next iteration's beside the edge step, better once the decryption fills
+        # the GPU itself (profiles/r02_pre_ahead_ab.txt: cfg3 2, cfg5 1)
+        self.pre_ahead = pre_ahead(n_own, torch.cuda.get_device_properties(self.device).multi_processor_count)
         nslot = self.pre_ahead + 1
         self.nslot = nslot
         self.edge_done = torch.cuda.Event()
@@ -819,10 +820,18 @@ class EncryptedSession(ShardedDriver):
 
 # ---- faithful trust: the private key on rank 0 only (north_star 5) -------------
 
-def pre_ahead() -> int:
-    """How many iterations ahead EncryptedSession computes the offline r^n (PCB_PRE_AHEAD, 1 or 2):
-    a run's last pre_ahead() iterations have no precompute left to overlap."""
-    return 1 if os.environ.get("PCB_PRE_AHEAD") == "1" else 2
+def pre_ahead(n_own: int, nsm: int = 148) -> int:
+    """How many iterations ahead EncryptedSession computes the offline r^n: 2 when the decryption of
+    the n_own rows leaves SMs idle (two CRT halves of ceil(n_own / 128)-element tiles on fewer CTAs
+    than SMs), else 1; PCB_PRE_AHEAD=1/2 forces it.  A run's last pre_ahead() iterations have no
+    precompute left to overlap (bench.py runs PRE_AHEAD_MAX untimed tail iterations)."""
+    env = os.environ.get("PCB_PRE_AHEAD")
+    if env in ("1", "2"):
+        return int(env)
+    return 2 if 2 * ((n_own + 127) // 128) < nsm else 1
+
+
+PRE_AHEAD_MAX = 2
 
 
 def rank_slice(total: int, world: int, rank: int) -> tuple[int, int]:
