@@ -166,6 +166,38 @@ pcb_status first_failure(const int32_t* stv, size_t count, cudaStream_t st) {
   return h == ~0ull ? PCB_OK : (pcb_status)(int32_t)(uint32_t)(h & 0xffffffffu);
 }
 
+// ---- host-buffer pipelining ----------------------------------------------------------------------
+// A large batch whose big arrays are host memory runs in chunks: chunk i+1's host->device copy and
+// chunk i-1's device->host copy run on their own streams while chunk i computes, instead of the
+// whole batch's copies before and after the compute.  The results are the per-chunk calls' on
+// device buffers, i.e. the same bytes.
+constexpr size_t kPipeMin = (size_t)4 * 148 * 256;  // below this a batch runs in one piece
+constexpr size_t kPipeChunks = 4;
+
+struct HostPipe {
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t in[2] = {nullptr, nullptr}, comp[2] = {nullptr, nullptr}, out[2] = {nullptr, nullptr}, start = nullptr;
+  pcb_status init(cudaStream_t st) {
+    if (cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking) != cudaSuccess) return PCB_E_CUDA;
+    if (cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking) != cudaSuccess) return PCB_E_CUDA;
+    for (cudaEvent_t* ev : {&in[0], &in[1], &comp[0], &comp[1], &out[0], &out[1], &start})
+      if (cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess) return PCB_E_CUDA;
+    // the copies follow everything already queued on the caller's stream
+    if (cudaEventRecord(start, st) != cudaSuccess) return PCB_E_CUDA;
+    if (cudaStreamWaitEvent(cin, start, 0) != cudaSuccess || cudaStreamWaitEvent(cout, start, 0) != cudaSuccess)
+      return PCB_E_CUDA;
+    return PCB_OK;
+  }
+  ~HostPipe() {
+    if (cin) cudaStreamSynchronize(cin);
+    if (cout) cudaStreamSynchronize(cout);
+    for (cudaEvent_t ev : {in[0], in[1], comp[0], comp[1], out[0], out[1], start})
+      if (ev) cudaEventDestroy(ev);
+    if (cin) cudaStreamDestroy(cin);
+    if (cout) cudaStreamDestroy(cout);
+  }
+};
+
 // ---- constants ------------------------------------------------------------------------------
 static uint32_t neg_inv32(uint32_t m0) {
   uint32_t inv = 1;
@@ -1492,6 +1524,52 @@ pcb_status pcb_decrypt(pcb_ctx* x, const uint32_t* c, size_t count, uint32_t* m,
   if (count == 0) return PCB_OK;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
+  const bool c_dev = is_device_ptr(c), m_dev = is_device_ptr(m);
+  if (count >= kPipeMin && (!c_dev || !m_dev)) {  // host buffers: chunked, copies beside the compute
+    const size_t WI = 2 * x->L, WO = x->L;
+    const size_t chunk = ((count + kPipeChunks - 1) / kPipeChunks + 255) / 256 * 256;
+    HostPipe hp;
+    pcb_status e = hp.init(st);
+    uint32_t *dc[2] = {nullptr, nullptr}, *dm[2] = {nullptr, nullptr};
+    int32_t* sall = nullptr;
+    for (int b = 0; b < 2 && !e; b++) {
+      if (!c_dev) e = scratch_alloc(chunk * WI * 4, (void**)&dc[b], st);
+      if (!e && !m_dev) e = scratch_alloc(chunk * WO * 4, (void**)&dm[b], st);
+    }
+    if (!e) e = scratch_alloc(count * 4, (void**)&sall, st);
+    if (!e) e = cuda_check(cudaStreamSynchronize(st));  // the scratch exists before the copy streams use it
+    for (size_t i = 0, off = 0; off < count && !e; i++, off += chunk) {
+      const int b = (int)(i & 1);
+      const size_t cnt = std::min(chunk, count - off);
+      const uint32_t* src = c + off * WI;
+      uint32_t* dst = m + off * WO;
+      if (!c_dev) {
+        if (i >= 2) e = cuda_check(cudaStreamWaitEvent(hp.cin, hp.comp[b], 0));
+        if (!e) e = cuda_check(cudaMemcpyAsync(dc[b], src, cnt * WI * 4, cudaMemcpyHostToDevice, hp.cin));
+        if (!e) e = cuda_check(cudaEventRecord(hp.in[b], hp.cin));
+        if (!e) e = cuda_check(cudaStreamWaitEvent(st, hp.in[b], 0));
+        src = dc[b];
+      }
+      if (!m_dev) {
+        if (i >= 2 && !e) e = cuda_check(cudaStreamWaitEvent(st, hp.out[b], 0));
+        dst = dm[b];
+      }
+      if (!e) e = pcb_decrypt(x, src, cnt, dst, use_crt, sall + off, stream);  // device buffers: asynchronous
+      if (!e) e = cuda_check(cudaEventRecord(hp.comp[b], st));
+      if (!m_dev && !e) {
+        e = cuda_check(cudaStreamWaitEvent(hp.cout, hp.comp[b], 0));
+        if (!e) e = cuda_check(cudaMemcpyAsync(m + off * WO, dm[b], cnt * WO * 4, cudaMemcpyDeviceToHost, hp.cout));
+        if (!e) e = cuda_check(cudaEventRecord(hp.out[b], hp.cout));
+      }
+    }
+    if (cudaStreamSynchronize(hp.cout) != cudaSuccess && !e) e = PCB_E_CUDA;
+    if (!e && status) e = cuda_check(cudaMemcpyAsync(status, sall, count * 4, cudaMemcpyDefault, st));
+    if (!e && !status) e = first_failure(sall, count, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+    for (void* p : {(void*)dc[0], (void*)dc[1], (void*)dm[0], (void*)dm[1], (void*)sall}) scratch_free(p, st);
+    cudaStreamSynchronize(st);
+    return e;
+  }
   Staged sc, sm, ss;
   pcb_status e = stage_in(c, count * 2 * x->L * 4, st, &sc);
   if (!e) e = stage_out(m, count * x->L * 4, st, &sm);
@@ -2824,6 +2902,39 @@ pcb_status pcb_quantize_encrypt(pcb_ctx* x, const double* v, size_t count, doubl
   if (count == 0) return PCB_OK;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
+  if (count >= kPipeMin && !is_device_ptr(c)) {  // host ciphertexts: chunked, each chunk's copy beside the next's compute
+    const size_t WO = 2 * x->L, qw = fine ? 2 : 1;
+    const size_t chunk = ((count + kPipeChunks - 1) / kPipeChunks + 255) / 256 * 256;
+    HostPipe hp;
+    pcb_status e = hp.init(st);
+    uint32_t* dc[2] = {nullptr, nullptr};
+    for (int b = 0; b < 2 && !e; b++) e = scratch_alloc(chunk * WO * 4, (void**)&dc[b], st);
+    if (!e) e = cuda_check(cudaStreamSynchronize(st));
+    uint64_t tot[2] = {0, 0};
+    for (size_t i = 0, off = 0; off < count && !e; i++, off += chunk) {
+      const int b = (int)(i & 1);
+      const size_t cnt = std::min(chunk, count - off);
+      if (i >= 2) e = cuda_check(cudaStreamWaitEvent(st, hp.out[b], 0));  // dc[b]'s previous chunk is home
+      uint64_t cl[2] = {0, 0};
+      if (!e)  // device output: the call returns once the chunk is computed (its status check synchronises)
+        e = pcb_quantize_encrypt(x, v + off, cnt, z_min, z_max, delta, fine, r + off * x->L, use_crt, dc[b],
+                                 q_out ? q_out + off * qw : nullptr, cl, stream);
+      tot[0] += cl[0];
+      tot[1] += cl[1];
+      if (!e) e = cuda_check(cudaEventRecord(hp.comp[b], st));
+      if (!e) e = cuda_check(cudaStreamWaitEvent(hp.cout, hp.comp[b], 0));
+      if (!e) e = cuda_check(cudaMemcpyAsync(c + off * WO, dc[b], cnt * WO * 4, cudaMemcpyDeviceToHost, hp.cout));
+      if (!e) e = cuda_check(cudaEventRecord(hp.out[b], hp.cout));
+    }
+    if (cudaStreamSynchronize(hp.cout) != cudaSuccess && !e) e = PCB_E_CUDA;
+    for (void* p : {(void*)dc[0], (void*)dc[1]}) scratch_free(p, st);
+    cudaStreamSynchronize(st);
+    if (!e && clamps) {
+      clamps[0] = tot[0];
+      clamps[1] = tot[1];
+    }
+    return e;
+  }
   Staged sv, sr, sc, sq;
   unsigned long long* dclamps = nullptr;
   if (!use_crt) {  // public-key form: prep (quantize + checks) then n^2 encryption
