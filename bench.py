@@ -113,7 +113,7 @@ def run_admm(args, rank: int, world: int, local: int):
     from paper_2601_14980_b200 import paillier as P
 
     a, y = gen_problem_fast(512, 4096, 0.1, 1)
-    keys = P.keygen(P.Rng(KEY_SEED), 2048)
+    keys = P.keygen(P.Rng(KEY_SEED), 2048, device=local)
     # untimed iterations at the end: every timed iteration then also runs the offline half of a
     # later one (steady state), as in a long session
     iters = args.admm_warmup + args.admm_iters + ADMM.PRE_AHEAD_MAX
@@ -167,7 +167,7 @@ def run_admm_collab(args, rank: int, world: int, local: int):
     from paper_2601_14980_b200 import paillier as P
 
     a, y = gen_problem_fast(512, 4096, 0.1, 1)
-    keys = P.keygen(P.Rng(KEY_SEED), 2048)
+    keys = P.keygen(P.Rng(KEY_SEED), 2048, device=local)
     # one more warm-up iteration than the basic line: the collaborative step runs on three streams,
     # and the stream-ordered scratch pool grows over its first iterations
     wu = args.admm_warmup + 1
@@ -197,7 +197,7 @@ def run_admm_faithful(args, rank: int, world: int, local: int):
     from paper_2601_14980_b200 import paillier as P
 
     a, y = gen_problem_fast(512, 4096, 0.1, 1)
-    keys = P.keygen(P.Rng(KEY_SEED), 2048)
+    keys = P.keygen(P.Rng(KEY_SEED), 2048, device=local)
     iters = args.admm_warmup + args.admm_faithful_iters + 1  # + an untimed tail (the offline r^n runs 1 ahead)
     cfg = ADMM.SessionConfig(nodes=8, iters=iters)
     dev = torch.device(f"cuda:{local}")
@@ -261,7 +261,7 @@ def run_cfg5(args, rank: int, world: int, local: int):
     idx = torch.randperm(65536, device="cuda", generator=g)[:6554]
     x[idx] = torch.randn(6554, dtype=torch.float64, device="cuda", generator=g)
     y = a @ x
-    keys = P.keygen(P.Rng(KEY_SEED), 2048)
+    keys = P.keygen(P.Rng(KEY_SEED), 2048, device=local)
     iters = args.admm_warmup + args.cfg5_iters + ADMM.PRE_AHEAD_MAX
     cfg = ADMM.SessionConfig(nodes=64, iters=iters)
     group = dist.group.WORLD if world > 1 else None
@@ -615,7 +615,7 @@ def main() -> None:
     lib = L.lib()
     N = args.n
     zmin, zmax, delta = SPEC
-    kp = P.keygen(P.Rng(KEY_SEED), 2048)
+    kp = P.keygen(P.Rng(KEY_SEED), 2048, device=local)
     ph = P.Paillier(kp, device=local)
     # rank k encrypts values [k N, (k+1) N) of the one job-wide cfg2 stream with the matching slice
     # of the one sample_r(Rng(2)) stream: the N-rank job computes the 1-rank job's ciphertexts
