@@ -2293,15 +2293,39 @@ static pcb_status matvec_rnsx(pcb_ctx* x, const uint32_t* alpha, const uint64_t*
     }
     e = launch_rnsx_prog(md, g, nullptr, 0, rows * nch, nullptr, st, mm * g.nsteps);
   }
-  if (!e) {  // C
+  // C: the nch chunk partials of every row are first multiplied pairwise in a tree (one product per
+  // level, rows x cur/2 elements on all SMs) while their count is even, then alpha_i times the
+  // remaining ones -- instead of a chain of nch products on ceil(rows / 128) CTAs.  The product mod
+  // n^2 does not depend on the order, and the output conversion is canonical.
+  uint32_t* tbuf = nullptr;
+  int cur = nch;
+  if (!e && cur % 2 == 0 && cur > 1 && !getenv("PCB_MATVEC_CHAIN"))
+    e = scratch_alloc(rows * (size_t)(cur / 2) * REC * 4, (void**)&tbuf, st);
+  uint32_t *pin = g.part, *pnext = tbuf;
+  while (!e && tbuf && cur % 2 == 0 && cur > 1) {
+    const int nxt = cur / 2;
+    g.part = pin;
+    g.pout = pnext;
+    g.nparts = 2;  // element (row, j) of rows x nxt reads partials (row, 2j) and (row, 2j + 1)
+    g.nsteps = 0;
+    g.st[g.nsteps++] = S(kRsPart, 0, kRsPart, 1, kRpRec, 0);
+    e = launch_rnsx_prog(md, g, nullptr, 0, rows * (size_t)nxt, nullptr, st, mm);
+    std::swap(pin, pnext);
+    cur = nxt;
+  }
+  g.part = pin;
+  g.pout = nullptr;
+  g.nparts = cur;
+  if (!e) {  // alpha_i times the cur remaining partials of row i, out of Montgomery form
     g.nsteps = 0;
     g.st[g.nsteps++] = S(kRsConv, 0, kRsCvec, kRxR2N, kRpNone, 0);
-    for (int c = 0; c < nch; c++) g.st[g.nsteps++] = S(kRsKeep, 0, kRsPart, (uint8_t)c, kRpNone, 0);
+    for (int c = 0; c < cur; c++) g.st[g.nsteps++] = S(kRsKeep, 0, kRsPart, (uint8_t)c, kRpNone, 0);
     g.st[g.nsteps++] = S(kRsKeep, 0, kRsCvec, kRxOne, kRpOut, 0);
     e = launch_rnsx_prog(md, g, alpha, 2 * (int)x->L, rows, out, st, mm * g.nsteps);
   }
   scratch_free(g.mtab, st);
-  scratch_free(g.part, st);
+  scratch_free(pin, st);  // {pin, pnext} = the partials buffer and the tree buffer
+  scratch_free(pnext, st);
   return e;
 }
 

@@ -514,7 +514,7 @@ __device__ __forceinline__ void compute_role(const XArgs& P, Thr<C>& T, int mine
           }
           case kRpChain: vec_op(rec(G.mtab, ((size_t)el * G.nwin + stp.pa) * 64 + 1), 4, XB, XQ, 2); break;
           case kRpSelf: vec_op(rec(G.mtab, (size_t)el * 64 + stp.pa), 4, XB, XQ, 2); break;
-          case kRpRec: vec_op(rec(G.part, (size_t)el), 4, XB, XQ, 2); break;
+          case kRpRec: vec_op(rec(G.pout ? G.pout : G.part, (size_t)el), 4, XB, XQ, 2); break;
           default: break;
         }
       }

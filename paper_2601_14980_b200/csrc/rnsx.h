@@ -49,6 +49,7 @@ struct RxProg {
   int nsteps = 0;
   uint32_t* mtab = nullptr;       // RNS records
   uint32_t* part = nullptr;       // RNS records
+  uint32_t* pout = nullptr;       // kRpRec destination (null: part)
   const uint64_t* expo = nullptr; // rows x cols exponents (matvec)
   int cols = 0, nwin = 0, cc = 1, nch = 1, brows = 0, nparts = 1;
 };

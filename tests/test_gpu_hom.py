@@ -158,7 +158,7 @@ def test_matvec_reference_recurrence_64bit():
         ph.hom_matvec(alpha, expo, zv, 9)
 
 
-@pytest.mark.parametrize("idx,rows,cols", [(1, 17, 23), (2, 9, 40)])
+@pytest.mark.parametrize("idx,rows,cols", [(1, 17, 23), (2, 9, 40), (2, 33, 96)])  # 96: partial tree 6 -> 3
 def test_matvec_matches_bigint_and_reference(idx, rows, cols):
     kp = key(idx)
     pub = P.Paillier(P.PublicKey(kp.n, kp.key_bits))
