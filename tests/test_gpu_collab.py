@@ -279,3 +279,66 @@ def test_delegated_power_fermat_equals_generic(key2048):
     assert got[count - 4] == 0 and got[count - 3] == 0 and got[count - 2] == 1
     # an exponent that is not a multiple of p - 1 has no Fermat form
     assert share.fermat_factor(eps + 1) is None
+
+
+def test_decrypt_update_half_async_matches_sync_and_flags(key2048):
+    """pcb_decrypt_update_blocks_half_async, with the q side computed inside or handed over from
+    pcb_decrypt_half_q, == the synchronous pcb_decrypt_update_blocks_half (decrypt_with_half +
+    range gate + update, protocol.cpp:20-27, 488-511): same x / z / v, and the range failure lands in
+    the device flag instead of the return code."""
+    import ctypes as C
+
+    import torch
+
+    kp, _ = key2048
+    ph = P.Paillier(kp)
+    share = P.crt_share(kp)
+    lib = L.lib()
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    n, p, q = kp.n, kp.p, kp.q
+    eps = _lcm(p - 1, q - 1)
+    cols = 8
+    zmin, zmax, delta = -2.0, 2.0, 1e15
+    cap = delta * delta / (zmax - zmin) + float(cols) * delta * 2.0 * delta
+    lim = int(cap * 1.000001 + 4.0)
+    qs = [0, 12345, lim - (1 << 40), 99, lim + (1 << 50), 7, 1 << 127, 5]
+    r = ph.sample_r_batch(P.Rng(3), cols)
+    c = ph.encrypt_batch(torch.from_numpy(L.ints_to_limbs(qs, ph.L).view(np.int32)).cuda(), r)
+    W = 2 * ph.L
+    obf = eps * (1 + 4242 * n)  # an edge's obf_dec (protocol.cpp:352-353)
+    U = torch.from_numpy(np.tile(share.fermat_factor(obf), (cols, 1)).view(np.int32)).cuda()
+    px = torch.zeros((cols, W), dtype=torch.int32, device="cuda")
+    px[:, :share.S] = share.delegated_power_fermat_tensor(c, U)
+    yq = torch.empty((cols, ph.crt_half_words()), dtype=torch.int32, device="cuda")
+    assert lib.pcb_decrypt_half_q(ph._ctx, L.ptr(c), cols, L.ptr(yq), stream) == 0
+    rowsum = torch.full((cols,), 1000, dtype=torch.int64, device="cuda")
+    qz = torch.full((cols,), 10, dtype=torch.int64, device="cuda")
+    qn = torch.full((cols,), 20, dtype=torch.int64, device="cuda")
+    one = np.array([cols], np.uint32)
+    outs = []
+    for mode in ("sync", "async", "async_q"):
+        x = torch.full((cols,), 7.0, dtype=torch.float64, device="cuda")
+        z, vv = x.clone(), x.clone()
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        if mode == "sync":
+            rc = lib.pcb_decrypt_update_blocks_half(ph._ctx, 1, one.ctypes.data, L.ptr(c), L.ptr(px), L.ptr(rowsum),
+                                                    L.ptr(qz), L.ptr(qn), zmin, zmax, delta, 1.0, L.ptr(x), L.ptr(z),
+                                                    L.ptr(vv), None, stream)
+            assert rc == L.PCB_E_RANGE_UPDATE
+        else:
+            rc = lib.pcb_decrypt_update_blocks_half_async(
+                ph._ctx, 1, one.ctypes.data, L.ptr(c), L.ptr(px), L.ptr(yq) if mode == "async_q" else None,
+                L.ptr(rowsum), L.ptr(qz), L.ptr(qn), zmin, zmax, delta, 1.0, L.ptr(x), L.ptr(z), L.ptr(vv),
+                L.ptr(err), stream)
+            torch.cuda.synchronize()
+            assert rc == 0 and int(err.item()) == L.PCB_E_RANGE_UPDATE
+        outs.append((x.cpu(), z.cpu(), vv.cpu()))
+    for a_, b_, c_ in zip(*outs):
+        assert torch.equal(a_, b_) and torch.equal(a_, c_)
+    # the accepted rows were updated, the rejected ones (qs above the cap) kept 7.0
+    assert outs[0][0][0].item() != 7.0 and outs[0][0][4].item() == 7.0 and outs[0][0][6].item() == 7.0
+    # host pointers are refused by the asynchronous form
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    assert lib.pcb_decrypt_update_blocks_half_async(
+        ph._ctx, 1, one.ctypes.data, c.cpu().numpy().ctypes.data, L.ptr(px), None, L.ptr(rowsum), L.ptr(qz),
+        L.ptr(qn), zmin, zmax, delta, 1.0, L.ptr(x), L.ptr(z), L.ptr(vv), L.ptr(err), stream) != 0
