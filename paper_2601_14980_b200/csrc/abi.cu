@@ -1412,6 +1412,58 @@ pcb_status pcb_encrypt(pcb_ctx* x, const uint32_t* m, uint32_t m_limbs, const ui
   if (!x->has_prv && use_crt) return PCB_E_NO_PRIVATE;
   if (auto e = set_device(x)) return e;
   cudaStream_t st = (cudaStream_t)stream;
+  const bool m_dev = is_device_ptr(m), r_dev = is_device_ptr(r), c_dev = is_device_ptr(c);
+  if (count >= kPipeMin && (!m_dev || !r_dev || !c_dev)) {  // host buffers: chunked, copies beside the compute
+    const size_t WM = m_limbs, WR = x->L, WO = 2 * x->L;
+    const size_t chunk = ((count + kPipeChunks - 1) / kPipeChunks + 255) / 256 * 256;
+    HostPipe hp;
+    pcb_status e = hp.init(st);
+    uint32_t *dmv[2] = {nullptr, nullptr}, *drv[2] = {nullptr, nullptr}, *dcv[2] = {nullptr, nullptr};
+    int32_t* sall = nullptr;
+    for (int b = 0; b < 2 && !e; b++) {
+      if (!m_dev) e = scratch_alloc(chunk * WM * 4, (void**)&dmv[b], st);
+      if (!e && !r_dev) e = scratch_alloc(chunk * WR * 4, (void**)&drv[b], st);
+      if (!e && !c_dev) e = scratch_alloc(chunk * WO * 4, (void**)&dcv[b], st);
+    }
+    if (!e) e = scratch_alloc(count * 4, (void**)&sall, st);
+    if (!e) e = cuda_check(cudaStreamSynchronize(st));  // the scratch exists before the copy streams use it
+    for (size_t i = 0, off = 0; off < count && !e; i++, off += chunk) {
+      const int b = (int)(i & 1);
+      const size_t cnt = std::min(chunk, count - off);
+      const uint32_t* ms = m + off * WM;
+      const uint32_t* rs = r + off * WR;
+      uint32_t* cs = c + off * WO;
+      if (!m_dev || !r_dev) {
+        if (i >= 2) e = cuda_check(cudaStreamWaitEvent(hp.cin, hp.comp[b], 0));
+        if (!e && !m_dev) e = cuda_check(cudaMemcpyAsync(dmv[b], ms, cnt * WM * 4, cudaMemcpyHostToDevice, hp.cin));
+        if (!e && !r_dev) e = cuda_check(cudaMemcpyAsync(drv[b], rs, cnt * WR * 4, cudaMemcpyHostToDevice, hp.cin));
+        if (!e) e = cuda_check(cudaEventRecord(hp.in[b], hp.cin));
+        if (!e) e = cuda_check(cudaStreamWaitEvent(st, hp.in[b], 0));
+        if (!m_dev) ms = dmv[b];
+        if (!r_dev) rs = drv[b];
+      }
+      if (!c_dev) {
+        if (i >= 2 && !e) e = cuda_check(cudaStreamWaitEvent(st, hp.out[b], 0));
+        cs = dcv[b];
+      }
+      if (!e) e = pcb_encrypt(x, ms, m_limbs, rs, cnt, cs, use_crt, sall + off, stream);  // device: asynchronous
+      if (!e) e = cuda_check(cudaEventRecord(hp.comp[b], st));
+      if (!c_dev && !e) {
+        e = cuda_check(cudaStreamWaitEvent(hp.cout, hp.comp[b], 0));
+        if (!e) e = cuda_check(cudaMemcpyAsync(c + off * WO, dcv[b], cnt * WO * 4, cudaMemcpyDeviceToHost, hp.cout));
+        if (!e) e = cuda_check(cudaEventRecord(hp.out[b], hp.cout));
+      }
+    }
+    if (cudaStreamSynchronize(hp.cout) != cudaSuccess && !e) e = PCB_E_CUDA;
+    if (!e && status) e = cuda_check(cudaMemcpyAsync(status, sall, count * 4, cudaMemcpyDefault, st));
+    if (!e && !status) e = first_failure(sall, count, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && !e) e = PCB_E_CUDA;
+    for (int b = 0; b < 2; b++)
+      for (void* p : {(void*)dmv[b], (void*)drv[b], (void*)dcv[b]}) scratch_free(p, st);
+    scratch_free(sall, st);
+    cudaStreamSynchronize(st);
+    return e;
+  }
   Staged sm, sr, sc, ss;
   if (!x->has_prv) {  // public-key context: direct encryption at n^2
     pcb_status e = stage_in(m, count * m_limbs * 4, st, &sm);

@@ -94,3 +94,37 @@ def test_decrypt_host_buffers_equal_device_and_report_first_failure(setup):
     ok = np.ones(N, bool)
     ok[bad] = False
     assert torch.equal(hm[torch.from_numpy(ok)], md.cpu()[torch.from_numpy(ok)])
+
+
+def test_encrypt_host_buffers_equal_device_and_report_first_failure(setup):
+    """pcb_encrypt with host m / r / c (chunked) == the device path; a plaintext >= n in the second
+    chunk and an r = 0 in the fourth are reported per element, the status-less call returns the
+    earlier one's code."""
+    import torch
+
+    kp, ph, vals, r = setup
+    lib = L.lib()
+    W = 2 * ph.L
+    g = np.random.default_rng(8)
+    m = torch.zeros((N, ph.L), dtype=torch.int32)
+    m[:, 0] = torch.from_numpy(g.integers(0, 2**31, N).astype(np.int32))
+    m[:, 1] = torch.from_numpy(g.integers(0, 2**20, N).astype(np.int32))
+    cd = torch.empty((N, W), dtype=torch.int32, device="cuda")
+    assert lib.pcb_encrypt(ph._ctx, L.ptr(m.cuda()), ph.L, L.ptr(r), N, L.ptr(cd), 1, None, None) == 0
+    rh = r.cpu()
+    for pin in (True, False):
+        mh, rr, hc = m.clone(), rh.clone(), torch.zeros((N, W), dtype=torch.int32)
+        if pin:
+            mh, rr, hc = mh.pin_memory(), rr.pin_memory(), hc.pin_memory()
+        st = torch.zeros(N, dtype=torch.int32)
+        assert lib.pcb_encrypt(ph._ctx, L.ptr(mh), ph.L, L.ptr(rr), N, L.ptr(hc), 1, L.ptr(st), None) == 0
+        assert torch.equal(hc, cd.cpu()) and int(st.abs().sum()) == 0, pin
+    bad_m, bad_r = N // 4 + 11, 3 * (N // 4) + 101
+    mh, rr, hc = m.clone(), rh.clone(), torch.zeros((N, W), dtype=torch.int32)
+    mh[bad_m] = torch.from_numpy(L.int_to_limbs(kp.n, ph.L).view(np.int32).copy())
+    rr[bad_r] = 0
+    st = torch.zeros(N, dtype=torch.int32)
+    assert lib.pcb_encrypt(ph._ctx, L.ptr(mh), ph.L, L.ptr(rr), N, L.ptr(hc), 1, L.ptr(st), None) == 0
+    assert sorted(np.nonzero(st.numpy())[0].tolist()) == [bad_m, bad_r]
+    rc = lib.pcb_encrypt(ph._ctx, L.ptr(mh), ph.L, L.ptr(rr), N, L.ptr(hc), 1, None, None)
+    assert rc == int(st[bad_m]) and rc != 0 and int(st[bad_r]) != 0
