@@ -1075,13 +1075,20 @@ class FaithfulGpuBackend:
             _raise_for(self.lib.pcb_ctx_set_priority(self.pre._ctx, 0), "priority")
             _raise_for(self.lib.pcb_ctx_set_priority(self.master._ctx, 1), "priority")
             self.pstream = torch.cuda.Stream(device=self.device, priority=0)
-            self.rn = [torch.empty((2 * n, self.width), dtype=torch.int32, device=self.device) for _ in range(2)]
-            self.st_pre = [torch.zeros(2 * n, dtype=torch.int32, device=self.device) for _ in range(2)]
+            # as EncryptedSession: two iterations ahead, behind the edge step, while the master's
+            # decryption of the n rows leaves SMs idle (pre_ahead), else one ahead
+            self.pre_ahead = pre_ahead(n, torch.cuda.get_device_properties(self.device).multi_processor_count)
+            self.nslot = self.pre_ahead + 1
+            self.rn = [torch.empty((2 * n, self.width), dtype=torch.int32, device=self.device)
+                       for _ in range(self.nslot)]
+            self.st_pre = [torch.zeros(2 * n, dtype=torch.int32, device=self.device) for _ in range(self.nslot)]
             self.pre_bad = torch.zeros((), dtype=torch.int32, device=self.device)
             self.m0 = torch.zeros((2 * n, 1), dtype=torch.int32, device=self.device)
-            self.rn_ready = [torch.cuda.Event() for _ in range(2)]
+            self.rn_ready = [torch.cuda.Event() for _ in range(self.nslot)]
             self.enc_done = torch.cuda.Event()
             self.enc_done.record(torch.cuda.current_stream(self.device))
+            self.edge_done = None  # recorded when the edge step's updates reach the master
+            self.t_enc = 0
 
     def master_encrypt(self, z, v, t):
         import torch
@@ -1099,17 +1106,20 @@ class FaithfulGpuBackend:
             _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(rn), vin.numel(), L.ptr(ct),
                                                L.ptr(self.st_enc), st), "enc_state")
         else:
-            slot = t % 2
+            slot = t % self.nslot
+            self.t_enc = t
             if t == 0:
                 self._precompute(slot)
+                if self.pre_ahead == 2 and self.cfg.iters > 1:
+                    self._precompute(1)
             cur = torch.cuda.current_stream(self.device)
             cur.wait_event(self.rn_ready[slot])
             self.pre_bad |= self.st_pre[slot].ne(0).any().to(torch.int32)
             _raise_for(self.lib.pcb_encrypt_rn(self.master._ctx, L.ptr(q), 2, L.ptr(self.rn[slot]), vin.numel(),
                                                L.ptr(ct), L.ptr(self.st_enc), st), "enc_state")
             self.enc_done.record(cur)
-            if t + 1 < self.cfg.iters:
-                self._precompute(1 - slot)
+            if self.pre_ahead == 1 and t + 1 < self.cfg.iters:
+                self._precompute((t + 1) % self.nslot)
         return ct, q
 
     def _precompute(self, slot):
@@ -1118,7 +1128,9 @@ class FaithfulGpuBackend:
         import torch
 
         ps = self.pstream
-        ps.wait_event(self.enc_done)  # the slot was last read by the previous online encryption
+        ps.wait_event(self.enc_done)  # the slot was last read by an earlier online encryption
+        if self.edge_done is not None:
+            ps.wait_event(self.edge_done)
         with torch.cuda.stream(ps):
             st = C.c_void_p(ps.cuda_stream)
             s_ = C.c_uint64(self.rng_r.state)
@@ -1158,7 +1170,16 @@ class FaithfulGpuBackend:
         res.edges = RoleStats(fe, he, 0)
 
     def master_update(self, upd, q, rowsum, sizes, spec, cfg, x, z, v):
+        import torch
+
         n = self.n
+        if getattr(self, "pre_ahead", 1) == 2 and self.t_enc + 2 < cfg.iters:
+            t = self.t_enc
+            # the updates are here: queue iteration t+2's offline r^n beside the decryption
+            if self.edge_done is None:
+                self.edge_done = torch.cuda.Event()
+            self.edge_done.record(torch.cuda.current_stream(self.device))
+            self._precompute((t + 2) % self.nslot)
         if not cfg.use_crt:  # decrypt_vec(use_crt = false): one full each (paillier.cpp:345-350)
             self.adj_full += n
             self.adj_half -= 2 * n
