@@ -1173,13 +1173,11 @@ class FaithfulGpuBackend:
         import torch
 
         n = self.n
-        if getattr(self, "pre_ahead", 1) == 2 and self.t_enc + 2 < cfg.iters:
-            t = self.t_enc
-            # the updates are here: queue iteration t+2's offline r^n beside the decryption
+        ahead2 = getattr(self, "pre_ahead", 1) == 2 and self.t_enc + 2 < cfg.iters
+        if ahead2:  # the updates are here: iteration t+2's offline r^n goes beside the decryption
             if self.edge_done is None:
                 self.edge_done = torch.cuda.Event()
             self.edge_done.record(torch.cuda.current_stream(self.device))
-            self._precompute((t + 2) % self.nslot)
         if not cfg.use_crt:  # decrypt_vec(use_crt = false): one full each (paillier.cpp:345-350)
             self.adj_full += n
             self.adj_half -= 2 * n
@@ -1188,6 +1186,8 @@ class FaithfulGpuBackend:
             self.master._ctx, len(sz), sz.ctypes.data, L.ptr(upd), L.ptr(rowsum), L.ptr(q[:n]), L.ptr(q[n:]),
             spec[0], spec[1], spec[2], self.kappa, L.ptr(x), L.ptr(z), L.ptr(v), L.ptr(self.err), self._st()),
             "master update")
+        if ahead2:  # launched after the decryption, so its CTAs reach the SMs first
+            self._precompute((self.t_enc + 2) % self.nslot)
 
     def check_iteration(self, t):
         code = int(self.err.item())
